@@ -1,0 +1,184 @@
+/*
+ * sparsekv_b200.h -- C ABI of the B200 (sm_100a) LServe sparse-attention hot path.
+ *
+ * The reference (`sparsekv`, /root/reference/pkg/src/sparsekv) is a pure
+ * Python/numpy package with no FFI; its drop-in boundary is the Python API
+ * in __init__.py:23-56.  This header is the native layer *beneath* that API:
+ * the host package `paper_2502_14866_b200` (same names, same argument
+ * meaning and errors as the reference) binds these entry points with
+ * ctypes.  Each entry point cites the reference computation it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Every pointer argument documented as
+ *    "device" is a CUDA device pointer; `stream` is a cudaStream_t (NULL =
+ *    legacy default stream).  All calls are asynchronous and stream-ordered.
+ *  - The library never allocates device memory: callers pass buffers and
+ *    workspaces (the required workspace size is returned by the *_workspace
+ *    query functions).
+ *  - Return value: SK_OK (0) or a negative status; sk_last_error() returns
+ *    a thread-local message for the last failure.
+ *  - A "stream" of the KV store (not to be confused with a CUDA stream) is
+ *    one (sequence, KV head) pair: index s = seq * n_kv_heads + kv_head.
+ */
+#ifndef SPARSEKV_B200_H
+#define SPARSEKV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SK_OK 0
+#define SK_EINVAL (-1)       /* invalid argument / shape -> ValueError */
+#define SK_ECUDA (-2)        /* CUDA launch or runtime error -> RuntimeError */
+#define SK_EUNSUPPORTED (-3) /* valid but unsupported on this build/device */
+
+#define SK_F16 0
+#define SK_BF16 1
+#define SK_F32 2
+
+#define SK_KIND_DENSE 0     /* dense pool: keeps every page, carries key stats */
+#define SK_KIND_STREAMING 1 /* streaming pool: keeps sink + local pages only */
+
+/*
+ * Paged KV store of one attention layer (possibly many sequences).
+ * Replaces cache.py:143-329 (HeadPages / TwoWayCache / PhysicalPage /
+ * PageTable / PageStats) with device-resident pools.
+ *
+ * Arena slot layout (slot_bytes = sk_slot_bytes(...)):
+ *   [0, P*R)        K codes, one row of R bytes per token
+ *   [P*R, 2*P*R)    V codes
+ *   [2*P*R, +8*D)   bits>0 only: k_lo[D], k_hi[D], v_lo[D], v_hi[D] in `dtype`
+ * where R = D/2 (bits<=4, two codes per byte, channel 2j in the low nibble
+ * of byte j), D (5<=bits<=8, one byte per code) or 2*D (bits=0: raw values).
+ * scale = (hi-lo)/(2^bits-1) (1 where hi==lo) and zero = lo reproduce the
+ * reference's per-page, per-channel quantiser (cache.py:20-51) exactly,
+ * because lo/hi are min/max of values that are exact in `dtype`.
+ */
+typedef struct sk_pool {
+  int32_t dtype;             /* SK_F16 or SK_BF16: raw K/V, bounds, stats, staging */
+  int32_t head_dim;          /* D (padded: 64 or 128) */
+  int32_t page_size;         /* physical page P (tokens), <= 128 */
+  int32_t logical_page;      /* logical page L, divides P */
+  int32_t bits;              /* 0 = raw pages, 2..8 = KV-b codes */
+  int32_t max_pages;         /* page-table row width per stream */
+  int32_t sink;              /* streaming window: sink pages (heads.py:107-125) */
+  int32_t local;             /* streaming window: local pages */
+  int64_t slot_bytes;        /* bytes per arena slot */
+  void* arena;               /* device [n_slots][slot_bytes] */
+  const int32_t* page_table; /* device [n_streams][max_pages]: page index -> arena slot (-1 none) */
+  void* stats;               /* device [n_streams][max_pages*P/L][2][D]: (k_min, k_max) per logical page */
+  void* staging;             /* device [n_streams][2][P][D]: raw K, V of each stream's open page */
+  const uint8_t* kind;       /* device [n_streams]: SK_KIND_DENSE / SK_KIND_STREAMING */
+} sk_pool;
+
+/* Library identity and health. */
+const char* sk_version(void);
+const char* sk_last_error(void);
+/* 1 if device `dev` is an sm_100 part this build can run on, else 0. */
+int sk_device_supported(int dev);
+/* Bytes per arena slot for a pool geometry. */
+int64_t sk_slot_bytes(int32_t head_dim, int32_t page_size, int32_t bits, int32_t dtype);
+
+/*
+ * K1 -- append m tokens to every stream (bulk prefill ingest or one decode
+ * token).  Replaces HeadPages.append -> _rebuild_open_page -> quantize_page
+ * + PageStats.from_keys -> _evict_outside_window (cache.py:189-261).
+ * For each stream s and each page touched by tokens [tokens[s], tokens[s]+m):
+ * rebuilds the page from the raw open-page staging plus the new tokens,
+ * recomputes lo/hi, codes (fp64 round-half-even, bit-exact with numpy) and,
+ * for dense streams, the logical-page (k_min, k_max); stores the raw tail
+ * of a partial last page in staging.  Streaming-pool pages that the append
+ * would evict are skipped.  Afterwards tokens[s] += m.
+ *   k_src/v_src: device, element (s, t, c) at src + s*src_stream_stride +
+ *                t*src_token_stride + c, in pool->dtype.
+ *   tokens:      device [n_streams] token counts before the append (updated).
+ *   max_pages_touched: upper bound on pages one stream touches (host-known).
+ * Caller guarantees page_table[s][p] is set for every touched page p.
+ */
+int sk_append_pages(const sk_pool* pool, int32_t n_streams, const void* k_src, const void* v_src,
+                    int64_t src_stream_stride, int64_t src_token_stride, int32_t* tokens, int32_t m_tokens,
+                    int32_t max_pages_touched, void* stream);
+
+/*
+ * K2 -- hierarchical page selection (Eq. 2).  Replaces
+ * score_pages / select_pages / pinned_pages (selector.py:39-108) and the
+ * call site engine.py:237-255.  For every stream with invoke[s] != 0 and a
+ * non-zero retrieval row mask: scores every logical page in fp64 as
+ * sum_c max(q_c*kmax_c, q_c*kmin_c), takes the max over the retrieval rows
+ * and over the logical pages of each physical page, then selects
+ * K = budget_pages pages: all pages if K >= n; the pins {0, n-2, n-1} if
+ * K <= |pins|; else pins + the best K-|pins| others ordered by
+ * (score desc, page index asc).  Output is ascending.
+ *   q:         device; row r of stream s at q + s*q_stream_stride + r*q_row_stride.
+ *   row_mask:  device [n_streams] bit r set = group row r is a retrieval row.
+ *   tokens:    device [n_streams] tokens currently in each stream.
+ *   invoke:    device [n_streams] (NULL = all).
+ *   sel_out:   device [n_streams][sel_stride] ascending page indices.
+ *   sel_count: device [n_streams].
+ *   max_pages_hint: >= ceil(max tokens / P), sizes the grid.
+ */
+int64_t sk_select_workspace(int32_t n_streams, int32_t max_pages);
+int sk_select_pages(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
+                    int64_t q_stream_stride, int64_t q_row_stride, const uint32_t* row_mask,
+                    const int32_t* tokens, const uint8_t* invoke, int32_t budget_pages, int32_t max_pages_hint,
+                    int32_t* sel_out, int32_t* sel_count, int32_t sel_stride, void* workspace,
+                    int64_t workspace_bytes, void* stream);
+
+/*
+ * K3 -- split-KV decode attention over the selected pages.  Replaces the
+ * per-head page loop of Engine.decode_step (engine.py:257-281) with
+ * PhysicalPage.dequantize (cache.py:97-102) and merge_block
+ * (attn.py:191-229).  Per stream, group row r attends: the stream's
+ * selection (retrieval rows) or the sink+local window of the current page
+ * count (streaming rows), then the raw new token in-register.  Pages are
+ * dequantised on the fly; splits are merged with log-sum-exp.  If
+ * fuse_append != 0 the last CTA of each stream then appends k_new/v_new
+ * (K1 semantics, one token) and increments tokens[s].
+ *   out: element (s, r, c) at out + s*out_stream_stride + r*out_row_stride + c, type out_dtype.
+ */
+int64_t sk_decode_workspace(int32_t n_streams, int32_t group_rows, int32_t head_dim, int32_t max_splits);
+int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
+                   int64_t q_stream_stride, int64_t q_row_stride, const void* k_new, const void* v_new,
+                   int64_t new_stream_stride, const uint32_t* row_mask, const int32_t* sel,
+                   const int32_t* sel_count, int32_t sel_stride, int32_t* tokens, float softmax_scale,
+                   void* out, int64_t out_stream_stride, int64_t out_row_stride, int32_t out_dtype,
+                   int32_t pages_per_split, int32_t max_splits, int32_t fuse_append, void* workspace,
+                   int64_t workspace_bytes, void* stream);
+
+/*
+ * K4 -- block-sparse causal prefill attention on tcgen05 tensor cores.
+ * Replaces blockwise_attention (attn.py:245-324) driven by Engine.prefill's
+ * schedules (engine.py:152-168).  q [n_q][n_heads][D], k/v [n_kv][n_kv_heads][D]
+ * token-major (device, `dtype`), out like q.  Query row i sees key columns
+ * <= n_kv - n_q + i.  Each work item is one 128-row query block of one head
+ * (two of the reference's 64-row query tiles) and a list of segments of
+ * consecutive 64-key blocks; the host builds items and segments from the
+ * per-(head, query tile) schedules (the paper's block iterator,
+ * PAPER.md:296-297) and orders items heaviest first.
+ *
+ * Segment = 3 x uint32: { first_block, count | flags << 24, mask_base } with
+ *   flags bit 0: query rows [0,64) of the block attend these key blocks
+ *   flags bit 1: query rows [64,128) attend them
+ *   flags bit 2: apply the element-wise causal mask (column > row position)
+ *   flags bit 3: explicit per-row column masks: block first_block+i uses
+ *                row_masks[(mask_base + i) * 128 + row] (bit c = column c
+ *                allowed; generic tile sizes).
+ */
+typedef struct sk_prefill_item {
+  int32_t head;      /* query head */
+  int32_t row0;      /* first query row of the 128-row block */
+  int32_t seg_begin; /* first segment (index into segs, in units of segments) */
+  int32_t seg_count; /* number of segments */
+} sk_prefill_item;
+
+int sk_prefill_attn(int32_t dtype, const void* q, const void* k, const void* v, void* out, int32_t n_q,
+                    int32_t n_kv, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, float softmax_scale,
+                    const sk_prefill_item* items, int32_t n_items, const uint32_t* segs,
+                    const uint64_t* row_masks, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSEKV_B200_H */

@@ -1,0 +1,385 @@
+// K4 -- block-sparse causal prefill attention, tcgen05 + TMEM + TMA (sm_100a).
+//
+// Replaces blockwise_attention (reference attn.py:245-324) as driven by
+// Engine.prefill (engine.py:152-168): every (head, 64-row query tile) visits
+// only its scheduled 64-key tiles -- range(diag+1) for retrieval heads, the
+// sink + local Lambda window for streaming heads -- with the element-wise
+// causal mask on tiles that cross the diagonal (attn.py:315-319) and an
+// online softmax over the visited tiles (attn.py:191-229).
+//
+// One CTA = one 128-row query block of one head (two reference query tiles;
+// per-64-row "half" flags keep their schedules distinct).  Warp roles:
+//   warp 0      TMA producer: Q once, then K/V 64-key blocks into a
+//               NS-stage ring (SWIZZLE_128B, mbarrier complete_tx)
+//   warp 1      MMA issuer (one elected thread): S_j = Q K_j^T into a
+//               double-buffered TMEM tile (M=128, N=64, K=D), and
+//               O += P_j V_j (M=128, N=D, K=64; V is an MN-major operand)
+//   warps 2..5  softmax: one thread per query row reads S from TMEM
+//               (tcgen05.ld 32x32b), masks, exp2, writes P (fp16/bf16)
+//               into a swizzled K-major smem tile for the PV MMA; O is
+//               rescaled in TMEM only when the running max grows by more
+//               than 2^8 (exact: the stale max is a shared reference point)
+// S_{j+1} is issued before PV_j so the tensor core overlaps the softmax.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
+
+#include "sk_common.cuh"
+#include "sk_sm100.cuh"
+
+namespace sk {
+namespace {
+
+constexpr int kNS = 3;            // K/V pipeline stages
+constexpr int kPfThreads = 192;   // 6 warps
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+template <int D>
+struct PfSmem {
+  static constexpr int NC = D / 64;  // 128-byte column chunks
+  alignas(1024) uint8_t q[NC][128 * 128];
+  alignas(1024) uint8_t kv[kNS][2][NC][64 * 128];
+  alignas(1024) uint8_t p[2][128 * 128];
+  uint64_t q_full;
+  uint64_t kv_full[kNS];
+  uint64_t kv_empty[kNS];
+  uint64_t s_full[2];
+  uint64_t p_full[2];
+  uint64_t p_empty[2];
+  uint64_t o_done;
+  uint32_t tmem_base;
+};
+
+struct PfParams {
+  void* out;
+  int n_q, n_kv, n_heads, n_kv_heads, group;
+  float scale_log2;
+  const sk_prefill_item* items;
+  const uint32_t* segs;
+  const uint64_t* row_masks;
+};
+
+// Walks an item's segments block by block.
+struct SegWalk {
+  const uint32_t* segs;
+  int seg, seg_end, i;
+  uint32_t first, count, flags, mask_base;
+  __device__ SegWalk(const uint32_t* s, int b, int n) : segs(s), seg(b), seg_end(b + n), i(0) { load(); }
+  __device__ void load() {
+    if (seg < seg_end) {
+      first = segs[3 * seg];
+      uint32_t w = segs[3 * seg + 1];
+      count = w & 0xFFFFFFu;
+      flags = w >> 24;
+      mask_base = segs[3 * seg + 2];
+    } else {
+      count = 0;
+    }
+  }
+  __device__ bool done() const { return seg >= seg_end; }
+  __device__ int block() const { return int(first) + i; }
+  __device__ void next() {
+    if (++i >= int(count)) {
+      i = 0;
+      ++seg;
+      load();
+    }
+  }
+};
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kPfThreads, 1)
+    prefill_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                   const __grid_constant__ CUtensorMap tv, const PfParams prm) {
+  using Sm = PfSmem<D>;
+  constexpr int NC = Sm::NC;
+  constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+  constexpr uint32_t kTmemCols = 256;  // S[2] (2 x 64) + O (D <= 128)
+  constexpr uint32_t kOCol = 128;
+  extern __shared__ uint8_t smem_raw[];
+  Sm& sm = *reinterpret_cast<Sm*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+  const int warp = warp_id_uniform(), lane = threadIdx.x & 31;
+  const sk_prefill_item item = prm.items[blockIdx.x];
+  const int kvh = item.head / prm.group;
+  int n_blocks = 0;
+  for (int sgi = 0; sgi < item.seg_count; ++sgi) n_blocks += prm.segs[3 * (item.seg_begin + sgi) + 1] & 0xFFFFFFu;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.q_full, 1);
+    for (int i = 0; i < kNS; ++i) {
+      mbar_init(&sm.kv_full[i], 1);
+      mbar_init(&sm.kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.s_full[i], 1);
+      mbar_init(&sm.p_full[i], 4);
+      mbar_init(&sm.p_empty[i], 1);
+    }
+    mbar_init(&sm.o_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------ TMA producer ------------------------------
+    if (elect_one()) {
+      tma_prefetch_desc(&tq);
+      tma_prefetch_desc(&tk);
+      tma_prefetch_desc(&tv);
+      mbar_arrive_expect_tx(&sm.q_full, NC * 128 * 128);
+      for (int c = 0; c < NC; ++c) tma_load_3d(sm.q[c], &tq, &sm.q_full, 64 * c, item.head, item.row0);
+      int j = 0;
+      for (SegWalk w(prm.segs, item.seg_begin, item.seg_count); !w.done(); w.next(), ++j) {
+        const int st = j % kNS;
+        if (j >= kNS) mbar_wait(&sm.kv_empty[st], ((j / kNS) - 1) & 1);
+        mbar_arrive_expect_tx(&sm.kv_full[st], 2 * NC * 64 * 128);
+        const int key0 = w.block() * 64;
+        for (int c = 0; c < NC; ++c) {
+          tma_load_3d(sm.kv[st][0][c], &tk, &sm.kv_full[st], 64 * c, kvh, key0);
+          tma_load_3d(sm.kv[st][1][c], &tv, &sm.kv_full[st], 64 * c, kvh, key0);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------ MMA issuer --------------------------------
+    constexpr uint32_t idesc_s = make_idesc_f16(128, 64, kBF16, false, false);
+    constexpr uint32_t idesc_o = make_idesc_f16(128, D, kBF16, false, true);
+    mbar_wait(&sm.q_full, 0);
+    tc_fence_after();
+    auto issue_s = [&](int jj) {
+      const int st = jj % kNS;
+      mbar_wait(&sm.kv_full[st], (jj / kNS) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          uint64_t a = make_sdesc_sw128(smem_u32(sm.q[kk / 4]) + (kk % 4) * 32, 16, 1024);
+          uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][0][kk / 4]) + (kk % 4) * 32, 16, 1024);
+          mma_f16_ss(tmem + (jj & 1) * 64, a, b, idesc_s, kk > 0);
+        }
+        mma_commit(&sm.s_full[jj & 1]);
+      }
+      __syncwarp();
+    };
+    if (n_blocks > 0) issue_s(0);
+    for (int j = 0; j < n_blocks; ++j) {
+      if (j + 1 < n_blocks) issue_s(j + 1);
+      mbar_wait(&sm.p_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const int st = j % kNS;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          uint64_t a = make_sdesc_sw128(smem_u32(sm.p[j & 1]) + kk * 32, 16, 1024);
+          uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][1][0]) + kk * 2048, 64 * 128, 1024);
+          mma_f16_ss(tmem + kOCol, a, b, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&sm.kv_empty[st]);
+        mma_commit(&sm.p_empty[j & 1]);
+        mma_commit(&sm.o_done);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------ softmax -----------------------------------
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
+    const int pos = item.row0 + row + (prm.n_kv - prm.n_q);
+    const uint32_t half_bit = row < 64 ? 1u : 2u;
+    const float sl2 = prm.scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;
+    int j = 0;
+    for (SegWalk w(prm.segs, item.seg_begin, item.seg_count); !w.done(); w.next(), ++j) {
+      mbar_wait(&sm.s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      float s[64];
+#pragma unroll
+      for (int c = 0; c < 64; c += 32) {
+        uint32_t r[32];
+        tmem_ld_x32(trow + (j & 1) * 64 + c, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(r[i]);
+      }
+      const uint32_t fl = w.flags;
+      const bool active = fl & half_bit;
+      const int col0 = w.block() * 64;
+      uint64_t emask = ~0ull;
+      if (fl & 8u) emask = prm.row_masks[(int64_t)(w.mask_base + w.i) * 128 + row];
+      const int lim = (fl & 4u) ? pos - col0 : 64;  // columns c <= lim visible
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        bool ok = active && i <= lim && ((emask >> i) & 1ull);
+        s[i] = ok ? s[i] * sl2 : -INFINITY;
+        mx = fmaxf(mx, s[i]);
+      }
+      // lazy rescale: only when the max grows by more than 2^threshold
+      float m_new = fmaxf(m_run, mx);
+      bool need = (m_run != -INFINITY) && (m_new > m_run + kRescaleThreshold);
+      if (m_run == -INFINITY) m_run = m_new;
+      if (__any_sync(0xffffffffu, need)) {
+        if (j > 0) mbar_wait(&sm.o_done, (j - 1) & 1);  // PV_{j-1} landed in O
+        tc_fence_after();
+        const float alpha = need ? exp2f(m_run - m_new) : 1.f;
+#pragma unroll
+        for (int c = 0; c < D; c += 16) {
+          uint32_t r[16];
+          tmem_ld_x16(trow + kOCol + c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          tmem_st_x16(trow + kOCol + c, r);
+        }
+        tmem_wait_st();
+        if (need) {
+          l_run *= alpha;
+          m_run = m_new;
+        }
+      }
+      const float shift = m_run == -INFINITY ? 0.f : m_run;
+      float rs = 0.f;
+      uint32_t pk[32];
+#pragma unroll
+      for (int i = 0; i < 64; i += 2) {
+        float p0 = exp2f(s[i] - shift), p1 = exp2f(s[i + 1] - shift);
+        rs += p0 + p1;
+        pk[i / 2] = kBF16 ? pack_bf162(p0, p1) : pack_half2(p0, p1);
+      }
+      l_run += rs;
+      if (j >= 2) mbar_wait(&sm.p_empty[j & 1], ((j >> 1) - 1) & 1);
+      uint8_t* prow = sm.p[j & 1] + row * 128;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        uint4 v = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+        *reinterpret_cast<uint4*>(prow + ((ch ^ (row & 7)) << 4)) = v;
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.p_full[j & 1]);
+    }
+    // epilogue: O / l -> out
+    if (n_blocks > 0) {
+      mbar_wait(&sm.o_done, (n_blocks - 1) & 1);
+      tc_fence_after();
+    }
+    const int grow = item.row0 + row;
+    const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
+    T* orow = reinterpret_cast<T*>(prm.out) + ((int64_t)grow * prm.n_heads + item.head) * D;
+#pragma unroll
+    for (int c = 0; c < D; c += 16) {
+      uint32_t r[16];
+      tmem_ld_x16(trow + kOCol + c, r);
+      tmem_wait_ld();
+      uint32_t pk[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float a = __uint_as_float(r[2 * i]) * inv_l, b = __uint_as_float(r[2 * i + 1]) * inv_l;
+        pk[i] = kBF16 ? pack_bf162(a, b) : pack_half2(a, b);
+      }
+      if (grow < prm.n_q) {
+        *reinterpret_cast<uint4*>(orow + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(orow + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 3-D map over a token-major [rows][heads][D] tensor; box = 64 channels x 1 head x box_rows.
+int make_map(CUtensorMap* m, const void* base, int dtype, int D, int heads, int rows, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return SK_ECUDA;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)heads, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)heads * D * 2};
+  cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, dtype == SK_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+                  const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return SK_ECUDA;
+  }
+  return SK_OK;
+}
+
+template <typename T, int D>
+int launch_prefill(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const PfParams& prm,
+                   int n_items, cudaStream_t st) {
+  size_t smem = sizeof(PfSmem<D>) + 1024;
+  auto kern = prefill_kernel<T, D>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<n_items, kPfThreads, smem, st>>>(tq, tk, tv, prm);
+  SK_CHECK_LAUNCH("prefill_kernel");
+  return SK_OK;
+}
+
+}  // namespace
+}  // namespace sk
+
+extern "C" int sk_prefill_attn(int32_t dtype, const void* q, const void* k, const void* v, void* out, int32_t n_q,
+                               int32_t n_kv, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
+                               float softmax_scale, const sk_prefill_item* items, int32_t n_items,
+                               const uint32_t* segs, const uint64_t* row_masks, void* stream) {
+  using namespace sk;
+  SK_CHECK_ARG(dtype == SK_F16 || dtype == SK_BF16, "prefill: dtype must be f16 or bf16");
+  SK_CHECK_ARG(head_dim == 64 || head_dim == 128, "prefill: head_dim must be 64 or 128 (pad smaller dims)");
+  SK_CHECK_ARG(n_q >= 1 && n_kv >= n_q, "prefill: history must cover queries");
+  SK_CHECK_ARG(n_heads >= 1 && n_kv_heads >= 1 && n_heads % n_kv_heads == 0,
+               "prefill: query head count is not a multiple of KV head count");
+  SK_CHECK_ARG(q && k && v && out && items && segs, "prefill: NULL pointer");
+  SK_CHECK_ARG((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) %
+                       16 == 0,
+               "prefill: q/k/v must be 16-byte aligned");
+  if (n_items == 0) return SK_OK;
+  CUtensorMap tq, tk, tv;
+  int rc;
+  if ((rc = make_map(&tq, q, dtype, head_dim, n_heads, n_q, 128))) return rc;
+  if ((rc = make_map(&tk, k, dtype, head_dim, n_kv_heads, n_kv, 64))) return rc;
+  if ((rc = make_map(&tv, v, dtype, head_dim, n_kv_heads, n_kv, 64))) return rc;
+  PfParams prm;
+  prm.out = out;
+  prm.n_q = n_q;
+  prm.n_kv = n_kv;
+  prm.n_heads = n_heads;
+  prm.n_kv_heads = n_kv_heads;
+  prm.group = n_heads / n_kv_heads;
+  prm.scale_log2 = softmax_scale * 1.4426950408889634f;
+  prm.items = items;
+  prm.segs = segs;
+  prm.row_masks = row_masks;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == SK_F16)
+    return head_dim == 128 ? launch_prefill<__half, 128>(tq, tk, tv, prm, n_items, st)
+                           : launch_prefill<__half, 64>(tq, tk, tv, prm, n_items, st);
+  return head_dim == 128 ? launch_prefill<__nv_bfloat16, 128>(tq, tk, tv, prm, n_items, st)
+                         : launch_prefill<__nv_bfloat16, 64>(tq, tk, tv, prm, n_items, st);
+}
