@@ -58,6 +58,15 @@ def to_device(x, dtype: torch.dtype, device: torch.device, pad_to: int | None = 
     return t.contiguous()
 
 
+def h2d(a, device: torch.device, dtype=None) -> torch.Tensor:
+    """Small host array -> device without a blocking pageable copy (pinned,
+    caching host allocator, stream-ordered)."""
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.pin_memory().to(device, non_blocking=True)
+
+
 def stream_ptr(device: torch.device):
     return torch.cuda.current_stream(device).cuda_stream
 

@@ -49,6 +49,8 @@ class Workload:
         if q.shape[1] % k.shape[1] != 0:
             raise ValueError(f"query head count {q.shape[1]} is not a multiple of KV head count {k.shape[1]}")
         for name, t in (("q", q), ("k", k), ("v", v)):
+            if _device.is_torch(t) and not t.is_cuda:
+                continue  # host torch tensors are checked on the device after upload (Engine / blockwise)
             finite = bool(torch.isfinite(t).all()) if _device.is_torch(t) else bool(np.isfinite(t).all())
             if not finite:
                 raise ValueError(f"non-finite values in {name}")
@@ -204,9 +206,9 @@ class PrefillPlan:
     def device_arrays(self, device):
         key = str(device)
         if key not in self._dev:
-            it = torch.from_numpy(self.items_np).to(device)
-            sg = torch.from_numpy(self.segs_np.view(np.int32)).to(device)
-            mk = torch.from_numpy(self.masks_np.view(np.int64)).to(device) if self.masks_np is not None else None
+            it = _device.h2d(self.items_np, device)
+            sg = _device.h2d(self.segs_np.view(np.int32), device)
+            mk = _device.h2d(self.masks_np.view(np.int64), device) if self.masks_np is not None else None
             self._dev[key] = (it, sg, mk)
         return self._dev[key]
 
@@ -308,6 +310,15 @@ def validate_schedules(schedules: Mapping, n_heads: int, n: int, s: int, tq: int
     return out
 
 
+def check_finite_device(w: Workload, q, k, v) -> None:
+    """Workload's finiteness rule (attn.py:54-56) for host torch tensors,
+    evaluated on their device copies."""
+    if _device.is_torch(w.q) and not w.q.is_cuda:
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            if not bool(torch.isfinite(t).all()):
+                raise ValueError(f"non-finite values in {name}")
+
+
 def run_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: PrefillPlan, scale: float) -> torch.Tensor:
     """Launch K4 on device tensors q [N,H,Dp], k/v [S,Hkv,Dp] (Dp in {64,128})."""
     lib = _lib.load()
@@ -343,6 +354,7 @@ def blockwise_attention(w: Workload, schedules: Mapping[tuple, Sequence[int]], t
     q = _device.to_device(w.q, dt, dev, dp)
     k = _device.to_device(w.k, dt, dev, dp)
     v = _device.to_device(w.v, dt, dev, dp)
+    check_finite_device(w, q, k, v)
     out = run_prefill(q, k, v, plan, 1.0 / math.sqrt(w.head_dim))[..., :w.head_dim]
     ledger = CostLedger()
     for h in range(w.num_heads):

@@ -157,8 +157,8 @@ class DevicePool:
         self.arena, self.stats, self.staging = arena, stats, staging
         self.slot_offsets = offs
         self.page_table_host = self._page_table(max_pages, offs)
-        self.page_table = torch.from_numpy(self.page_table_host).to(dev)
-        self.kind_dev = torch.tensor(self.kinds, dtype=torch.uint8, device=dev)
+        self.page_table = _device.h2d(self.page_table_host, dev)
+        self.kind_dev = _device.h2d(np.array(self.kinds, np.uint8), dev)
         self.max_pages = max_pages
 
     def reserve(self, tokens: int) -> None:

@@ -1,0 +1,163 @@
+"""CUDA-graph decode over many layers (extension outside the reference API).
+
+A decode step of a model runs every layer's attention: K2 selection (only
+on reuse-window starts) and K3 split-KV decode with the fused append.  At
+128k context one layer's kernels take a few microseconds, so Python launch
+overhead would dominate; this runner captures the whole multi-layer step
+into two CUDA graphs (selection step / reuse step) over static buffers and
+replays them.  Token counters, page tables and workspaces are device
+resident, so replays need no host->device traffic besides the new q/k/v
+rows.  Per-engine host bookkeeping (token mirrors, step counters, ledger)
+is advanced exactly like Engine.decode_step would.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import _device, _lib
+from .engine import DECODE, Engine
+from .heads import RETRIEVAL, lambda_segments
+from .selector import _Workspace, selection_size
+
+
+class DecodeGraph:
+    def __init__(self, engines: list, max_steps: int, head_dim: int, record_ledger: bool = True):
+        if not engines:
+            raise ValueError("need at least one engine")
+        e0 = engines[0]
+        self.engines = engines
+        self.cfg = e0.config
+        self.dev = e0.device
+        self.head_dim = head_dim
+        self.record_ledger = record_ledger
+        pools = [e.cache.pool for e in engines]
+        tok = pools[0].tokens_host[0]
+        for p in pools:
+            if set(p.tokens_host) != {tok}:
+                raise ValueError("all layers must hold the same token count")
+            p.reserve(tok + max_steps + 1)
+        self.pools = pools
+        self.g = e0._group_size
+        self.h_kv = pools[0].n_streams
+        self.h = self.h_kv * self.g
+        self.dp = pools[0].Dp
+        self.dtype = pools[0].dtype
+        self.start_tokens = tok
+        self.steps_done = 0
+        self.max_steps = max_steps
+        cfg = self.cfg
+        self.k_pages = -(-cfg.budget_tokens // cfg.physical_page)
+        self.max_pages_hint = -(-(tok + max_steps) // cfg.physical_page)
+        L = len(engines)
+        z = lambda *s, dt=self.dtype: torch.zeros(*s, dtype=dt, device=self.dev)  # noqa: E731
+        self.q = z(L, self.h, self.dp)
+        self.k = z(L, self.h_kv, self.dp)
+        self.v = z(L, self.h_kv, self.dp)
+        self.out = z(L, self.h, self.dp)
+        width = max(4, self.k_pages)
+        self.sel = [torch.zeros((self.h_kv, width), dtype=torch.int32, device=self.dev) for _ in engines]
+        self.cnt = [torch.zeros(self.h_kv, dtype=torch.int32, device=self.dev) for _ in engines]
+        units = max(selection_size(self.max_pages_hint, self.k_pages), 1) + cfg.sink_blocks + cfg.local_blocks
+        self.pps = 4
+        self.max_splits = -(-units // self.pps)
+        need = _lib.load().sk_decode_workspace(self.h_kv, self.g, self.dp, self.max_splits)
+        self.dec_ws = [torch.zeros(need, dtype=torch.uint8, device=self.dev) for _ in engines]
+        self.sel_ws = [torch.zeros(_lib.load().sk_select_workspace(self.h_kv, self.max_pages_hint),
+                                   dtype=torch.uint8, device=self.dev) for _ in engines]
+        self.graphs = {}
+        # prime selections (first step must select anyway) then capture
+        self._capture()
+
+    # -- launches ---------------------------------------------------------------
+    def _launch_layer(self, li: int, select: bool) -> None:
+        e, pool = self.engines[li], self.pools[li]
+        lib = _lib.load()
+        stream = _device.stream_ptr(self.dev)
+        abi = pool.abi()
+        if select:
+            ws = self.sel_ws[li]
+            rc = lib.sk_select_pages(C.byref(abi), self.h_kv, self.g, self.q[li].data_ptr(), self.g * self.dp,
+                                     self.dp, e._row_mask.data_ptr(), pool.tokens.data_ptr(), None, self.k_pages,
+                                     self.max_pages_hint, self.sel[li].data_ptr(), self.cnt[li].data_ptr(),
+                                     self.sel[li].shape[1], ws.data_ptr(), ws.numel(), stream)
+            _lib.check(rc)
+        ws = self.dec_ws[li]
+        rc = lib.sk_decode_attn(C.byref(abi), self.h_kv, self.g, self.q[li].data_ptr(), self.g * self.dp, self.dp,
+                                self.k[li].data_ptr(), self.v[li].data_ptr(), self.dp, e._row_mask.data_ptr(),
+                                self.sel[li].data_ptr(), self.cnt[li].data_ptr(), self.sel[li].shape[1],
+                                pool.tokens.data_ptr(), C.c_float(1.0 / math.sqrt(self.head_dim)),
+                                self.out[li].data_ptr(), self.g * self.dp, self.dp, _device.sk_dtype(self.dtype),
+                                self.pps, self.max_splits, 1, ws.data_ptr(), ws.numel(), stream)
+        _lib.check(rc)
+
+    def _launch_step(self, select: bool) -> None:
+        for li in range(len(self.engines)):
+            self._launch_layer(li, select)
+
+    def _capture(self) -> None:
+        # capture mutates device token counters when kernels run? No: capture
+        # only records.  Warm the kernels (function attributes) outside capture
+        # on a throw-away copy of nothing: attributes are set at first launch,
+        # which is allowed during capture.
+        for select in (True, False):
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream(device=self.dev)
+            s.wait_stream(torch.cuda.current_stream(self.dev))
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    self._launch_step(select)
+            torch.cuda.current_stream(self.dev).wait_stream(s)
+            self.graphs[select] = g
+
+    # -- stepping ---------------------------------------------------------------
+    def step(self) -> torch.Tensor:
+        """Run one decode step for every layer on the current contents of
+        self.q / self.k / self.v; returns self.out (device)."""
+        if self.steps_done >= self.max_steps:
+            raise RuntimeError("DecodeGraph capacity exhausted; build a new one")
+        cfg = self.cfg
+        step = self.engines[0].decode_steps
+        select = any(not (st is not None and st.valid_for(step, cfg.budget_tokens, cfg.reuse_interval))
+                     for e in self.engines for kv, st in [(kv, e.selection_states.get(kv))
+                                                            for kv in e.cache.dense_pool if e._row_mask_host[kv]])
+        self.graphs[select].replay()
+        n_tok = self.start_tokens + self.steps_done
+        n_pages = -(-n_tok // cfg.physical_page)
+        for e, pool in zip(self.engines, self.pools):
+            if select:
+                from .selector import SelectionState
+                size = selection_size(n_pages, self.k_pages)
+                for kv in e.cache.dense_pool:
+                    if e._row_mask_host[kv]:
+                        e.selection_states[kv] = SelectionState(_Sized(size), step, cfg.reuse_interval,
+                                                                cfg.budget_tokens)
+                        e.ledger.record_selector(kv)
+            if self.record_ledger:
+                for hh, prof in enumerate(e.profiles):
+                    kv = hh // self.g
+                    if prof.role == RETRIEVAL:
+                        vis = len(e.selection_states[kv].selected_pages)
+                    else:
+                        vis = sum(b - a for a, b in lambda_segments(n_pages, prof.sink_blocks, prof.local_blocks,
+                                                                     n_pages - 1))
+                    e.ledger.record_tiles(DECODE, hh, vis, n_pages)
+            for s in range(pool.n_streams):
+                pool.tokens_host[s] += 1
+            e.decode_steps += 1
+        self.steps_done += 1
+        return self.out
+
+
+class _Sized(list):
+    """Placeholder selection list of known length (contents stay on device)."""
+
+    def __init__(self, n: int):
+        super().__init__()
+        self._n = n
+
+    def __len__(self) -> int:
+        return self._n

@@ -30,7 +30,7 @@ import numpy as np
 import torch
 
 from . import _device, _lib
-from .attn import Workload, diagonal_tile, kv_tile_count, plan_from_segments, plan_generic, query_tile_count, \
+from .attn import Workload, check_finite_device, diagonal_tile, kv_tile_count, plan_from_segments, plan_generic, query_tile_count, \
     run_prefill
 from .cache import TwoWayCache
 from .heads import RETRIEVAL, HeadProfile, lambda_segments
@@ -210,7 +210,7 @@ class Engine:
                     mk |= 1 << r
             masks.append(mk)
         self._row_mask_host = masks
-        self._row_mask = torch.tensor(masks, dtype=torch.int32, device=self.device)
+        self._row_mask = _device.h2d(np.array(masks, np.int32), self.device)
         self._sel = None
         self.selection_states = {}
         del g
@@ -253,6 +253,7 @@ class Engine:
         q = _device.to_device(w.q, self._dtype, dev, dp)
         k = _device.to_device(w.k, self._dtype, dev, dp)
         v = _device.to_device(w.v, self._dtype, dev, dp)
+        check_finite_device(w, q, k, v)
         out = self.prefill_device(q, k, v, w.head_dim)
         np_dt = None if _device.is_torch(w.q) else np.asarray(w.q).dtype
         return _device.to_output(out[..., :w.head_dim], w.q, np_dt)
@@ -343,7 +344,7 @@ class Engine:
                 # partial invocation: keep the other streams' selections (copy: the
                 # previous tensors back DevicePageLists that must stay immutable)
                 sel, cnt = self._sel[0].clone(), self._sel[1].clone()
-                inv = torch.tensor([1 if kv in need else 0 for kv in range(h_kv)], dtype=torch.uint8, device=dev)
+                inv = _device.h2d(np.array([1 if kv in need else 0 for kv in range(h_kv)], np.uint8), dev)
             else:
                 sel = torch.empty((h_kv, width), dtype=torch.int32, device=dev)
                 cnt = torch.zeros(h_kv, dtype=torch.int32, device=dev)
