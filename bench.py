@@ -123,8 +123,8 @@ def cpu_reference_sample(ctx: int, layers: int, seed: int = 0, budget_s: float =
     vis_layer = sum((qt + 1) if roles[h].role == O.RETRIEVAL else len(O.lambda_tiles(n_tiles, SINK, LOCAL, qt))
                     for h in range(H) for qt in range(n_tiles))
     prefill_ms = t_pre / vis_sample * vis_layer * layers * 1e3
-    # decode sample: one layer at a shorter context, extrapolated per page
-    s_dec = min(ctx, 16384)
+    # decode sample: one layer at the full context, one reuse window of steps
+    s_dec = ctx
     eng = O.OracleEngine(O.Config(quant_bits=BITS, budget_tokens=BUDGET, reuse_interval=REUSE, sink_blocks=SINK,
                                   local_blocks=LOCAL), roles)
     k = rng.standard_normal((s_dec, HKV, D)).astype(np.float16).astype(np.float32)
@@ -136,13 +136,12 @@ def cpu_reference_sample(ctx: int, layers: int, seed: int = 0, budget_s: float =
         kn = rng.standard_normal((HKV, D)).astype(np.float32)
         eng.decode_step(qn, kn, kn)
     t_dec = (time.perf_counter() - t0) / steps
-    # decode cost is ~linear in pages read + pages scored; scale the scoring share by ctx
-    sel_frac = 0.25
-    dec_step_ms = t_dec * (1 + sel_frac * (ctx / s_dec - 1) * 0.1) * layers * 1e3
+    dec_step_ms = t_dec * layers * 1e3
     return {"prefill_ms": prefill_ms, "decode_us_per_step": dec_step_ms * 1e3, "cores": int(threads),
             "sample": (f"oracle port (numpy) prefill of query tiles {qts} x 32 heads of one 128k layer "
                        f"({vis_sample} visited 64x64 tiles, {t_pre:.1f}s), extrapolated by visited tiles to "
-                       f"{layers} layers; decode: {steps} steps of one layer at {s_dec} tokens, x{layers} layers"),
+                       f"{layers} layers; decode: one reuse window ({steps} steps, 1 selection) of one layer at {s_dec} "
+                       f"tokens, x{layers} layers"),
             "seconds": t_pre + t_dec * steps}
 
 
@@ -207,8 +206,9 @@ def run_ours(args, rank, world, local_rank):
 
     for _ in range(args.warmup):
         timed(prefill_step, 1)
-    with Clocks(local_rank) as clk:
-        pre_ts = timed(prefill_step, args.steps)
+    clk = Clocks(local_rank)
+    clk.__enter__()
+    pre_ts = timed(prefill_step, args.steps)
     pre_ms = statistics.mean(pre_ts)
     if world > 1:
         t = torch.tensor([pre_ms], device=dev)
@@ -263,6 +263,7 @@ def run_ours(args, rank, world, local_rank):
         b.record()
         torch.cuda.synchronize()
         dec_ts.append(a.elapsed_time(b))
+    clk.__exit__()
     dec_us = statistics.mean(dec_ts) * 1e3
     if world > 1:
         t = torch.tensor([dec_us], device=dev)
