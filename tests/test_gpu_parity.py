@@ -200,3 +200,37 @@ def test_decode_long_context_selection_matches_oracle():
         assert res.invoked == rr.invoked
         assert_close_attn(res.output, rr.output)
     assert eng.ledger.tiles == {k2: v2 for k2, v2 in ref.tally.tiles.items()}
+
+
+def test_decode_graph_matches_eager_engine():
+    """The CUDA-graph multi-layer decode runner reproduces Engine.decode_step
+    (same selections -> same outputs, same ledger) for 2 layers x 9 steps."""
+    from paper_2502_14866_b200.decode_graph import DecodeGraph
+
+    rng = np.random.default_rng(13)
+    s, h, h_kv, d, L = 4096 + 37, 8, 2, 128, 2
+    gates = [0.9, 0.8, 0.1, 0.2, 0.85, 0.15, 0.12, 0.11]
+    cfg = sk.EngineConfig(quant_bits=4, budget_tokens=512, reuse_interval=4, local_blocks=4)
+    prof = sk.classify_heads(gates, 0.5, 1, 4)
+    ks = [rng.standard_normal((s, h_kv, d)).astype(np.float16) for _ in range(L)]
+    vs = [rng.standard_normal((s, h_kv, d)).astype(np.float16) for _ in range(L)]
+    eager = [sk.Engine(cfg, prof, device="cuda:0") for _ in range(L)]
+    graph = [sk.Engine(cfg, prof, device="cuda:0") for _ in range(L)]
+    for e1, e2, k, v in zip(eager, graph, ks, vs):
+        e1.load_context(k.astype(np.float32), v.astype(np.float32))
+        e2.load_context(k.astype(np.float32), v.astype(np.float32))
+    dg = DecodeGraph(graph, 16, d)
+    for t in range(9):
+        qn = torch.from_numpy(rng.standard_normal((L, h, d)).astype(np.float16)).cuda()
+        kn = torch.from_numpy(rng.standard_normal((L, h_kv, d)).astype(np.float16)).cuda()
+        vn = torch.from_numpy(rng.standard_normal((L, h_kv, d)).astype(np.float16)).cuda()
+        dg.q.copy_(qn)
+        dg.k.copy_(kn)
+        dg.v.copy_(vn)
+        out_g = dg.step().float().cpu().numpy()
+        for li in range(L):
+            res = eager[li].decode_step(qn[li], kn[li], vn[li])
+            np.testing.assert_allclose(out_g[li], res.output.float().cpu().numpy(), atol=1e-3, rtol=0)
+    for e1, e2 in zip(eager, graph):
+        assert e1.ledger.tiles == e2.ledger.tiles
+        assert e1.ledger.selector_invocations == e2.ledger.selector_invocations
