@@ -205,4 +205,142 @@ __device__ void append_page(const PoolView& pv, int s, int p, int n0, int n1, co
   }
 }
 
+
+// Decode-step append of ONE token to stream s holding n_tok tokens, for an
+// open page that already has t_old = n_tok % P > 0 tokens.  Bit-identical
+// to append_page(): a channel whose min/max did not move keeps its lo and
+// scale, so only the new token's code changes; channels whose bounds moved
+// are re-coded for every token of the page from the raw staging copy.
+// Whole CTA; smem >= 2*D*(4 + 3*8 + 1) bytes.
+template <typename T>
+__device__ void append_one_token(const PoolView& pv, int s, int n_tok, const T* __restrict__ kn,
+                                 const T* __restrict__ vn, uint8_t* smem) {
+  const int D = pv.D, P = pv.P;
+  const int t_old = n_tok % P;
+  const int p = n_tok / P;
+  if (t_old == 0 || pv.bits == 0) {
+    append_page<T>(pv, s, p, n_tok, n_tok + 1, kn, vn, 0, smem);
+    return;
+  }
+  const bool dense = pv.kind[s] == SK_KIND_DENSE;
+  uint8_t* slot = pv.slot_ptr(s, p);
+  T* bnd = reinterpret_cast<T*>(pv.bounds(slot));
+  const T* stg[2] = {reinterpret_cast<const T*>(pv.staging_ptr(s, 0)),
+                     reinterpret_cast<const T*>(pv.staging_ptr(s, 1))};
+  float* xnew = reinterpret_cast<float*>(smem);   // [2][D]
+  double* lo = reinterpret_cast<double*>(xnew + 2 * D);  // [2][D]
+  double* sc = lo + 2 * D;
+  double* inv = sc + 2 * D;
+  uint8_t* chg = reinterpret_cast<uint8_t*>(inv + 2 * D);  // [2][D]
+  const int levels = (1 << pv.bits) - 1;
+  for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) {
+    const int which = i / D, c = i % D;
+    const float x = DT<T>::to_f((which ? vn : kn)[c]);
+    const int pos = which ? vbound_pos(c, D) : kbound_pos(c, D);
+    const float olo = DT<T>::to_f(bnd[2 * which * D + pos]), ohi = DT<T>::to_f(bnd[(2 * which + 1) * D + pos]);
+    const float nlo = fminf(olo, x), nhi = fmaxf(ohi, x);
+    const bool changed = (nlo != olo) || (nhi != ohi);
+    if (changed) {
+      bnd[2 * which * D + pos] = DT<T>::from_f(nlo);
+      bnd[(2 * which + 1) * D + pos] = DT<T>::from_f(nhi);
+    }
+    double scl = ((double)nhi - (double)nlo) / levels;
+    if (!(scl > 0.0)) scl = 1.0;
+    xnew[i] = x;
+    lo[i] = nlo;
+    sc[i] = scl;
+    inv[i] = 1.0 / scl;
+    chg[i] = changed;
+  }
+  __syncthreads();
+  auto code_at = [&](int which, int t, int c) -> uint32_t {
+    if (t > t_old) return 0u;  // padding slots of the page
+    const float raw = t == t_old ? xnew[which * D + c] : DT<T>::to_f(stg[which][t * D + c]);
+    const int i = which * D + c;
+    return quant_code((double)raw, lo[i], sc[i], inv[i], levels);
+  };
+  uint32_t* kw = reinterpret_cast<uint32_t*>(pv.k_codes(slot));
+  uint32_t* vw = reinterpret_cast<uint32_t*>(pv.v_codes(slot));
+  const bool nib = pv.bits <= 4;
+  const int cpw = nib ? 8 : 4;                      // codes per 32-bit word
+  const int wpt = nib ? D / 8 : D / 4;              // K words per token
+  const int wpc = nib ? D / 32 : D / 16;            // K words per (token, j) chunk
+  const int vwl = nib ? P / 32 : P / 16;            // V words per (cn, lane)
+  // (q-th code of a word) -> (register index offset, e, bit position)
+  auto qmap = [&](int w, int q, int& ri, int& e, int& bit) {
+    if (nib) {
+      const int slt = q >> 1;
+      e = q & 1;
+      ri = 4 * w + slt;
+      bit = 4 * slt + 16 * e;
+    } else {
+      const int r2 = q >> 1;
+      e = q & 1;
+      ri = 2 * w + r2;
+      bit = 8 * (2 * r2 + e);
+    }
+  };
+  const uint32_t cmask = nib ? 0xFu : 0xFFu;
+  // K: words of tokens 0..t_old (token t_old fully rewritten, others only if a channel moved)
+  for (int wi = threadIdx.x; wi < (t_old + 1) * wpt; wi += blockDim.x) {
+    const int t = wi / wpt, rem = wi % wpt, j = rem / wpc, w = rem % wpc;
+    uint32_t word = t == t_old ? 0u : kw[t * wpt + rem];
+    bool dirty = t == t_old;
+    for (int q = 0; q < cpw; ++q) {
+      int ri, e, bit;
+      qmap(w, q, ri, e, bit);
+      const int d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j + e;
+      if (t == t_old || chg[d]) {
+        word = (word & ~(cmask << bit)) | (code_at(0, t, d) << bit);
+        dirty = true;
+      }
+    }
+    if (dirty) kw[t * wpt + rem] = word;
+  }
+  // V: a moved channel rewrites all its words; otherwise only the nibble/byte of token t_old
+  const int vwords = P * D / cpw;
+  for (int wi = threadIdx.x; wi < vwords; wi += blockDim.x) {
+    const int cn = wi / (32 * vwl), rem = wi % (32 * vwl), lane = rem / vwl, w = rem % vwl;
+    const int c = 8 * cn + lane / 4, j = lane % 4;
+    const bool moved = chg[D + c];
+    uint32_t word = moved ? 0u : vw[wi];
+    bool dirty = moved;
+    for (int q = 0; q < cpw; ++q) {
+      int ri, e, bit;
+      qmap(w, q, ri, e, bit);
+      const int t = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j + e;
+      if (moved || t == t_old) {
+        word = (word & ~(cmask << bit)) | (code_at(1, t, c) << bit);
+        dirty = true;
+      }
+    }
+    if (dirty) vw[wi] = word;
+  }
+  // logical-page key stats of the page's open logical page (dense pool)
+  if (dense && pv.stats != nullptr) {
+    const int L = pv.L;
+    T* st = reinterpret_cast<T*>(pv.stats_ptr(s, p * (P / L) + t_old / L));
+    const bool fresh = (t_old % L) == 0;
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+      const float x = xnew[c];
+      if (fresh) {
+        st[c] = DT<T>::from_f(x);
+        st[D + c] = DT<T>::from_f(x);
+      } else {
+        st[c] = DT<T>::from_f(fminf(DT<T>::to_f(st[c]), x));
+        st[D + c] = DT<T>::from_f(fmaxf(DT<T>::to_f(st[D + c]), x));
+      }
+    }
+  }
+  // raw staging of the open page (unless the page is now full)
+  if (t_old + 1 < P) {
+    T* wk = reinterpret_cast<T*>(pv.staging_ptr(s, 0));
+    T* wv = reinterpret_cast<T*>(pv.staging_ptr(s, 1));
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+      wk[t_old * D + c] = kn[c];
+      wv[t_old * D + c] = vn[c];
+    }
+  }
+}
+
 }  // namespace sk

@@ -19,6 +19,7 @@
 // (atomic ticket) together with the new token's raw K/V, then -- if asked --
 // that CTA appends the new token to its page (K1's page rebuild).
 #include "append_impl.cuh"
+#include "sk_sm100.cuh"
 
 namespace sk {
 namespace {
@@ -113,7 +114,9 @@ __device__ __forceinline__ bool contains(const int32_t* a, int n, int x) {
 }
 
 // KIND: 0 raw pages (MMA in T), 1 nibble codes, 2 byte codes (MMA in fp16).
-template <typename T, int KIND, int D, int P>
+// NBUF: pages staged per warp in shared memory by cp.async (0 = read the
+// arena directly, 2 = double-buffered prefetch of the warp's next page).
+template <typename T, int KIND, int D, int P, int NBUF>
 __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
   using MT = typename std::conditional<KIND == 0, T, __half>::type;
   constexpr int NKS = D / 16;   // QK k-steps
@@ -121,6 +124,8 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
   constexpr int NCN = D / 8;    // PV n-tiles (8 channels)
   constexpr int NPK = P / 16;   // PV k-steps (16 tokens)
   constexpr int QR = D / 4;     // q / o / bounds values per thread
+  constexpr int RB = KIND == 0 ? 2 * D : (KIND == 1 ? D / 2 : D);  // code row bytes
+  constexpr int SLOT_USED = 2 * P * RB + (KIND == 0 ? 0 : 8 * D);  // bytes of a slot the kernel reads
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_extra[kMaxExtra];
   __shared__ int s_nextra;
@@ -139,12 +144,32 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
   const int nsel = rmask ? prm.sel_count[s] : 0;
   const int32_t* sel = prm.sel + (int64_t)s * prm.sel_stride;
   const int sink_end = min(pv.sink, n_pages), local_start = max(n_pages - pv.local, 0);
+  const int u_begin = split * prm.pps;
+  uint8_t* wbuf = smem + warp * (NBUF > 0 ? NBUF : 1) * SLOT_USED;
 
+  auto prefetch = [&](int p, int b) {
+    const uint8_t* src = pv.slot_ptr(s, p);
+    uint8_t* dst = wbuf + b * SLOT_USED;
+    for (int i = lane; i < SLOT_USED / 16; i += 32) cp_async16(dst + 16 * i, src + 16 * i);
+    cp_async_commit();
+  };
+  // the warp's first page can start streaming before the union is known
+  int first_u = u_begin + warp;
+  bool first_issued = false;
+  if constexpr (NBUF > 0) {
+    if (first_u < nsel && first_u < u_begin + prm.pps) {
+      prefetch(sel[first_u], 0);
+      first_issued = true;
+    }
+  }
   if (tid == 0) {
     int ne = 0;
     if (smask) {
       for (int p = 0; p < n_pages && ne < kMaxExtra; ++p) {
-        if (p >= sink_end && p < local_start) { p = local_start - 1; continue; }
+        if (p >= sink_end && p < local_start) {
+          p = local_start - 1;
+          continue;
+        }
         if (!contains(sel, nsel, p)) s_extra[ne++] = p;
       }
     }
@@ -153,6 +178,16 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
   __syncthreads();
   const int U = nsel + s_nextra;
   const int n_used = (U + prm.pps - 1) / prm.pps;
+  const int u_end = min(U, u_begin + prm.pps);
+  auto page_of = [&](int u, uint32_t& um) -> int {
+    if (u < nsel) {
+      int p = sel[u];
+      um = rmask | ((smask && (p < sink_end || p >= local_start)) ? smask : 0u);
+      return p;
+    }
+    um = smask;
+    return s_extra[u - nsel];
+  };
 
   // ---- per-thread row state: row r (lane/4), dims/channels of j (lane%4) ----
   const bool row_ok = r < G;
@@ -172,25 +207,35 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
   for (int i = 0; i < QR; ++i) o[i] = 0.f;
   float m_run = -INFINITY, l_run = 0.f;
   const float sl2 = prm.scale_log2;
-  const int levels = (1 << pv.bits) - 1;
-  const float inv_levels = KIND == 0 ? 1.f : 1.f / float(levels);
+  const float inv_levels = KIND == 0 ? 1.f : 1.f / float((1 << pv.bits) - 1);
 
-  const int u_begin = split * prm.pps, u_end = min(U, u_begin + prm.pps);
-  for (int u = u_begin + warp; u < u_end; u += kWarps) {
-    int p;
+  int it = 0;
+  for (int u = first_u; u < u_end; u += kWarps, ++it) {
     uint32_t um;
-    if (u < nsel) {
-      p = sel[u];
-      um = rmask | ((smask && (p < sink_end || p >= local_start)) ? smask : 0u);
+    const int p = page_of(u, um);
+    const uint8_t* pg;
+    if constexpr (NBUF > 0) {
+      if (!first_issued || (NBUF == 1 && it > 0)) {
+        prefetch(p, 0);
+        first_issued = true;
+      }
+      const int un = u + kWarps;
+      if (NBUF == 2 && un < u_end) {
+        uint32_t um2;
+        prefetch(page_of(un, um2), (it + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      pg = wbuf + (NBUF == 2 ? (it & 1) : 0) * SLOT_USED;
     } else {
-      p = s_extra[u - nsel];
-      um = smask;
+      pg = pv.slot_ptr(s, p);
     }
     const int tok_in_page = min(P, n_tok - p * P);
-    const uint8_t* slot = pv.slot_ptr(s, p);
-    const uint8_t* kc = slot;
-    const uint8_t* vc = slot + (int64_t)P * pv.row_bytes;
-    const T* bnd = reinterpret_cast<const T*>(slot + 2ll * P * pv.row_bytes);
+    const uint8_t* kc = pg;
+    const uint8_t* vc = pg + P * RB;
+    const T* bnd = reinterpret_cast<const T*>(pg + 2 * P * RB);
 
     // ---- K side: q' = q * s_k / smax (A fragments), qz = q . lo_k ----
     uint32_t afr[NKS][2];
@@ -243,14 +288,13 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
       const int tok = 8 * nt + r;  // B operand: n = lane/4
       float c[4] = {0.f, 0.f, 0.f, 0.f};
       if constexpr (KIND == 1) {
-        // D/8 bytes = D/32 words for this (token, j)
-        const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(kc + tok * (D / 2) + j * (D / 8));
         uint32_t wd[D / 32];
+        const uint8_t* src = kc + tok * (D / 2) + j * (D / 8);
         if constexpr (D == 128) {
-          uint4 v = *reinterpret_cast<const uint4*>(wsrc);
+          uint4 v = *reinterpret_cast<const uint4*>(src);
           wd[0] = v.x; wd[1] = v.y; wd[2] = v.z; wd[3] = v.w;
         } else {
-          uint2 v = *reinterpret_cast<const uint2*>(wsrc);
+          uint2 v = *reinterpret_cast<const uint2*>(src);
           wd[0] = v.x; wd[1] = v.y;
         }
 #pragma unroll
@@ -260,11 +304,11 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
           mma16816<MT>(c, afr[ks][0], 0u, afr[ks][1], 0u, b0, b1);
         }
       } else if constexpr (KIND == 2) {
-        const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(kc + tok * D + j * (D / 4));
         uint32_t wd[D / 16];
+        const uint4* src = reinterpret_cast<const uint4*>(kc + tok * D + j * (D / 4));
 #pragma unroll
         for (int i = 0; i < D / 64; ++i) {
-          uint4 v = reinterpret_cast<const uint4*>(wsrc)[i];
+          uint4 v = src[i];
           wd[4 * i] = v.x; wd[4 * i + 1] = v.y; wd[4 * i + 2] = v.z; wd[4 * i + 3] = v.w;
         }
 #pragma unroll
@@ -273,17 +317,16 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
           mma16816<MT>(c, afr[ks][0], 0u, afr[ks][1], 0u, b0, b1);
         }
       } else {
-        const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(kc + (int64_t)tok * D * 2 + j * (D / 2));
         uint32_t wd[D / 8];
+        const uint4* src = reinterpret_cast<const uint4*>(kc + tok * D * 2 + j * (D / 2));
 #pragma unroll
         for (int i = 0; i < D / 32; ++i) {
-          uint4 v = reinterpret_cast<const uint4*>(wsrc)[i];
+          uint4 v = src[i];
           wd[4 * i] = v.x; wd[4 * i + 1] = v.y; wd[4 * i + 2] = v.z; wd[4 * i + 3] = v.w;
         }
 #pragma unroll
         for (int ks = 0; ks < NKS; ++ks) mma16816<MT>(c, afr[ks][0], 0u, afr[ks][1], 0u, wd[2 * ks], wd[2 * ks + 1]);
       }
-      // C fragment: row r, tokens 8nt + 2j + {0,1}
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         int t = 8 * nt + 2 * j + e;
@@ -348,11 +391,16 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
       float c[4] = {0.f, 0.f, 0.f, 0.f};
       const int vl = 32 * cn + lane;  // (cn, lane) chunk
       if constexpr (KIND == 1) {
-        constexpr int NW = P / 32;  // words per chunk
-        const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(vc + vl * (P / 8));
+        constexpr int NW = P / 32;
         uint32_t wd[NW];
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(vc + vl * (P / 8));
+        if constexpr (NW == 2) {
+          uint2 v = *reinterpret_cast<const uint2*>(src);
+          wd[0] = v.x; wd[1] = v.y;
+        } else {
 #pragma unroll
-        for (int i = 0; i < NW; ++i) wd[i] = wsrc[i];
+          for (int i = 0; i < NW; ++i) wd[i] = src[i];
+        }
 #pragma unroll
         for (int ks = 0; ks < NPK; ++ks) {
           int ri0 = 2 * ks, ri1 = 2 * ks + 1;
@@ -360,19 +408,19 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
         }
       } else if constexpr (KIND == 2) {
         constexpr int NW = P / 16;
-        const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(vc + vl * (P / 4));
         uint32_t wd[NW];
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(vc + vl * (P / 4));
 #pragma unroll
-        for (int i = 0; i < NW; ++i) wd[i] = wsrc[i];
+        for (int i = 0; i < NW; ++i) wd[i] = src[i];
 #pragma unroll
         for (int ks = 0; ks < NPK; ++ks)
           mma16816<MT>(c, pfr[ks][0], 0u, pfr[ks][1], 0u, byte2h(wd[ks], 0), byte2h(wd[ks], 1));
       } else {
         constexpr int NW = P / 8;
-        const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(vc + (int64_t)vl * (P / 2));
         uint32_t wd[NW];
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(vc + vl * (P / 2));
 #pragma unroll
-        for (int i = 0; i < NW; ++i) wd[i] = wsrc[i];
+        for (int i = 0; i < NW; ++i) wd[i] = src[i];
 #pragma unroll
         for (int ks = 0; ks < NPK; ++ks) mma16816<MT>(c, pfr[ks][0], 0u, pfr[ks][1], 0u, wd[2 * ks], wd[2 * ks + 1]);
       }
@@ -382,9 +430,11 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
         o[2 * cn + e] = fmaf(o[2 * cn + e], alpha, add);
       }
     }
+    if constexpr (NBUF > 0) __syncwarp();  // buffer may be refilled next iteration
   }
 
   // ---- merge the 4 warps of this CTA (rows < kMaxRows) ----
+  __syncthreads();  // page buffers are reused as the merge area
   float* sm_m = reinterpret_cast<float*>(smem);  // [kWarps][8]
   float* sm_l = sm_m + kWarps * kMaxRows;        // [kWarps][8]
   float* sm_o = sm_l + kWarps * kMaxRows;        // [kWarps][8][D]
@@ -424,10 +474,23 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
       }
     }
   }
-  // ---- last CTA of the stream: merge splits + the new token, write, append ----
-  __threadfence();
+  const T* kn = reinterpret_cast<const T*>(prm.k_new) + s * prm.new_ss;
+  const T* vn = reinterpret_cast<const T*>(prm.v_new) + s * prm.new_ss;
+  // The new token joins an open page (t_old > 0): the only reader of that page
+  // in this step is the unit holding page n_pages-1, so the CTA that owns it
+  // appends right after its own reads -- off the critical serial tail.
+  const bool opens_page = (n_tok % P) == 0;
+  if (prm.fuse_append && !opens_page) {
+    const int u_last = nsel > 0 ? nsel - 1 : U - 1;
+    if (u_last >= u_begin && u_last < u_end) {
+      __syncthreads();  // smem is reused by the append
+      append_one_token<T>(pv, s, n_tok, kn, vn, smem);
+    }
+  }
+  // ---- last CTA of the stream: merge splits + the new token, write ----
   __syncthreads();
   if (tid == 0) {
+    __threadfence();
     uint32_t t = atomicAdd(prm.ws_ticket + s, 1u);
     s_last = (t == gridDim.x - 1);
     if (s_last) prm.ws_ticket[s] = 0;
@@ -435,8 +498,6 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const T* kn = reinterpret_cast<const T*>(prm.k_new) + s * prm.new_ss;
-  const T* vn = reinterpret_cast<const T*>(prm.v_new) + s * prm.new_ss;
   for (int rr = warp; rr < G; rr += kWarps) {
     const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)rr * prm.q_rs;
     float dot = 0.f;
@@ -470,16 +531,27 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
     }
   }
   if (prm.fuse_append) {
-    __syncthreads();  // smem is reused by the page rebuild
-    append_page<T>(pv, s, n_tok / P, n_tok, n_tok + 1, kn, vn, 0, smem);
+    if (opens_page) {
+      // a fresh page may reuse a streaming ring slot read in this step: only now is it free
+      __syncthreads();
+      append_page<T>(pv, s, n_tok / P, n_tok, n_tok + 1, kn, vn, 0, smem);
+    }
     __syncthreads();
     if (tid == 0) prm.tokens[s] = n_tok + 1;
   }
 }
 
+__host__ __device__ constexpr int slot_used(int kind, int D, int P) {
+  return 2 * P * (kind == 0 ? 2 * D : (kind == 1 ? D / 2 : D)) + (kind == 0 ? 0 : 8 * D);
+}
+
 template <typename T, int KIND, int D, int P>
-int launch_one(const DecodeParams& prm, dim3 grid, size_t smem, cudaStream_t st) {
-  auto kern = decode_kernel<T, KIND, D, P>;
+int launch_one(const DecodeParams& prm, dim3 grid, size_t smem_min, cudaStream_t st) {
+  constexpr int SLOT = slot_used(KIND, D, P);
+  constexpr int NBUF = (2 * kWarps * SLOT <= 160 * 1024) ? 2 : ((kWarps * SLOT <= 160 * 1024) ? 1 : 0);
+  size_t smem = (size_t)kWarps * (NBUF > 0 ? NBUF : 0) * SLOT;
+  if (smem < smem_min) smem = smem_min;
+  auto kern = decode_kernel<T, KIND, D, P, NBUF>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, kDecThreads, smem, st>>>(prm);
   SK_CHECK_LAUNCH("decode_kernel");
@@ -556,6 +628,8 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
                                               (int64_t)n_streams * max_splits * kMaxRows * (2 + pool->head_dim) * 4);
   size_t smem_merge = (size_t)kWarps * kMaxRows * (2 + pool->head_dim) * 4;
   size_t smem_app = fuse_append ? append_smem_bytes(pool->head_dim, pool->page_size) : 0;
+  size_t smem_one = (size_t)2 * pool->head_dim * (4 + 3 * 8 + 1);
+  if (smem_app < smem_one) smem_app = smem_one;
   size_t smem = smem_merge > smem_app ? smem_merge : smem_app;
   dim3 grid(max_splits, n_streams);
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -20,7 +20,7 @@ namespace sk {
 namespace {
 
 constexpr int kSelThreads = 256;
-constexpr int kPagesPerWarp = 2;
+constexpr int kPagesPerWarp = 1;
 constexpr int kPagesPerCta = (kSelThreads / 32) * kPagesPerWarp;
 
 __device__ __forceinline__ int pins_of(int n, int* pin) {  // selector.py:75-78
@@ -102,33 +102,35 @@ __device__ void score_pages_cta(const PoolView& pv, int s, int n_tok, const T* q
   for (int it = 0; it < kPagesPerWarp; ++it) {
     int p = blockIdx.x * kPagesPerCta + it * (kSelThreads / 32) + warp;
     if (p >= n_pages) break;
-    double v[NV];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) v[i] = 0.0;
+    // issue every stats load of the page before any arithmetic (latency)
+    uint2 wmin[LP], wmax[LP];
 #pragma unroll
     for (int j = 0; j < LP; ++j) {
-      int lp = p * LP + j;
-      if (lp < n_log) {
-        const T* st = reinterpret_cast<const T*>(pv.stats_ptr(s, lp));
-        double kmin[4] = {0, 0, 0, 0}, kmax[4] = {0, 0, 0, 0};
-        if (cpl == 4) {
-          load4(st + lane * 4, kmin);
-          load4(st + D + lane * 4, kmax);
-        } else {
-          float2 a = DT<T>::to_f2(*reinterpret_cast<const uint32_t*>(st + lane * 2));
-          float2 b = DT<T>::to_f2(*reinterpret_cast<const uint32_t*>(st + D + lane * 2));
-          kmin[0] = a.x; kmin[1] = a.y; kmax[0] = b.x; kmax[1] = b.y;
-        }
+      const int lp = min(p * LP + j, n_log - 1);  // clamp: invalid entries are masked below
+      const T* st = reinterpret_cast<const T*>(pv.stats_ptr(s, lp));
+      if (cpl == 4) {
+        wmin[j] = __ldcg(reinterpret_cast<const uint2*>(st + lane * 4));
+        wmax[j] = __ldcg(reinterpret_cast<const uint2*>(st + D + lane * 4));
+      } else {
+        wmin[j] = make_uint2(__ldcg(reinterpret_cast<const uint32_t*>(st + lane * 2)), 0u);
+        wmax[j] = make_uint2(__ldcg(reinterpret_cast<const uint32_t*>(st + D + lane * 2)), 0u);
+      }
+    }
+    double v[NV];
 #pragma unroll
-        for (int r = 0; r < RMAX; ++r) {
-          double acc = 0.0;
+    for (int j = 0; j < LP; ++j) {
+      float2 a0 = DT<T>::to_f2(wmin[j].x), a1 = DT<T>::to_f2(wmin[j].y);
+      float2 b0 = DT<T>::to_f2(wmax[j].x), b1 = DT<T>::to_f2(wmax[j].y);
+      const double kmin[4] = {a0.x, a0.y, a1.x, a1.y}, kmax[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            acc = fma(qp[r][c], kmax[c], acc);
-            acc = fma(qm[r][c], kmin[c], acc);
-          }
-          v[r * LP + j] = acc;
+      for (int r = 0; r < RMAX; ++r) {
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc = fma(qp[r][c], kmax[c], acc);
+          acc = fma(qm[r][c], kmin[c], acc);
         }
+        v[r * LP + j] = acc;
       }
     }
     Butterfly<NV, 16>::run(v, lane);
@@ -137,7 +139,10 @@ __device__ void score_pages_cta(const PoolView& pv, int s, int n_tok, const T* q
     double mine = (r < rows && p * LP + j < n_log) ? v[0] : -INFINITY;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) mine = fmax(mine, __shfl_xor_sync(0xffffffffu, mine, off));
-    if (lane == 0) scores[p] = mine;
+    if (lane == 0) {
+      scores[p] = mine;
+      __threadfence();  // publish before the CTA's ticket
+    }
   }
 }
 
@@ -170,7 +175,7 @@ __device__ void topk_cta(const double* scores, int n, int K, int32_t* sel_out, i
     __syncthreads();
     for (int i = tid; i < n; i += blockDim.x) {
       if (is_pin(i, n)) continue;
-      uint64_t key = order_key(scores[i]);
+      uint64_t key = order_key(__ldcg(scores + i));
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
     }
     __syncthreads();
@@ -217,7 +222,7 @@ __device__ void topk_cta(const double* scores, int n, int K, int32_t* sel_out, i
     int i = base + tid;
     bool valid = i < n;
     bool pinned = valid && is_pin(i, n);
-    uint64_t key = valid && !pinned ? order_key(scores[i]) : 0;
+    uint64_t key = valid && !pinned ? order_key(__ldcg(scores + i)) : 0;
     uint64_t km = key & mask;
     bool gt = valid && !pinned && km > prefix;
     bool eq = valid && !pinned && km == prefix;
@@ -268,9 +273,9 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(PoolView pv, const 
   if (!trivial) score_pages_cta<T, RMAX, LP>(pv, s, n_tok, q + s * q_ss, q_rs, rmask, scores);
   // last CTA of this stream runs the top-k
   __shared__ uint32_t is_last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     uint32_t t = atomicAdd(ws_ticket + s, 1u);
     is_last = (t == gridDim.x - 1);
     if (is_last) ws_ticket[s] = 0;  // re-arm for the next invocation

@@ -212,3 +212,17 @@ __device__ __forceinline__ float fast_exp2(float x) {
 }
 
 }  // namespace sk
+
+namespace sk {
+// ---------------------------------------------------------------------------
+// cp.async (LDGSTS): 16-byte global -> shared copies, L2-only caching
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+}  // namespace sk
