@@ -234,3 +234,56 @@ def test_decode_graph_matches_eager_engine():
     for e1, e2 in zip(eager, graph):
         assert e1.ledger.tiles == e2.ledger.tiles
         assert e1.ledger.selector_invocations == e2.ledger.selector_invocations
+
+
+def _oracle_pages(ref_pools):
+    out = []
+    for dense, pool in ((1, ref_pools.dense), (0, ref_pools.streaming)):
+        for kv in sorted(pool):
+            for pg in pool[kv].live():
+                out.append((dense, kv, pg))
+    return out
+
+
+@pytest.mark.parametrize("bits", [4, 8, 3, None])
+def test_decode_appends_bit_exact_across_formats(bits):
+    """Misaligned context (1000 tokens, open page of 40) + 40 decode steps:
+    every page (codes, scale/zero, logical stats) equals the oracle's after
+    the fused incremental / page-opening appends; outputs within tolerance."""
+    rng = np.random.default_rng(21 + (bits or 0))
+    s, h, h_kv, d = 1000, 8, 2, 128
+    gates = [0.9, 0.1, 0.8, 0.2, 0.05, 0.15, 0.12, 0.11]  # kv 1 all-streaming -> ring pool
+    cfg = sk.EngineConfig(quant_bits=bits, budget_tokens=384, reuse_interval=3, local_blocks=2)
+    prof = sk.classify_heads(gates, 0.75, 1, 2)
+    k = rng.standard_normal((s, h_kv, d)).astype(np.float16).astype(np.float32)
+    v = rng.standard_normal((s, h_kv, d)).astype(np.float16).astype(np.float32)
+    eng = sk.Engine(cfg, prof, device="cuda:0")
+    eng.load_context(k, v)
+    ref = O.OracleEngine(O.Config(quant_bits=bits, budget_tokens=384, reuse_interval=3, local_blocks=2),
+                         O.assign_roles(gates, 0.75, 1, 2))
+    ref.load_context(k, v)
+    for t in range(40):
+        scale = 1.0 + 3.0 * (t % 5 == 0)  # occasional out-of-range tokens move page bounds
+        qn = rng.standard_normal((h, d)).astype(np.float16).astype(np.float32)
+        kn = (rng.standard_normal((h_kv, d)) * scale).astype(np.float16).astype(np.float32)
+        vn = (rng.standard_normal((h_kv, d)) * scale).astype(np.float16).astype(np.float32)
+        res = eng.decode_step(qn, kn, vn)
+        rr = ref.decode_step(qn, kn, vn)
+        assert [tuple(tb.positions) for tb in res.index_tables] == rr.tables, f"step {t}"
+        assert_close_attn(res.output, rr.output)
+    mine = [(1, kv, pg) for kv in sorted(eng.cache.dense_pool) for pg in eng.cache.dense_pool[kv].live_pages()] + \
+           [(0, kv, pg) for kv in sorted(eng.cache.streaming_pool) for pg in eng.cache.streaming_pool[kv].live_pages()]
+    theirs = _oracle_pages(ref.pools)
+    assert [(a, b, c.page_id, c.token_count) for a, b, c in mine] == \
+        [(a, b, c.index, c.tokens) for a, b, c in theirs]
+    for (_, _, pg), (_, _, rp) in zip(mine, theirs):
+        t = pg.token_count
+        np.testing.assert_array_equal(pg.k_codes[:t], rp.k_codes[:t])
+        np.testing.assert_array_equal(pg.v_codes[:t], rp.v_codes[:t])
+        for name in ("k_scale", "k_zero", "v_scale", "v_zero"):
+            np.testing.assert_array_equal(getattr(pg, name), getattr(rp, name))
+        assert len(pg.stats) == len(rp.bounds)
+        for st, (kmin, kmax, cov) in zip(pg.stats, rp.bounds):
+            np.testing.assert_array_equal(st.k_min, kmin)
+            np.testing.assert_array_equal(st.k_max, kmax)
+            assert st.covered_tokens == cov
