@@ -498,6 +498,18 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // stage every split's partial (m, l, O[D]) of this stream in smem with one
+  // coalesced sweep (serialised L2 round trips would dominate the step)
+  float* stage = reinterpret_cast<float*>(smem);  // [n_used][G][part_stride]
+  {
+    const int per_split = G * part_stride;
+    const float* src = prm.ws_part + (int64_t)s * prm.max_splits * kMaxRows * part_stride;
+    for (int i = tid; i < n_used * per_split; i += kDecThreads) {
+      const int sp = i / per_split, rem = i % per_split;
+      stage[i] = __ldcg(src + (int64_t)sp * kMaxRows * part_stride + rem);
+    }
+  }
+  __syncthreads();
   for (int rr = warp; rr < G; rr += kWarps) {
     const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)rr * prm.q_rs;
     float dot = 0.f;
@@ -505,23 +517,22 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
     const float s_self = dot * sl2;
-    const float* pbase = prm.ws_part + (int64_t)s * prm.max_splits * kMaxRows * part_stride + rr * part_stride;
+    const float* pb = stage + rr * part_stride;
+    const int sstride = G * part_stride;
     float M = s_self;
-    for (int sp = 0; sp < n_used; ++sp) M = fmaxf(M, __ldcg(pbase + (int64_t)sp * kMaxRows * part_stride));
+    for (int sp = 0; sp < n_used; ++sp) M = fmaxf(M, pb[sp * sstride]);
     float L = exp2f(s_self - M);
     for (int sp = 0; sp < n_used; ++sp) {
-      const float* pp = pbase + (int64_t)sp * kMaxRows * part_stride;
-      float pm = __ldcg(pp);
-      L += pm == -INFINITY ? 0.f : exp2f(pm - M) * __ldcg(pp + 1);
+      const float pm = pb[sp * sstride];
+      L += pm == -INFINITY ? 0.f : exp2f(pm - M) * pb[sp * sstride + 1];
     }
     const float inv_L = 1.f / L;
     const float fs = exp2f(s_self - M);
     for (int c = lane; c < D; c += 32) {
       float O = fs * DT<T>::to_f(vn[c]);
       for (int sp = 0; sp < n_used; ++sp) {
-        const float* pp = pbase + (int64_t)sp * kMaxRows * part_stride;
-        float pm = __ldcg(pp);
-        if (pm != -INFINITY) O = fmaf(exp2f(pm - M), __ldcg(pp + 2 + c), O);
+        const float pm = pb[sp * sstride];
+        if (pm != -INFINITY) O = fmaf(exp2f(pm - M), pb[sp * sstride + 2 + c], O);
       }
       O *= inv_L;
       int64_t oi = s * prm.out_ss + (int64_t)rr * prm.out_rs + c;
@@ -630,6 +641,8 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   size_t smem_app = fuse_append ? append_smem_bytes(pool->head_dim, pool->page_size) : 0;
   size_t smem_one = (size_t)2 * pool->head_dim * (4 + 3 * 8 + 1);
   if (smem_app < smem_one) smem_app = smem_one;
+  size_t smem_comb = (size_t)max_splits * group_rows * (2 + pool->head_dim) * 4;
+  if (smem_app < smem_comb) smem_app = smem_comb;
   size_t smem = smem_merge > smem_app ? smem_merge : smem_app;
   dim3 grid(max_splits, n_streams);
   cudaStream_t st = static_cast<cudaStream_t>(stream);

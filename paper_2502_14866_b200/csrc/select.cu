@@ -146,7 +146,8 @@ __device__ void score_pages_cta(const PoolView& pv, int s, int n_tok, const T* q
   }
 }
 
-// Phase 2: top-k of one stream (whole CTA).
+// Phase 2: top-k of one stream (whole CTA).  `scores` may point to shared
+// memory (staged) or global memory.
 __device__ void topk_cta(const double* scores, int n, int K, int32_t* sel_out, int32_t* sel_count) {
   __shared__ uint32_t hist[256];
   __shared__ uint32_t sh_bin, sh_kk, sh_done, sh_base;
@@ -175,7 +176,7 @@ __device__ void topk_cta(const double* scores, int n, int K, int32_t* sel_out, i
     __syncthreads();
     for (int i = tid; i < n; i += blockDim.x) {
       if (is_pin(i, n)) continue;
-      uint64_t key = order_key(__ldcg(scores + i));
+      uint64_t key = order_key(scores[i]);
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
     }
     __syncthreads();
@@ -222,7 +223,7 @@ __device__ void topk_cta(const double* scores, int n, int K, int32_t* sel_out, i
     int i = base + tid;
     bool valid = i < n;
     bool pinned = valid && is_pin(i, n);
-    uint64_t key = valid && !pinned ? order_key(__ldcg(scores + i)) : 0;
+    uint64_t key = valid && !pinned ? order_key(scores[i]) : 0;
     uint64_t km = key & mask;
     bool gt = valid && !pinned && km > prefix;
     bool eq = valid && !pinned && km == prefix;
@@ -260,7 +261,8 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(PoolView pv, const 
                                                              const int32_t* __restrict__ tokens,
                                                              const uint8_t* __restrict__ invoke, int K,
                                                              int32_t* sel_out, int32_t* sel_count, int sel_stride,
-                                                             double* ws_scores, uint32_t* ws_ticket, int ws_pages) {
+                                                             double* ws_scores, uint32_t* ws_ticket, int ws_pages,
+                                                             int stage_smem) {
   const int s = blockIdx.y;
   if (invoke != nullptr && invoke[s] == 0) return;
   const uint32_t rmask = row_mask[s];
@@ -283,7 +285,14 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(PoolView pv, const 
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  topk_cta(scores, n_pages, K, sel_out + (int64_t)s * sel_stride, sel_count + s);
+  extern __shared__ double s_scores[];
+  const double* src = scores;
+  if (stage_smem && !trivial) {
+    for (int i = threadIdx.x; i < n_pages; i += blockDim.x) s_scores[i] = __ldcg(scores + i);
+    __syncthreads();
+    src = s_scores;
+  }
+  topk_cta(src, n_pages, K, sel_out + (int64_t)s * sel_stride, sel_count + s);
 }
 
 template <typename T>
@@ -294,9 +303,16 @@ int select_dispatch(const PoolView& pv, int n_streams, int group_rows, const voi
   const int LP = pv.P / pv.L;
   dim3 grid((max_pages + kPagesPerCta - 1) / kPagesPerCta, n_streams);
   const T* qt = static_cast<const T*>(q);
-#define SK_SEL(R, LPV)                                                                                    \
-  select_kernel<T, R, LPV><<<grid, kSelThreads, 0, st>>>(pv, qt, q_ss, q_rs, row_mask, tokens, invoke, K, \
-                                                          sel_out, sel_count, sel_stride, scores, ticket, max_pages)
+  const size_t smem = (size_t)max_pages * 8;
+  const int stage = smem <= 160 * 1024 ? 1 : 0;
+#define SK_SEL(R, LPV)                                                                                         \
+  do {                                                                                                         \
+    if (stage)                                                                                                 \
+      cudaFuncSetAttribute(select_kernel<T, R, LPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    select_kernel<T, R, LPV><<<grid, kSelThreads, stage ? smem : 0, st>>>(                                    \
+        pv, qt, q_ss, q_rs, row_mask, tokens, invoke, K, sel_out, sel_count, sel_stride, scores, ticket,       \
+        max_pages, stage);                                                                                     \
+  } while (0)
   int rows = group_rows;
   if (LP == 4 && rows <= 4) SK_SEL(4, 4);
   else if (LP == 4 && rows <= 8) SK_SEL(8, 4);

@@ -1,0 +1,19 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum launch list (csv)."""
+import collections
+import csv
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+h = rows[hdr]
+ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+agg = collections.OrderedDict()
+for r in rows[hdr + 1:]:
+    if len(r) <= vi:
+        continue
+    us = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+    agg.setdefault(r[ki].split("(")[0][:70], []).append(us)
+tot = sum(sum(v) for v in agg.values())
+for k, v in agg.items():
+    print(f"{k:70s} n={len(v):4d} mean={sum(v) / len(v):11.2f} us  total={sum(v):12.1f} us  share={100 * sum(v) / tot:5.1f}%")
