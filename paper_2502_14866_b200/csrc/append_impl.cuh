@@ -6,6 +6,9 @@
 
 namespace sk {
 
+__host__ __device__ inline size_t append_one_smem_bytes(int D, int P) {
+  return (size_t)2 * D * (4 + 3 * 8) + ((2 * D + 15) & ~15) + (size_t)2 * P * D * 2;
+}
 __host__ __device__ inline size_t append_smem_bytes(int D, int P) {
   return (size_t)2 * P * D * 2 + 6 * D * sizeof(double);
 }
@@ -211,7 +214,7 @@ __device__ void append_page(const PoolView& pv, int s, int p, int n0, int n1, co
 // to append_page(): a channel whose min/max did not move keeps its lo and
 // scale, so only the new token's code changes; channels whose bounds moved
 // are re-coded for every token of the page from the raw staging copy.
-// Whole CTA; smem >= 2*D*(4 + 3*8 + 1) bytes.
+// Whole CTA; smem >= append_one_smem_bytes(D, P).
 template <typename T>
 __device__ void append_one_token(const PoolView& pv, int s, int n_tok, const T* __restrict__ kn,
                                  const T* __restrict__ vn, uint8_t* smem) {
@@ -232,7 +235,14 @@ __device__ void append_one_token(const PoolView& pv, int s, int n_tok, const T* 
   double* sc = lo + 2 * D;
   double* inv = sc + 2 * D;
   uint8_t* chg = reinterpret_cast<uint8_t*>(inv + 2 * D);  // [2][D]
+  T* raw = reinterpret_cast<T*>(chg + ((2 * D + 15) & ~15));  // [2][t_old][D] staged raw tokens
   const int levels = (1 << pv.bits) - 1;
+  // the open page's raw tokens -> smem (one coalesced sweep; code_at reads them often)
+  for (int i = threadIdx.x; i < 2 * t_old * (D / 8); i += blockDim.x) {
+    const int which = i / (t_old * (D / 8)), rem = i % (t_old * (D / 8));
+    *reinterpret_cast<uint4*>(raw + (which * t_old) * D + rem * 8) =
+        *reinterpret_cast<const uint4*>(stg[which] + rem * 8);
+  }
   for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) {
     const int which = i / D, c = i % D;
     const float x = DT<T>::to_f((which ? vn : kn)[c]);
@@ -255,9 +265,9 @@ __device__ void append_one_token(const PoolView& pv, int s, int n_tok, const T* 
   __syncthreads();
   auto code_at = [&](int which, int t, int c) -> uint32_t {
     if (t > t_old) return 0u;  // padding slots of the page
-    const float raw = t == t_old ? xnew[which * D + c] : DT<T>::to_f(stg[which][t * D + c]);
+    const float x = t == t_old ? xnew[which * D + c] : DT<T>::to_f(raw[(which * t_old + t) * D + c]);
     const int i = which * D + c;
-    return quant_code((double)raw, lo[i], sc[i], inv[i], levels);
+    return quant_code((double)x, lo[i], sc[i], inv[i], levels);
   };
   uint32_t* kw = reinterpret_cast<uint32_t*>(pv.k_codes(slot));
   uint32_t* vw = reinterpret_cast<uint32_t*>(pv.v_codes(slot));

@@ -639,7 +639,7 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
                                               (int64_t)n_streams * max_splits * kMaxRows * (2 + pool->head_dim) * 4);
   size_t smem_merge = (size_t)kWarps * kMaxRows * (2 + pool->head_dim) * 4;
   size_t smem_app = fuse_append ? append_smem_bytes(pool->head_dim, pool->page_size) : 0;
-  size_t smem_one = (size_t)2 * pool->head_dim * (4 + 3 * 8 + 1);
+  size_t smem_one = append_one_smem_bytes(pool->head_dim, pool->page_size);
   if (smem_app < smem_one) smem_app = smem_one;
   size_t smem_comb = (size_t)max_splits * group_rows * (2 + pool->head_dim) * 4;
   if (smem_app < smem_comb) smem_app = smem_comb;

@@ -20,7 +20,7 @@ namespace sk {
 namespace {
 
 constexpr int kSelThreads = 256;
-constexpr int kPagesPerWarp = 1;
+constexpr int kPagesPerWarp = 4;
 constexpr int kPagesPerCta = (kSelThreads / 32) * kPagesPerWarp;
 
 __device__ __forceinline__ int pins_of(int n, int* pin) {  // selector.py:75-78
@@ -99,28 +99,37 @@ __device__ void score_pages_cta(const PoolView& pv, int s, int n_tok, const T* q
       qm[r][c] = x < 0.0 ? x : 0.0;
     }
   }
-  for (int it = 0; it < kPagesPerWarp; ++it) {
-    int p = blockIdx.x * kPagesPerCta + it * (kSelThreads / 32) + warp;
-    if (p >= n_pages) break;
-    // issue every stats load of the page before any arithmetic (latency)
-    uint2 wmin[LP], wmax[LP];
+  // each warp walks kPagesPerWarp pages; the next page's stats are loaded
+  // while the current one is scored (register double buffer)
+  uint2 wmin[2][LP], wmax[2][LP];
+  auto load_page = [&](int p, int b) {
 #pragma unroll
     for (int j = 0; j < LP; ++j) {
       const int lp = min(p * LP + j, n_log - 1);  // clamp: invalid entries are masked below
       const T* st = reinterpret_cast<const T*>(pv.stats_ptr(s, lp));
       if (cpl == 4) {
-        wmin[j] = __ldcg(reinterpret_cast<const uint2*>(st + lane * 4));
-        wmax[j] = __ldcg(reinterpret_cast<const uint2*>(st + D + lane * 4));
+        wmin[b][j] = __ldcg(reinterpret_cast<const uint2*>(st + lane * 4));
+        wmax[b][j] = __ldcg(reinterpret_cast<const uint2*>(st + D + lane * 4));
       } else {
-        wmin[j] = make_uint2(__ldcg(reinterpret_cast<const uint32_t*>(st + lane * 2)), 0u);
-        wmax[j] = make_uint2(__ldcg(reinterpret_cast<const uint32_t*>(st + D + lane * 2)), 0u);
+        wmin[b][j] = make_uint2(__ldcg(reinterpret_cast<const uint32_t*>(st + lane * 2)), 0u);
+        wmax[b][j] = make_uint2(__ldcg(reinterpret_cast<const uint32_t*>(st + D + lane * 2)), 0u);
       }
     }
+  };
+  const int p0 = blockIdx.x * kPagesPerCta + warp;
+  constexpr int kStride = kSelThreads / 32;
+  if (p0 < n_pages) load_page(p0, 0);
+#pragma unroll
+  for (int it = 0; it < kPagesPerWarp; ++it) {
+    const int p = p0 + it * kStride;
+    if (p >= n_pages) break;
+    const int b = it & 1;
+    if (it + 1 < kPagesPerWarp && p + kStride < n_pages) load_page(p + kStride, b ^ 1);
     double v[NV];
 #pragma unroll
     for (int j = 0; j < LP; ++j) {
-      float2 a0 = DT<T>::to_f2(wmin[j].x), a1 = DT<T>::to_f2(wmin[j].y);
-      float2 b0 = DT<T>::to_f2(wmax[j].x), b1 = DT<T>::to_f2(wmax[j].y);
+      float2 a0 = DT<T>::to_f2(wmin[b][j].x), a1 = DT<T>::to_f2(wmin[b][j].y);
+      float2 b0 = DT<T>::to_f2(wmax[b][j].x), b1 = DT<T>::to_f2(wmax[b][j].y);
       const double kmin[4] = {a0.x, a0.y, a1.x, a1.y}, kmax[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) {
@@ -139,11 +148,9 @@ __device__ void score_pages_cta(const PoolView& pv, int s, int n_tok, const T* q
     double mine = (r < rows && p * LP + j < n_log) ? v[0] : -INFINITY;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) mine = fmax(mine, __shfl_xor_sync(0xffffffffu, mine, off));
-    if (lane == 0) {
-      scores[p] = mine;
-      __threadfence();  // publish before the CTA's ticket
-    }
+    if (lane == 0) scores[p] = mine;
   }
+  if (lane == 0) __threadfence();  // publish before the CTA's ticket
 }
 
 // Phase 2: top-k of one stream (whole CTA).  `scores` may point to shared
