@@ -1,0 +1,79 @@
+"""Isolate decode/select kernel costs at 128k: CUDA-event timing of the raw
+ABI calls with features toggled (fused append on/off, streaming rows on/off,
+pages per split)."""
+import ctypes as C
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2502_14866_b200 as sk
+from paper_2502_14866_b200 import _device, _lib
+from paper_2502_14866_b200.selector import _Workspace
+
+ctx = int(os.environ.get("SK_CTX", 131072))
+H, HKV, D = 32, 8, 128
+lib = _lib.load()
+st = torch.cuda.current_stream().cuda_stream
+
+
+def make(gates):
+    cfg = sk.EngineConfig(quant_bits=4, budget_tokens=4096, reuse_interval=4, local_blocks=4)
+    prof = sk.classify_heads(gates, 0.5 if len(set(gates)) > 1 else 0.0, 1, 4)
+    e = sk.Engine(cfg, prof, device="cuda:0", capacity_tokens=ctx + 4096)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    k = torch.randn((ctx + 5, HKV, D), generator=g, device="cuda", dtype=torch.float16)
+    e.load_context(k, k)
+    return e
+
+
+def time_it(fn, n=20):
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(n):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / n * 1e3
+
+
+for name, gates in [("balanced", [0.9 - 0.001 * h if h % 4 < 2 else 0.1 + 0.001 * h for h in range(H)]),
+                    ("all-retrieval", [0.9] * H)]:
+    e = make(gates)
+    pool = e.cache.pool
+    g = e._group_size
+    q = torch.randn((H, D), device="cuda", dtype=torch.float16)
+    kn = torch.randn((HKV, D), device="cuda", dtype=torch.float16)
+    kp = 64
+    sel = torch.zeros((HKV, kp), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(HKV, dtype=torch.int32, device="cuda")
+    n_pages = -(-pool.tokens_host[0] // 64)
+    ws = _Workspace.get(pool.device, HKV, n_pages)
+    abi = pool.abi()
+
+    def sel_call():
+        rc = lib.sk_select_pages(C.byref(abi), HKV, g, q.data_ptr(), g * D, D, e._row_mask.data_ptr(),
+                                 pool.tokens.data_ptr(), None, kp, n_pages, sel.data_ptr(), cnt.data_ptr(), kp,
+                                 ws.data_ptr(), ws.numel(), st)
+        _lib.check(rc)
+
+    print(name, "select us", round(time_it(sel_call), 2))
+    for pps in (4, 8, 16):
+        for fuse in (0,):
+            units = 64 + 5
+            ms = -(-units // pps)
+            wsd = torch.zeros(lib.sk_decode_workspace(HKV, g, D, ms), dtype=torch.uint8, device="cuda")
+            out = torch.empty((H, D), dtype=torch.float16, device="cuda")
+
+            def dec_call():
+                rc = lib.sk_decode_attn(C.byref(abi), HKV, g, q.data_ptr(), g * D, D, kn.data_ptr(), kn.data_ptr(), D,
+                                        e._row_mask.data_ptr(), sel.data_ptr(), cnt.data_ptr(), kp,
+                                        pool.tokens.data_ptr(), C.c_float(1 / math.sqrt(D)), out.data_ptr(), g * D, D,
+                                        _lib.SK_F16, pps, ms, fuse, wsd.data_ptr(), wsd.numel(), st)
+                _lib.check(rc)
+
+            print(name, f"decode pps={pps} splits={ms} fuse={fuse} us", round(time_it(dec_call), 2))
