@@ -24,10 +24,12 @@
 namespace sk {
 namespace {
 
-constexpr int kDecThreads = 128;
+constexpr int kDecThreads = 256;
 constexpr int kWarps = kDecThreads / 32;
 constexpr int kMaxRows = 8;
 constexpr int kMaxExtra = 64;
+constexpr int kMaxSel = 2048;  // selection entries staged in smem
+constexpr int kMaxPps = 16;    // pages per split (CTA)
 
 struct DecodeParams {
   PoolView pv;
@@ -114,21 +116,30 @@ __device__ __forceinline__ bool contains(const int32_t* a, int n, int x) {
 }
 
 // KIND: 0 raw pages (MMA in T), 1 nibble codes, 2 byte codes (MMA in fp16).
-// NBUF: pages staged per warp in shared memory by cp.async (0 = read the
-// arena directly, 2 = double-buffered prefetch of the warp's next page).
-template <typename T, int KIND, int D, int P, int NBUF>
-__global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
+//
+// Work decomposition.  A CTA (8 warps) owns `pps` consecutive units (pages)
+// of one stream's union.  All of them are staged into shared memory with
+// one CTA-wide cp.async sweep, then each page is cut into P/16 token tiles
+// of 16 tokens and the (page, tile) items are dealt to the warps: a warp
+// runs QK for its 16 tokens (2 n-tiles x D/16 k-steps) and one PV k-step
+// over all D/8 channel tiles, keeping its own online-softmax state.  Short
+// per-warp chains + many resident warps hide the MMA / shuffle latencies
+// (one warp per page serialised ~3.5k dependent instructions).
+template <typename T, int KIND, int D, int P>
+__global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm) {
   using MT = typename std::conditional<KIND == 0, T, __half>::type;
   constexpr int NKS = D / 16;   // QK k-steps
-  constexpr int NNT = P / 8;    // QK n-tiles (8 tokens)
   constexpr int NCN = D / 8;    // PV n-tiles (8 channels)
-  constexpr int NPK = P / 16;   // PV k-steps (16 tokens)
+  constexpr int NTT = P / 16;   // 16-token tiles per page
   constexpr int QR = D / 4;     // q / o / bounds values per thread
   constexpr int RB = KIND == 0 ? 2 * D : (KIND == 1 ? D / 2 : D);  // code row bytes
   constexpr int SLOT_USED = 2 * P * RB + (KIND == 0 ? 0 : 8 * D);  // bytes of a slot the kernel reads
   extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_sel[kMaxSel];
   __shared__ int s_extra[kMaxExtra];
-  __shared__ int s_nextra;
+  __shared__ int s_page[kMaxPps];
+  __shared__ uint32_t s_um[kMaxPps];
+  __shared__ int s_nextra, s_nunits;
   __shared__ uint32_t s_last;
 
   const PoolView& pv = prm.pv;
@@ -144,62 +155,70 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
   const int nsel = rmask ? prm.sel_count[s] : 0;
   const int32_t* sel = prm.sel + (int64_t)s * prm.sel_stride;
   const int sink_end = min(pv.sink, n_pages), local_start = max(n_pages - pv.local, 0);
-  const int u_begin = split * prm.pps;
-  uint8_t* wbuf = smem + warp * (NBUF > 0 ? NBUF : 1) * SLOT_USED;
+  const int pps = prm.pps;
+  const int u_begin = split * pps;
 
-  auto prefetch = [&](int p, int b) {
-    const uint8_t* src = pv.slot_ptr(s, p);
-    uint8_t* dst = wbuf + b * SLOT_USED;
-    for (int i = lane; i < SLOT_USED / 16; i += 32) cp_async16(dst + 16 * i, src + 16 * i);
-    cp_async_commit();
-  };
-  // the warp's first page can start streaming before the union is known
-  int first_u = u_begin + warp;
-  bool first_issued = false;
-  if constexpr (NBUF > 0) {
-    if (first_u < nsel && first_u < u_begin + prm.pps) {
-      prefetch(sel[first_u], 0);
-      first_issued = true;
-    }
+  // ---- the stream's page union: selection (+ sink/local extras) -----------
+  // Extras are only needed by CTAs whose range reaches past the selection
+  // (and by whichever CTA ends up merging): the selection is staged in smem
+  // once so the membership tests never chain global loads.
+  const bool need_extras = smask != 0u;
+  if (need_extras) {
+    for (int i = tid; i < nsel; i += kDecThreads) s_sel[i] = sel[i];
   }
+  __syncthreads();
   if (tid == 0) {
     int ne = 0;
-    if (smask) {
+    if (need_extras) {
       for (int p = 0; p < n_pages && ne < kMaxExtra; ++p) {
         if (p >= sink_end && p < local_start) {
           p = local_start - 1;
           continue;
         }
-        if (!contains(sel, nsel, p)) s_extra[ne++] = p;
+        if (!contains(s_sel, nsel, p)) s_extra[ne++] = p;
       }
     }
     s_nextra = ne;
+    const int U = nsel + ne;
+    const int nu = max(0, min(U, u_begin + pps) - u_begin);
+    s_nunits = nu;
+    for (int i = 0; i < nu; ++i) {
+      const int u = u_begin + i;
+      int pg;
+      uint32_t um;
+      if (u < nsel) {
+        pg = sel[u];
+        um = rmask | ((smask && (pg < sink_end || pg >= local_start)) ? smask : 0u);
+      } else {
+        pg = s_extra[u - nsel];
+        um = smask;
+      }
+      s_page[i] = pg;
+      s_um[i] = um;
+    }
   }
   __syncthreads();
   const int U = nsel + s_nextra;
-  const int n_used = (U + prm.pps - 1) / prm.pps;
-  const int u_end = min(U, u_begin + prm.pps);
-  auto page_of = [&](int u, uint32_t& um) -> int {
-    if (u < nsel) {
-      int p = sel[u];
-      um = rmask | ((smask && (p < sink_end || p >= local_start)) ? smask : 0u);
-      return p;
-    }
-    um = smask;
-    return s_extra[u - nsel];
-  };
+  const int n_used = (U + pps - 1) / pps;
+  const int n_units = s_nunits;
+
+  // ---- stage the CTA's pages in smem (one cp.async sweep) -------------------
+  for (int i = 0; i < n_units; ++i) {
+    const uint8_t* src = pv.slot_ptr(s, s_page[i]);
+    uint8_t* dst = smem + i * SLOT_USED;
+    for (int c = tid; c < SLOT_USED / 16; c += kDecThreads) cp_async16(dst + 16 * c, src + 16 * c);
+  }
+  cp_async_commit();
 
   // ---- per-thread row state: row r (lane/4), dims/channels of j (lane%4) ----
   const bool row_ok = r < G;
-  float qf[QR];
+  uint32_t qw[QR / 2];  // the thread's q values, packed pairs in the input dtype (exact)
   {
     const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)(row_ok ? r : 0) * prm.q_rs;
 #pragma unroll
     for (int ri = 0; ri < D / 8; ++ri) {
       int d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j;
-      float2 v = DT<T>::to_f2(*reinterpret_cast<const uint32_t*>(qrow + d));
-      qf[2 * ri] = row_ok ? v.x : 0.f;
-      qf[2 * ri + 1] = row_ok ? v.y : 0.f;
+      qw[ri] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + d) : 0u;
     }
   }
   float o[QR];
@@ -208,31 +227,17 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
   float m_run = -INFINITY, l_run = 0.f;
   const float sl2 = prm.scale_log2;
   const float inv_levels = KIND == 0 ? 1.f : 1.f / float((1 << pv.bits) - 1);
+  cp_async_wait<0>();
+  __syncthreads();
 
-  int it = 0;
-  for (int u = first_u; u < u_end; u += kWarps, ++it) {
-    uint32_t um;
-    const int p = page_of(u, um);
-    const uint8_t* pg;
-    if constexpr (NBUF > 0) {
-      if (!first_issued || (NBUF == 1 && it > 0)) {
-        prefetch(p, 0);
-        first_issued = true;
-      }
-      const int un = u + kWarps;
-      if (NBUF == 2 && un < u_end) {
-        uint32_t um2;
-        prefetch(page_of(un, um2), (it + 1) & 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncwarp();
-      pg = wbuf + (NBUF == 2 ? (it & 1) : 0) * SLOT_USED;
-    } else {
-      pg = pv.slot_ptr(s, p);
-    }
+  for (int item = warp; item < n_units * NTT; item += kWarps) {
+    const int ui = item / NTT, tt = item % NTT;
+    const int p = s_page[ui];
+    const uint32_t um = s_um[ui];
+    const bool attend = row_ok && ((um >> r) & 1u);
+    const uint8_t* pg = smem + ui * SLOT_USED;
     const int tok_in_page = min(P, n_tok - p * P);
+    if (16 * tt >= tok_in_page) continue;  // tile past the open page's tokens
     const uint8_t* kc = pg;
     const uint8_t* vc = pg + P * RB;
     const T* bnd = reinterpret_cast<const T*>(pg + 2 * P * RB);
@@ -243,48 +248,44 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
     if constexpr (KIND == 0) {
 #pragma unroll
       for (int ks = 0; ks < NKS; ++ks) {
-        afr[ks][0] = pack2<MT>(qf[4 * ks], qf[4 * ks + 1]);
-        afr[ks][1] = pack2<MT>(qf[4 * ks + 2], qf[4 * ks + 3]);
+        afr[ks][0] = qw[2 * ks];  // raw pages: q is the A operand as is
+        afr[ks][1] = qw[2 * ks + 1];
       }
     } else {
-      float sk[QR];
-      const uint4* klo4 = reinterpret_cast<const uint4*>(bnd + j * QR);
-      const uint4* khi4 = reinterpret_cast<const uint4*>(bnd + D + j * QR);
-#pragma unroll
-      for (int i = 0; i < QR / 8; ++i) {
-        uint4 a = klo4[i], b = khi4[i];
-        uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          float2 lo = DT<T>::to_f2(aw[k]), hi = DT<T>::to_f2(bw[k]);
-          int idx = 8 * i + 2 * k;
-          float s0 = (hi.x - lo.x) * inv_levels, s1 = (hi.y - lo.y) * inv_levels;
-          sk[idx] = s0 > 0.f ? s0 : 1.f;
-          sk[idx + 1] = s1 > 0.f ? s1 : 1.f;
-          qz = fmaf(qf[idx], lo.x, qz);
-          qz = fmaf(qf[idx + 1], lo.y, qz);
-        }
-      }
+      // two sweeps over the page's K bounds (smem) keep register pressure low:
+      // (1) smax = max_d s_d (shared by the 4 lanes of a row) and qz = q . lo_k,
+      // (2) q' = q * s / smax packed straight into the A fragments.
+      const uint32_t* klo = reinterpret_cast<const uint32_t*>(bnd + j * QR);
+      const uint32_t* khi = reinterpret_cast<const uint32_t*>(bnd + D + j * QR);
       float mx = 0.f;
 #pragma unroll
-      for (int i = 0; i < QR; ++i) mx = fmaxf(mx, sk[i]);
+      for (int i = 0; i < QR / 2; ++i) {
+        const float2 lo = DT<T>::to_f2(klo[i]), hi = DT<T>::to_f2(khi[i]), qv = DT<T>::to_f2(qw[i]);
+        float s0 = (hi.x - lo.x) * inv_levels, s1 = (hi.y - lo.y) * inv_levels;
+        mx = fmaxf(mx, fmaxf(s0 > 0.f ? s0 : 1.f, s1 > 0.f ? s1 : 1.f));
+        qz = fmaf(qv.x, lo.x, qz);
+        qz = fmaf(qv.y, lo.y, qz);
+      }
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
       qz += __shfl_xor_sync(0xffffffffu, qz, 1);
       qz += __shfl_xor_sync(0xffffffffu, qz, 2);
       smax = mx;
-      const float inv_mx = 1.f / mx;
+      const float f = inv_levels / mx;
 #pragma unroll
-      for (int ks = 0; ks < NKS; ++ks) {
-        afr[ks][0] = pack2<MT>(qf[4 * ks] * sk[4 * ks] * inv_mx, qf[4 * ks + 1] * sk[4 * ks + 1] * inv_mx);
-        afr[ks][1] = pack2<MT>(qf[4 * ks + 2] * sk[4 * ks + 2] * inv_mx, qf[4 * ks + 3] * sk[4 * ks + 3] * inv_mx);
+      for (int i = 0; i < QR / 2; ++i) {
+        const float2 lo = DT<T>::to_f2(klo[i]), hi = DT<T>::to_f2(khi[i]), qv = DT<T>::to_f2(qw[i]);
+        const float d0 = hi.x - lo.x, d1 = hi.y - lo.y;
+        const float s0 = d0 > 0.f ? d0 * f : 1.f / mx, s1 = d1 > 0.f ? d1 * f : 1.f / mx;
+        afr[i / 2][i % 2] = pack2<MT>(qv.x * s0, qv.y * s1);
       }
     }
 
-    // ---- S = q' K^T over the page's NNT n-tiles of 8 tokens ----
-    float sc[NNT][2];
+    // ---- S = q' K^T for the tile's two n-tiles of 8 tokens ----
+    float sc[2][2];
 #pragma unroll
-    for (int nt = 0; nt < NNT; ++nt) {
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int nt = 2 * tt + h2;
       const int tok = 8 * nt + r;  // B operand: n = lane/4
       float c[4] = {0.f, 0.f, 0.f, 0.f};
       if constexpr (KIND == 1) {
@@ -331,33 +332,26 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
       for (int e = 0; e < 2; ++e) {
         int t = 8 * nt + 2 * j + e;
         float v = (c[e] * smax + qz) * sl2;
-        sc[nt][e] = t < tok_in_page ? v : -INFINITY;
+        sc[h2][e] = t < tok_in_page ? v : -INFINITY;
       }
     }
 
-    // ---- online softmax for row r (4 lanes j share a row) ----
-    const bool attend = row_ok && ((um >> r) & 1u);
-    float tmax = -INFINITY;
-#pragma unroll
-    for (int nt = 0; nt < NNT; ++nt) tmax = fmaxf(tmax, fmaxf(sc[nt][0], sc[nt][1]));
+    // ---- online softmax for row r over the 16 tokens (4 lanes j share a row) ----
+    float tmax = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
     tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
     tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
     const float m_new = attend ? fmaxf(m_run, tmax) : m_run;
     const float alpha = attend ? exp2f(m_run - m_new) : 1.f;  // exp2(-inf) = 0
-    uint32_t pfr[NPK][2];
+    uint32_t pfr[2];
     float psum = 0.f;
 #pragma unroll
-    for (int ks = 0; ks < NPK; ++ks) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int nt = 2 * ks + h;
-        float p0 = attend ? exp2f(sc[nt][0] - m_new) : 0.f;
-        float p1 = attend ? exp2f(sc[nt][1] - m_new) : 0.f;
-        uint32_t pk = pack2<MT>(p0, p1);
-        float2 pr = unpack2<MT>(pk);  // the rounded values the MMA sees
-        psum += pr.x + pr.y;
-        pfr[ks][h] = pk;
-      }
+    for (int h2 = 0; h2 < 2; ++h2) {
+      float p0 = attend ? exp2f(sc[h2][0] - m_new) : 0.f;
+      float p1 = attend ? exp2f(sc[h2][1] - m_new) : 0.f;
+      uint32_t pk = pack2<MT>(p0, p1);
+      float2 pr = unpack2<MT>(pk);  // the rounded values the MMA sees
+      psum += pr.x + pr.y;
+      pfr[h2] = pk;
     }
     l_run = l_run * alpha + psum;  // per-thread partial (tokens of lane j)
     m_run = m_new;
@@ -365,75 +359,42 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
     prow += __shfl_xor_sync(0xffffffffu, prow, 1);
     prow += __shfl_xor_sync(0xffffffffu, prow, 2);
 
-    // ---- O += P V : C fragment row r, channels 8cn + 2j + {0,1} ----
-    float sv[2 * NCN], vlo[2 * NCN];
-    if constexpr (KIND != 0) {
-      const uint4* vlo4 = reinterpret_cast<const uint4*>(bnd + 2 * D + j * QR);
-      const uint4* vhi4 = reinterpret_cast<const uint4*>(bnd + 3 * D + j * QR);
-#pragma unroll
-      for (int i = 0; i < QR / 8; ++i) {
-        uint4 a = vlo4[i], b = vhi4[i];
-        uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          float2 lo = DT<T>::to_f2(aw[k]), hi = DT<T>::to_f2(bw[k]);
-          int idx = 8 * i + 2 * k;
-          float s0 = (hi.x - lo.x) * inv_levels, s1 = (hi.y - lo.y) * inv_levels;
-          sv[idx] = s0 > 0.f ? s0 : 1.f;
-          sv[idx + 1] = s1 > 0.f ? s1 : 1.f;
-          vlo[idx] = lo.x;
-          vlo[idx + 1] = lo.y;
-        }
-      }
-    }
+    // ---- O += P V over the tile's 16 tokens: one k-step per channel n-tile ----
+    const int ri0 = 2 * tt, ri1 = 2 * tt + 1;
 #pragma unroll
     for (int cn = 0; cn < NCN; ++cn) {
       float c[4] = {0.f, 0.f, 0.f, 0.f};
       const int vl = 32 * cn + lane;  // (cn, lane) chunk
+      uint32_t b0, b1;
       if constexpr (KIND == 1) {
-        constexpr int NW = P / 32;
-        uint32_t wd[NW];
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(vc + vl * (P / 8));
-        if constexpr (NW == 2) {
-          uint2 v = *reinterpret_cast<const uint2*>(src);
-          wd[0] = v.x; wd[1] = v.y;
-        } else {
-#pragma unroll
-          for (int i = 0; i < NW; ++i) wd[i] = src[i];
-        }
-#pragma unroll
-        for (int ks = 0; ks < NPK; ++ks) {
-          int ri0 = 2 * ks, ri1 = 2 * ks + 1;
-          mma16816<MT>(c, pfr[ks][0], 0u, pfr[ks][1], 0u, nib2h(wd[ri0 / 4], ri0 % 4), nib2h(wd[ri1 / 4], ri1 % 4));
-        }
+        const uint32_t w = reinterpret_cast<const uint32_t*>(vc + vl * (P / 8))[ri0 / 4];
+        b0 = nib2h(w, ri0 % 4);
+        b1 = nib2h(w, ri1 % 4);
       } else if constexpr (KIND == 2) {
-        constexpr int NW = P / 16;
-        uint32_t wd[NW];
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(vc + vl * (P / 4));
-#pragma unroll
-        for (int i = 0; i < NW; ++i) wd[i] = src[i];
-#pragma unroll
-        for (int ks = 0; ks < NPK; ++ks)
-          mma16816<MT>(c, pfr[ks][0], 0u, pfr[ks][1], 0u, byte2h(wd[ks], 0), byte2h(wd[ks], 1));
+        const uint32_t w = reinterpret_cast<const uint32_t*>(vc + vl * (P / 4))[tt];
+        b0 = byte2h(w, 0);
+        b1 = byte2h(w, 1);
       } else {
-        constexpr int NW = P / 8;
-        uint32_t wd[NW];
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(vc + vl * (P / 2));
-#pragma unroll
-        for (int i = 0; i < NW; ++i) wd[i] = src[i];
-#pragma unroll
-        for (int ks = 0; ks < NPK; ++ks) mma16816<MT>(c, pfr[ks][0], 0u, pfr[ks][1], 0u, wd[2 * ks], wd[2 * ks + 1]);
+        const uint2 w = reinterpret_cast<const uint2*>(vc + vl * (P / 2))[tt];
+        b0 = w.x;
+        b1 = w.y;
       }
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        float add = KIND == 0 ? c[e] : fmaf(sv[2 * cn + e], c[e], vlo[2 * cn + e] * prow);
-        o[2 * cn + e] = fmaf(o[2 * cn + e], alpha, add);
+      mma16816<MT>(c, pfr[0], 0u, pfr[1], 0u, b0, b1);
+      float add0 = c[0], add1 = c[1];
+      if constexpr (KIND != 0) {
+        // channels 8cn+2j, +1 are adjacent in the permuted bounds (vbound_pos)
+        const float2 lo = DT<T>::to_f2(*reinterpret_cast<const uint32_t*>(bnd + 2 * D + j * QR + 2 * cn));
+        const float2 hi = DT<T>::to_f2(*reinterpret_cast<const uint32_t*>(bnd + 3 * D + j * QR + 2 * cn));
+        const float s0 = (hi.x - lo.x) * inv_levels, s1 = (hi.y - lo.y) * inv_levels;
+        add0 = fmaf(s0 > 0.f ? s0 : 1.f, c[0], lo.x * prow);
+        add1 = fmaf(s1 > 0.f ? s1 : 1.f, c[1], lo.y * prow);
       }
+      o[2 * cn] = fmaf(o[2 * cn], alpha, add0);
+      o[2 * cn + 1] = fmaf(o[2 * cn + 1], alpha, add1);
     }
-    if constexpr (NBUF > 0) __syncwarp();  // buffer may be refilled next iteration
   }
 
-  // ---- merge the 4 warps of this CTA (rows < kMaxRows) ----
+  // ---- merge the 8 warps of this CTA (rows < kMaxRows) ----
   __syncthreads();  // page buffers are reused as the merge area
   float* sm_m = reinterpret_cast<float*>(smem);  // [kWarps][8]
   float* sm_l = sm_m + kWarps * kMaxRows;        // [kWarps][8]
@@ -482,7 +443,7 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecodeParams prm) {
   const bool opens_page = (n_tok % P) == 0;
   if (prm.fuse_append && !opens_page) {
     const int u_last = nsel > 0 ? nsel - 1 : U - 1;
-    if (u_last >= u_begin && u_last < u_end) {
+    if (u_last >= u_begin && u_last < u_begin + n_units) {
       __syncthreads();  // smem is reused by the append
       append_one_token<T>(pv, s, n_tok, kn, vn, smem);
     }
@@ -559,10 +520,13 @@ __host__ __device__ constexpr int slot_used(int kind, int D, int P) {
 template <typename T, int KIND, int D, int P>
 int launch_one(const DecodeParams& prm, dim3 grid, size_t smem_min, cudaStream_t st) {
   constexpr int SLOT = slot_used(KIND, D, P);
-  constexpr int NBUF = (2 * kWarps * SLOT <= 160 * 1024) ? 2 : ((kWarps * SLOT <= 160 * 1024) ? 1 : 0);
-  size_t smem = (size_t)kWarps * (NBUF > 0 ? NBUF : 0) * SLOT;
+  size_t smem = (size_t)prm.pps * SLOT;
   if (smem < smem_min) smem = smem_min;
-  auto kern = decode_kernel<T, KIND, D, P, NBUF>;
+  if (smem > 220 * 1024) {
+    set_error("decode: pages_per_split too large for shared memory");
+    return SK_EINVAL;
+  }
+  auto kern = decode_kernel<T, KIND, D, P>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, kDecThreads, smem, st>>>(prm);
   SK_CHECK_LAUNCH("decode_kernel");
@@ -604,7 +568,8 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   if (rc) return rc;
   SK_CHECK_ARG(n_streams >= 1, "decode: no streams");
   SK_CHECK_ARG(group_rows >= 1 && group_rows <= kMaxRows, "decode: group size must be in [1, 8]");
-  SK_CHECK_ARG(pages_per_split >= 1 && max_splits >= 1, "decode: bad split geometry");
+  SK_CHECK_ARG(pages_per_split >= 1 && pages_per_split <= kMaxPps && max_splits >= 1, "decode: bad split geometry");
+  SK_CHECK_ARG(sel_stride <= kMaxSel, "decode: selection wider than 2048 pages");
   SK_CHECK_ARG(pool->sink + pool->local <= kMaxExtra, "decode: sink + local window too large");
   SK_CHECK_ARG(out_dtype == SK_F16 || out_dtype == SK_BF16 || out_dtype == SK_F32, "decode: bad out dtype");
   SK_CHECK_ARG(workspace_bytes >= sk_decode_workspace(n_streams, group_rows, pool->head_dim, max_splits),

@@ -62,7 +62,7 @@ class DecodeGraph:
         self.sel = [torch.zeros((self.h_kv, width), dtype=torch.int32, device=self.dev) for _ in engines]
         self.cnt = [torch.zeros(self.h_kv, dtype=torch.int32, device=self.dev) for _ in engines]
         units = max(selection_size(self.max_pages_hint, self.k_pages), 1) + cfg.sink_blocks + cfg.local_blocks
-        self.pps = 4
+        self.pps = max(1, 128 // cfg.physical_page)  # 8 warps x 16-token tiles per CTA
         self.max_splits = -(-units // self.pps)
         need = _lib.load().sk_decode_workspace(self.h_kv, self.g, self.dp, self.max_splits)
         self.dec_ws = [torch.zeros(need, dtype=torch.uint8, device=self.dev) for _ in engines]

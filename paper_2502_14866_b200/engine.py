@@ -362,7 +362,7 @@ class Engine:
         sel, cnt = self._sel if self._sel is not None else (
             torch.zeros((h_kv, 4), dtype=torch.int32, device=dev), torch.zeros(h_kv, dtype=torch.int32, device=dev))
         units = max(selection_size(n_pages, k_pages), 1) + cfg.sink_blocks + cfg.local_blocks
-        pps = 4 if h_kv * units <= 4 * 148 * 2 else 8
+        pps = max(1, 128 // cfg.physical_page)  # 8 warps x 16-token tiles per CTA
         max_splits = -(-units // pps)
         ws = self._decode_workspace(h_kv, max_splits, pool.Dp)
         out = torch.empty((h_kv * g, pool.Dp), dtype=self._dtype, device=dev)

@@ -62,7 +62,7 @@ for name, gates in [("balanced", [0.9 - 0.001 * h if h % 4 < 2 else 0.1 + 0.001 
         _lib.check(rc)
 
     print(name, "select us", round(time_it(sel_call), 2))
-    for pps in (4, 8, 16):
+    for pps in (1, 2, 4):
         for fuse in (0,):
             units = 64 + 5
             ms = -(-units // pps)
