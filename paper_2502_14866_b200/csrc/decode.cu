@@ -459,16 +459,16 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // stage every split's partial (m, l, O[D]) of this stream in smem with one
-  // coalesced sweep (serialised L2 round trips would dominate the step)
-  float* stage = reinterpret_cast<float*>(smem);  // [n_used][G][part_stride]
-  {
-    const int per_split = G * part_stride;
-    const float* src = prm.ws_part + (int64_t)s * prm.max_splits * kMaxRows * part_stride;
-    for (int i = tid; i < n_used * per_split; i += kDecThreads) {
-      const int sp = i / per_split, rem = i % per_split;
-      stage[i] = __ldcg(src + (int64_t)sp * kMaxRows * part_stride + rem);
-    }
+  // Parallel merge of the n_used split partials (m, l, O[D]) + the new token:
+  //  (A) split maxima -> smem, (B) one warp per row: row max, rescale factors,
+  //  denominator, (C) one thread per (row, channel): sum_sp fac * O_sp.
+  const float* wsp = prm.ws_part + (int64_t)s * prm.max_splits * kMaxRows * part_stride;
+  float* fac = reinterpret_cast<float*>(smem);  // [G][n_used]
+  float* row_l = fac + G * n_used;               // [G]
+  float* row_f = row_l + G;                      // [G] factor of the new token
+  for (int i = tid; i < G * n_used; i += kDecThreads) {
+    const int rr = i / n_used, sp = i % n_used;
+    fac[i] = __ldcg(wsp + ((int64_t)sp * kMaxRows + rr) * part_stride);
   }
   __syncthreads();
   for (int rr = warp; rr < G; rr += kWarps) {
@@ -478,29 +478,38 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
     const float s_self = dot * sl2;
-    const float* pb = stage + rr * part_stride;
-    const int sstride = G * part_stride;
     float M = s_self;
-    for (int sp = 0; sp < n_used; ++sp) M = fmaxf(M, pb[sp * sstride]);
-    float L = exp2f(s_self - M);
-    for (int sp = 0; sp < n_used; ++sp) {
-      const float pm = pb[sp * sstride];
-      L += pm == -INFINITY ? 0.f : exp2f(pm - M) * pb[sp * sstride + 1];
+    for (int sp = lane; sp < n_used; sp += 32) M = fmaxf(M, fac[rr * n_used + sp]);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    float L = 0.f;
+    for (int sp = lane; sp < n_used; sp += 32) {
+      const float pm = fac[rr * n_used + sp];
+      const float f = pm == -INFINITY ? 0.f : exp2f(pm - M);
+      L = fmaf(f, __ldcg(wsp + ((int64_t)sp * kMaxRows + rr) * part_stride + 1), L);
+      fac[rr * n_used + sp] = f;
     }
-    const float inv_L = 1.f / L;
-    const float fs = exp2f(s_self - M);
-    for (int c = lane; c < D; c += 32) {
-      float O = fs * DT<T>::to_f(vn[c]);
-      for (int sp = 0; sp < n_used; ++sp) {
-        const float pm = pb[sp * sstride];
-        if (pm != -INFINITY) O = fmaf(exp2f(pm - M), pb[sp * sstride + 2 + c], O);
-      }
-      O *= inv_L;
-      int64_t oi = s * prm.out_ss + (int64_t)rr * prm.out_rs + c;
-      if (prm.out_dtype == SK_F32) reinterpret_cast<float*>(prm.out)[oi] = O;
-      else if (prm.out_dtype == SK_F16) reinterpret_cast<__half*>(prm.out)[oi] = __float2half_rn(O);
-      else reinterpret_cast<__nv_bfloat16*>(prm.out)[oi] = __float2bfloat16_rn(O);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+    if (lane == 0) {
+      const float fs = exp2f(s_self - M);
+      row_l[rr] = L + fs;
+      row_f[rr] = fs;
     }
+  }
+  __syncthreads();
+  for (int i = tid; i < G * D; i += kDecThreads) {
+    const int rr = i / D, c = i % D;
+    float O = row_f[rr] * DT<T>::to_f(vn[c]);
+    const float* fr = fac + rr * n_used;
+    const float* src = wsp + (int64_t)rr * part_stride + 2 + c;
+#pragma unroll 4
+    for (int sp = 0; sp < n_used; ++sp) O = fmaf(fr[sp], __ldcg(src + (int64_t)sp * kMaxRows * part_stride), O);
+    O /= row_l[rr];
+    const int64_t oi = s * prm.out_ss + (int64_t)rr * prm.out_rs + c;
+    if (prm.out_dtype == SK_F32) reinterpret_cast<float*>(prm.out)[oi] = O;
+    else if (prm.out_dtype == SK_F16) reinterpret_cast<__half*>(prm.out)[oi] = __float2half_rn(O);
+    else reinterpret_cast<__nv_bfloat16*>(prm.out)[oi] = __float2bfloat16_rn(O);
   }
   if (prm.fuse_append) {
     if (opens_page) {
@@ -606,7 +615,7 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   size_t smem_app = fuse_append ? append_smem_bytes(pool->head_dim, pool->page_size) : 0;
   size_t smem_one = append_one_smem_bytes(pool->head_dim, pool->page_size);
   if (smem_app < smem_one) smem_app = smem_one;
-  size_t smem_comb = (size_t)max_splits * group_rows * (2 + pool->head_dim) * 4;
+  size_t smem_comb = (size_t)(max_splits + 2) * group_rows * 4;
   if (smem_app < smem_comb) smem_app = smem_comb;
   size_t smem = smem_merge > smem_app ? smem_merge : smem_app;
   dim3 grid(max_splits, n_streams);
