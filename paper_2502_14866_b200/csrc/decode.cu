@@ -25,6 +25,25 @@ namespace sk {
 namespace {
 
 constexpr int kDecThreads = 256;
+
+// Debug timeline: %globaltimer stamps at phase boundaries for the first
+// CTA(s) of stream 0 (build with -DSK_DECODE_TIMING; read via sk_debug_times).
+#ifdef SK_DECODE_TIMING
+__device__ unsigned long long g_dec_times[64][10];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SK_STAMP(i)                                                                        \
+  do {                                                                                     \
+    if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < 64) g_dec_times[blockIdx.x][(i) + 1] = gtimer(); \
+  } while (0)
+#else
+#define SK_STAMP(i) \
+  do {              \
+  } while (0)
+#endif
 constexpr int kWarps = kDecThreads / 32;
 constexpr int kMaxRows = 8;
 constexpr int kMaxExtra = 64;
@@ -135,6 +154,9 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
   constexpr int RB = KIND == 0 ? 2 * D : (KIND == 1 ? D / 2 : D);  // code row bytes
   constexpr int SLOT_USED = 2 * P * RB + (KIND == 0 ? 0 : 8 * D);  // bytes of a slot the kernel reads
   extern __shared__ __align__(16) uint8_t smem[];
+#ifdef SK_DECODE_TIMING
+  if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < 64) g_dec_times[blockIdx.x][0] = gtimer();
+#endif
   __shared__ int s_sel[kMaxSel];
   __shared__ int s_extra[kMaxExtra];
   __shared__ int s_page[kMaxPps];
@@ -198,6 +220,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
     }
   }
   __syncthreads();
+  SK_STAMP(0);
   const int U = nsel + s_nextra;
   const int n_used = (U + pps - 1) / pps;
   const int n_units = s_nunits;
@@ -229,6 +252,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
   const float inv_levels = KIND == 0 ? 1.f : 1.f / float((1 << pv.bits) - 1);
   cp_async_wait<0>();
   __syncthreads();
+  SK_STAMP(1);
 
   for (int item = warp; item < n_units * NTT; item += kWarps) {
     const int ui = item / NTT, tt = item % NTT;
@@ -396,6 +420,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
 
   // ---- merge the 8 warps of this CTA (rows < kMaxRows) ----
   __syncthreads();  // page buffers are reused as the merge area
+  SK_STAMP(2);
   float* sm_m = reinterpret_cast<float*>(smem);  // [kWarps][8]
   float* sm_l = sm_m + kWarps * kMaxRows;        // [kWarps][8]
   float* sm_o = sm_l + kWarps * kMaxRows;        // [kWarps][8][D]
@@ -413,6 +438,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
       for (int e = 0; e < 2; ++e) sm_o[(warp * kMaxRows + r) * D + 8 * cn + 2 * j + e] = o[2 * cn + e];
   }
   __syncthreads();
+  SK_STAMP(3);
   const int part_stride = 2 + D;
   float* part = prm.ws_part + ((int64_t)s * prm.max_splits + split) * kMaxRows * part_stride;
   if (split < n_used) {
@@ -450,6 +476,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
   }
   // ---- last CTA of the stream: merge splits + the new token, write ----
   __syncthreads();
+  SK_STAMP(4);
   if (tid == 0) {
     __threadfence();
     uint32_t t = atomicAdd(prm.ws_ticket + s, 1u);
@@ -458,6 +485,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
   }
   __syncthreads();
   if (!s_last) return;
+  SK_STAMP(5);
   __threadfence();
   // Parallel merge of the n_used split partials (m, l, O[D]) + the new token:
   //  (A) split maxima -> smem, (B) one warp per row: row max, rescale factors,
@@ -498,6 +526,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
     }
   }
   __syncthreads();
+  SK_STAMP(6);
   for (int i = tid; i < G * D; i += kDecThreads) {
     const int rr = i / D, c = i % D;
     float O = row_f[rr] * DT<T>::to_f(vn[c]);
@@ -518,6 +547,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
       append_page<T>(pv, s, n_tok / P, n_tok, n_tok + 1, kn, vn, 0, smem);
     }
     __syncthreads();
+  SK_STAMP(7);
     if (tid == 0) prm.tokens[s] = n_tok + 1;
   }
 }
@@ -629,4 +659,13 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   if (kind == 0) return launch_kind<__nv_bfloat16, 0>(prm, grid, smem, st);
   if (kind == 1) return launch_kind<__nv_bfloat16, 1>(prm, grid, smem, st);
   return launch_kind<__nv_bfloat16, 2>(prm, grid, smem, st);
+}
+
+extern "C" int sk_debug_decode_times(unsigned long long* host_out) {
+#ifdef SK_DECODE_TIMING
+  return cudaMemcpyFromSymbol(host_out, sk::g_dec_times, sizeof(sk::g_dec_times)) == cudaSuccess ? 0 : -2;
+#else
+  (void)host_out;
+  return -3;
+#endif
 }
