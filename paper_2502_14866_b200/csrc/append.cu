@@ -28,6 +28,20 @@ __global__ void __launch_bounds__(256) append_kernel(PoolView pv, const T* __res
   append_page<T>(pv, s, p, n0, n1, k_src + s * src_ss, v_src + s * src_ss, src_ts, smem);
 }
 
+// One new token per stream (decode): one CTA per stream, incremental page
+// update (append_one_token) or a fresh page, then the stream's counter.
+template <typename T>
+__global__ void __launch_bounds__(256) append_one_kernel(PoolView pv, const T* __restrict__ k_src,
+                                                         const T* __restrict__ v_src, int64_t src_ss,
+                                                         int32_t* __restrict__ tokens) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int s = blockIdx.x;
+  const int n0 = tokens[s];
+  append_one_token<T>(pv, s, n0, k_src + s * src_ss, v_src + s * src_ss, smem);
+  __syncthreads();
+  if (threadIdx.x == 0) tokens[s] = n0 + 1;
+}
+
 __global__ void advance_tokens_kernel(int32_t* tokens, int n, int m) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) tokens[i] += m;
@@ -41,10 +55,26 @@ int append_launch(const sk_pool* pool, int n_streams, const void* k_src, const v
   if (rc) return rc;
   SK_CHECK_ARG(n_streams >= 1 && m >= 1 && max_pages_touched >= 1, "append: empty launch");
   SK_CHECK_ARG(k_src && v_src && tokens, "append: NULL pointer");
-  SK_CHECK_ARG(ss % 8 == 0 && ts % 8 == 0, "append: source strides must be multiples of 8 elements");
+  SK_CHECK_ARG(ss % 8 == 0 && (ts % 8 == 0 || m == 1), "append: source strides must be multiples of 8 elements");
   SK_CHECK_ARG(pool->page_size % (pool->bits >= 1 && pool->bits <= 4 ? 32 : 16) == 0,
                "append: page_size must be a multiple of 32 (<=4-bit codes) or 16");
   PoolView pv = make_view(*pool);
+  if (m == 1) {
+    size_t smem1 = append_smem_bytes(pv.D, pv.P);
+    size_t smem2 = append_one_smem_bytes(pv.D, pv.P);
+    size_t sm = smem1 > smem2 ? smem1 : smem2;
+    if (pv.dtype == SK_F16) {
+      cudaFuncSetAttribute(append_one_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      append_one_kernel<__half><<<n_streams, 256, sm, st>>>(pv, (const __half*)k_src, (const __half*)v_src, ss,
+                                                           tokens);
+    } else {
+      cudaFuncSetAttribute(append_one_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      append_one_kernel<__nv_bfloat16><<<n_streams, 256, sm, st>>>(pv, (const __nv_bfloat16*)k_src,
+                                                                  (const __nv_bfloat16*)v_src, ss, tokens);
+    }
+    SK_CHECK_LAUNCH("append_one_kernel");
+    return SK_OK;
+  }
   size_t smem = append_smem_bytes(pv.D, pv.P);
   dim3 grid(max_pages_touched, n_streams);
   if (pv.dtype == SK_F16) {

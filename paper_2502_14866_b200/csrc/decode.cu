@@ -19,6 +19,11 @@
 // (atomic ticket) together with the new token's raw K/V, then -- if asked --
 // that CTA appends the new token to its page (K1's page rebuild).
 #include "append_impl.cuh"
+
+namespace sk {
+int append_launch(const sk_pool* pool, int n_streams, const void* k_src, const void* v_src, int64_t ss, int64_t ts,
+                  int32_t* tokens, int m, int max_pages_touched, cudaStream_t st);
+}  // namespace sk
 #include "sk_sm100.cuh"
 
 namespace sk {
@@ -169,29 +174,36 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = lane >> 2, j = lane & 3;
   const int G = prm.G;
-  const int n_tok = prm.tokens[s];
-  const int n_pages = (n_tok + P - 1) / P;
-  const uint32_t gmask = (G >= 32) ? 0xffffffffu : ((1u << G) - 1u);
-  const uint32_t rmask = prm.row_mask[s] & gmask;
-  const uint32_t smask = gmask & ~rmask;
-  const int nsel = rmask ? prm.sel_count[s] : 0;
-  const int32_t* sel = prm.sel + (int64_t)s * prm.sel_stride;
-  const int sink_end = min(pv.sink, n_pages), local_start = max(n_pages - pv.local, 0);
   const int pps = prm.pps;
   const int u_begin = split * pps;
-
-  // ---- the stream's page union: selection (+ sink/local extras) -----------
-  // Extras are only needed by CTAs whose range reaches past the selection
-  // (and by whichever CTA ends up merging): the selection is staged in smem
-  // once so the membership tests never chain global loads.
-  const bool need_extras = smask != 0u;
-  if (need_extras) {
-    for (int i = tid; i < nsel; i += kDecThreads) s_sel[i] = sel[i];
+  const int32_t* sel = prm.sel + (int64_t)s * prm.sel_stride;
+  // ---- one parallel round of header loads (no dependent global chains) ----
+  const int n_tok = prm.tokens[s];
+  const uint32_t rm_raw = prm.row_mask[s];
+  const int cnt_raw = prm.sel_count[s];
+  const int sel_w = min(prm.sel_stride, kMaxSel);
+  for (int i = tid; i < sel_w; i += kDecThreads) s_sel[i] = sel[i];
+  const bool row_ok = r < G;
+  uint32_t qw[QR / 2];  // the thread's q values, packed pairs in the input dtype (exact)
+  {
+    const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)(row_ok ? r : 0) * prm.q_rs;
+#pragma unroll
+    for (int ri = 0; ri < D / 8; ++ri) {
+      int d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j;
+      qw[ri] = *reinterpret_cast<const uint32_t*>(qrow + d);
+    }
   }
+  const int n_pages = (n_tok + P - 1) / P;
+  const uint32_t gmask = (G >= 32) ? 0xffffffffu : ((1u << G) - 1u);
+  const uint32_t rmask = rm_raw & gmask;
+  const uint32_t smask = gmask & ~rmask;
+  const int nsel = rmask ? cnt_raw : 0;
+  const int sink_end = min(pv.sink, n_pages), local_start = max(n_pages - pv.local, 0);
   __syncthreads();
+  // ---- the stream's page union from smem: selection + sink/local extras ----
   if (tid == 0) {
     int ne = 0;
-    if (need_extras) {
+    if (smask) {
       for (int p = 0; p < n_pages && ne < kMaxExtra; ++p) {
         if (p >= sink_end && p < local_start) {
           p = local_start - 1;
@@ -209,7 +221,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
       int pg;
       uint32_t um;
       if (u < nsel) {
-        pg = sel[u];
+        pg = s_sel[u];
         um = rmask | ((smask && (pg < sink_end || pg >= local_start)) ? smask : 0u);
       } else {
         pg = s_extra[u - nsel];
@@ -234,15 +246,9 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
   cp_async_commit();
 
   // ---- per-thread row state: row r (lane/4), dims/channels of j (lane%4) ----
-  const bool row_ok = r < G;
-  uint32_t qw[QR / 2];  // the thread's q values, packed pairs in the input dtype (exact)
-  {
-    const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)(row_ok ? r : 0) * prm.q_rs;
+  if (!row_ok) {
 #pragma unroll
-    for (int ri = 0; ri < D / 8; ++ri) {
-      int d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j;
-      qw[ri] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + d) : 0u;
-    }
+    for (int ri = 0; ri < D / 8; ++ri) qw[ri] = 0u;
   }
   float o[QR];
 #pragma unroll
@@ -463,17 +469,6 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
   }
   const T* kn = reinterpret_cast<const T*>(prm.k_new) + s * prm.new_ss;
   const T* vn = reinterpret_cast<const T*>(prm.v_new) + s * prm.new_ss;
-  // The new token joins an open page (t_old > 0): the only reader of that page
-  // in this step is the unit holding page n_pages-1, so the CTA that owns it
-  // appends right after its own reads -- off the critical serial tail.
-  const bool opens_page = (n_tok % P) == 0;
-  if (prm.fuse_append && !opens_page) {
-    const int u_last = nsel > 0 ? nsel - 1 : U - 1;
-    if (u_last >= u_begin && u_last < u_begin + n_units) {
-      __syncthreads();  // smem is reused by the append
-      append_one_token<T>(pv, s, n_tok, kn, vn, smem);
-    }
-  }
   // ---- last CTA of the stream: merge splits + the new token, write ----
   __syncthreads();
   SK_STAMP(4);
@@ -488,17 +483,20 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
   SK_STAMP(5);
   __threadfence();
   // Parallel merge of the n_used split partials (m, l, O[D]) + the new token:
-  //  (A) split maxima -> smem, (B) one warp per row: row max, rescale factors,
-  //  denominator, (C) one thread per (row, channel): sum_sp fac * O_sp.
-  const float* wsp = prm.ws_part + (int64_t)s * prm.max_splits * kMaxRows * part_stride;
-  float* fac = reinterpret_cast<float*>(smem);  // [G][n_used]
-  float* row_l = fac + G * n_used;               // [G]
-  float* row_f = row_l + G;                      // [G] factor of the new token
-  for (int i = tid; i < G * n_used; i += kDecThreads) {
-    const int rr = i / n_used, sp = i % n_used;
-    fac[i] = __ldcg(wsp + ((int64_t)sp * kMaxRows + rr) * part_stride);
+  // stage the G rows of every split in smem with independent coalesced loads,
+  // then one warp per row reduces (max, factors, denominator) and one thread
+  // per (row, channel) sums the rescaled partial outputs.
+  const int ps = part_stride;
+  float* stg = reinterpret_cast<float*>(smem);  // [n_used][G * ps]
+  float* row_l = stg + n_used * G * ps;         // [G]
+  float* row_f = row_l + G;                     // [G] factor of the new token
+  {
+    const float* wsp = prm.ws_part + (int64_t)s * prm.max_splits * kMaxRows * ps;
+    for (int sp = warp; sp < n_used; sp += kWarps)
+      for (int idx = lane; idx < G * ps; idx += 32) stg[sp * G * ps + idx] = __ldcg(wsp + (int64_t)sp * kMaxRows * ps + idx);
   }
   __syncthreads();
+  SK_STAMP(6);
   for (int rr = warp; rr < G; rr += kWarps) {
     const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)rr * prm.q_rs;
     float dot = 0.f;
@@ -507,15 +505,16 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
     for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
     const float s_self = dot * sl2;
     float M = s_self;
-    for (int sp = lane; sp < n_used; sp += 32) M = fmaxf(M, fac[rr * n_used + sp]);
+    for (int sp = lane; sp < n_used; sp += 32) M = fmaxf(M, stg[(sp * G + rr) * ps]);
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
     float L = 0.f;
     for (int sp = lane; sp < n_used; sp += 32) {
-      const float pm = fac[rr * n_used + sp];
+      float* cell = stg + (sp * G + rr) * ps;
+      const float pm = cell[0];
       const float f = pm == -INFINITY ? 0.f : exp2f(pm - M);
-      L = fmaf(f, __ldcg(wsp + ((int64_t)sp * kMaxRows + rr) * part_stride + 1), L);
-      fac[rr * n_used + sp] = f;
+      L = fmaf(f, cell[1], L);
+      cell[0] = f;  // the split's rescale factor for the output pass
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
@@ -526,29 +525,18 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
     }
   }
   __syncthreads();
-  SK_STAMP(6);
   for (int i = tid; i < G * D; i += kDecThreads) {
     const int rr = i / D, c = i % D;
     float O = row_f[rr] * DT<T>::to_f(vn[c]);
-    const float* fr = fac + rr * n_used;
-    const float* src = wsp + (int64_t)rr * part_stride + 2 + c;
-#pragma unroll 4
-    for (int sp = 0; sp < n_used; ++sp) O = fmaf(fr[sp], __ldcg(src + (int64_t)sp * kMaxRows * part_stride), O);
+    for (int sp = 0; sp < n_used; ++sp) {
+      const float* cell = stg + (sp * G + rr) * ps;
+      O = fmaf(cell[0], cell[2 + c], O);
+    }
     O /= row_l[rr];
     const int64_t oi = s * prm.out_ss + (int64_t)rr * prm.out_rs + c;
     if (prm.out_dtype == SK_F32) reinterpret_cast<float*>(prm.out)[oi] = O;
     else if (prm.out_dtype == SK_F16) reinterpret_cast<__half*>(prm.out)[oi] = __float2half_rn(O);
     else reinterpret_cast<__nv_bfloat16*>(prm.out)[oi] = __float2bfloat16_rn(O);
-  }
-  if (prm.fuse_append) {
-    if (opens_page) {
-      // a fresh page may reuse a streaming ring slot read in this step: only now is it free
-      __syncthreads();
-      append_page<T>(pv, s, n_tok / P, n_tok, n_tok + 1, kn, vn, 0, smem);
-    }
-    __syncthreads();
-  SK_STAMP(7);
-    if (tid == 0) prm.tokens[s] = n_tok + 1;
   }
 }
 
@@ -642,23 +630,24 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   prm.ws_ticket = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(workspace) +
                                               (int64_t)n_streams * max_splits * kMaxRows * (2 + pool->head_dim) * 4);
   size_t smem_merge = (size_t)kWarps * kMaxRows * (2 + pool->head_dim) * 4;
-  size_t smem_app = fuse_append ? append_smem_bytes(pool->head_dim, pool->page_size) : 0;
-  size_t smem_one = append_one_smem_bytes(pool->head_dim, pool->page_size);
-  if (smem_app < smem_one) smem_app = smem_one;
-  size_t smem_comb = (size_t)(max_splits + 2) * group_rows * 4;
-  if (smem_app < smem_comb) smem_app = smem_comb;
-  size_t smem = smem_merge > smem_app ? smem_merge : smem_app;
+  size_t smem_comb = ((size_t)max_splits * group_rows * (2 + pool->head_dim) + 2 * group_rows) * 4;
+  size_t smem = smem_merge > smem_comb ? smem_merge : smem_comb;
   dim3 grid(max_splits, n_streams);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int kind = pool->bits == 0 ? 0 : (pool->bits <= 4 ? 1 : 2);
+  int rc2;
   if (pool->dtype == SK_F16) {
-    if (kind == 0) return launch_kind<__half, 0>(prm, grid, smem, st);
-    if (kind == 1) return launch_kind<__half, 1>(prm, grid, smem, st);
-    return launch_kind<__half, 2>(prm, grid, smem, st);
+    rc2 = kind == 0 ? launch_kind<__half, 0>(prm, grid, smem, st)
+                    : (kind == 1 ? launch_kind<__half, 1>(prm, grid, smem, st) : launch_kind<__half, 2>(prm, grid, smem, st));
+  } else {
+    rc2 = kind == 0 ? launch_kind<__nv_bfloat16, 0>(prm, grid, smem, st)
+                    : (kind == 1 ? launch_kind<__nv_bfloat16, 1>(prm, grid, smem, st)
+                                 : launch_kind<__nv_bfloat16, 2>(prm, grid, smem, st));
   }
-  if (kind == 0) return launch_kind<__nv_bfloat16, 0>(prm, grid, smem, st);
-  if (kind == 1) return launch_kind<__nv_bfloat16, 1>(prm, grid, smem, st);
-  return launch_kind<__nv_bfloat16, 2>(prm, grid, smem, st);
+  if (rc2 != SK_OK || !fuse_append) return rc2;
+  // the new token is appended by K1's one-token kernel right behind the
+  // attention (stream order: every read of its page has completed)
+  return append_launch(pool, n_streams, k_new, v_new, new_stream_stride, 0, tokens, 1, 1, st);
 }
 
 extern "C" int sk_debug_decode_times(unsigned long long* host_out) {

@@ -69,14 +69,16 @@ class DecodeGraph:
         self.sel_ws = [torch.zeros(_lib.load().sk_select_workspace(self.h_kv, self.max_pages_hint),
                                    dtype=torch.uint8, device=self.dev) for _ in engines]
         self.graphs = {}
+        self._side = torch.cuda.Stream(device=self.dev)
         # prime selections (first step must select anyway) then capture
         self._capture()
 
     # -- launches ---------------------------------------------------------------
-    def _launch_layer(self, li: int, select: bool) -> None:
+    def _launch_layer(self, li: int, select: bool, side) -> None:
         e, pool = self.engines[li], self.pools[li]
         lib = _lib.load()
-        stream = _device.stream_ptr(self.dev)
+        main = torch.cuda.current_stream(self.dev)
+        stream = main.cuda_stream
         abi = pool.abi()
         if select:
             ws = self.sel_ws[li]
@@ -91,12 +93,20 @@ class DecodeGraph:
                                 self.sel[li].data_ptr(), self.cnt[li].data_ptr(), self.sel[li].shape[1],
                                 pool.tokens.data_ptr(), C.c_float(1.0 / math.sqrt(self.head_dim)),
                                 self.out[li].data_ptr(), self.g * self.dp, self.dp, _device.sk_dtype(self.dtype),
-                                self.pps, self.max_splits, 1, ws.data_ptr(), ws.numel(), stream)
+                                self.pps, self.max_splits, 0, ws.data_ptr(), ws.numel(), stream)
+        _lib.check(rc)
+        # K1 one-token append on a side stream: overlaps the next layer's attention
+        side.wait_stream(main)
+        rc = lib.sk_append_pages(C.byref(abi), self.h_kv, self.k[li].data_ptr(), self.v[li].data_ptr(), self.dp, 0,
+                                 pool.tokens.data_ptr(), 1, 1, side.cuda_stream)
         _lib.check(rc)
 
     def _launch_step(self, select: bool) -> None:
+        main = torch.cuda.current_stream(self.dev)
+        side = self._side
         for li in range(len(self.engines)):
-            self._launch_layer(li, select)
+            self._launch_layer(li, select, side)
+        main.wait_stream(side)
 
     def _capture(self) -> None:
         # capture mutates device token counters when kernels run? No: capture

@@ -63,7 +63,7 @@ for name, gates in [("balanced", [0.9 - 0.001 * h if h % 4 < 2 else 0.1 + 0.001 
 
     print(name, "select us", round(time_it(sel_call), 2))
     for pps in (1, 2, 4):
-        for fuse in (0,):
+        for fuse in (0, 1):
             units = 64 + 5
             ms = -(-units // pps)
             wsd = torch.zeros(lib.sk_decode_workspace(HKV, g, D, ms), dtype=torch.uint8, device="cuda")
