@@ -150,7 +150,7 @@ __device__ __forceinline__ bool contains(const int32_t* a, int n, int x) {
 // per-warp chains + many resident warps hide the MMA / shuffle latencies
 // (one warp per page serialised ~3.5k dependent instructions).
 template <typename T, int KIND, int D, int P>
-__global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm) {
+__global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(DecodeParams prm) {
   using MT = typename std::conditional<KIND == 0, T, __half>::type;
   constexpr int NKS = D / 16;   // QK k-steps
   constexpr int NCN = D / 8;    // PV n-tiles (8 channels)
@@ -182,7 +182,10 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
   const uint32_t rm_raw = prm.row_mask[s];
   const int cnt_raw = prm.sel_count[s];
   const int sel_w = min(prm.sel_stride, kMaxSel);
+  if (n_tok < 0) s_sel[0] = 0;  // keep n_tok live for the stamp below
+  SK_STAMP(6);
   for (int i = tid; i < sel_w; i += kDecThreads) s_sel[i] = sel[i];
+  SK_STAMP(7);
   const bool row_ok = r < G;
   uint32_t qw[QR / 2];  // the thread's q values, packed pairs in the input dtype (exact)
   {
@@ -200,24 +203,31 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
   const int nsel = rmask ? cnt_raw : 0;
   const int sink_end = min(pv.sink, n_pages), local_start = max(n_pages - pv.local, 0);
   __syncthreads();
+  SK_STAMP(8);
   // ---- the stream's page union from smem: selection + sink/local extras ----
-  if (tid == 0) {
+  // warp 0: each lane tests one sink/local candidate against the staged
+  // selection (binary search in smem), ballots keep the ascending order.
+  if (warp == 0) {
     int ne = 0;
     if (smask) {
-      for (int p = 0; p < n_pages && ne < kMaxExtra; ++p) {
-        if (p >= sink_end && p < local_start) {
-          p = local_start - 1;
-          continue;
-        }
-        if (!contains(s_sel, nsel, p)) s_extra[ne++] = p;
+      const int loc0 = max(local_start, sink_end);
+      const int ncand = sink_end + (n_pages - loc0);
+      for (int base = 0; base < ncand; base += 32) {
+        const int ci = base + lane;
+        const int p = ci < sink_end ? ci : loc0 + (ci - sink_end);
+        const bool extra = ci < ncand && !contains(s_sel, nsel, p);
+        const uint32_t bal = __ballot_sync(0xffffffffu, extra);
+        const int pos = ne + __popc(bal & ((1u << lane) - 1u));
+        if (extra && pos < kMaxExtra) s_extra[pos] = p;
+        ne += __popc(bal);
       }
+      ne = min(ne, kMaxExtra);
     }
-    s_nextra = ne;
-    const int U = nsel + ne;
-    const int nu = max(0, min(U, u_begin + pps) - u_begin);
-    s_nunits = nu;
-    for (int i = 0; i < nu; ++i) {
-      const int u = u_begin + i;
+    __syncwarp();
+    const int U0 = nsel + ne;
+    const int nu = max(0, min(U0, u_begin + pps) - u_begin);
+    if (lane < nu) {
+      const int u = u_begin + lane;
       int pg;
       uint32_t um;
       if (u < nsel) {
@@ -227,8 +237,12 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
         pg = s_extra[u - nsel];
         um = smask;
       }
-      s_page[i] = pg;
-      s_um[i] = um;
+      s_page[lane] = pg;
+      s_um[lane] = um;
+    }
+    if (lane == 0) {
+      s_nextra = ne;
+      s_nunits = nu;
     }
   }
   __syncthreads();
@@ -259,6 +273,39 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
   cp_async_wait<0>();
   __syncthreads();
   SK_STAMP(1);
+  // ---- per-page dequantisation tables, once per page (warp w -> page w) ----
+  // tab[0:D)  = s_k / smax  (K bounds order)   tab[D:2D)  = lo_k
+  // tab[2D:3D) = s_v         (V bounds order)   tab[3D:4D) = lo_v   tab[4D] = smax
+  constexpr int TAB = 4 * D + 4;
+  float* tabs = reinterpret_cast<float*>(smem + ((prm.pps * SLOT_USED + 15) & ~15));
+  if constexpr (KIND != 0) {
+    for (int i = warp; i < n_units; i += kWarps) {
+      const T* bnd = reinterpret_cast<const T*>(smem + i * SLOT_USED + 2 * P * RB);
+      float* tab = tabs + i * TAB;
+      float mx = 0.f;
+      float skv[D / 32];
+#pragma unroll
+      for (int q = 0; q < D / 32; ++q) {
+        const int x = lane + 32 * q;
+        const float lo = DT<T>::to_f(bnd[x]), hi = DT<T>::to_f(bnd[D + x]);
+        const float sv = (hi - lo) * inv_levels;
+        skv[q] = sv > 0.f ? sv : 1.f;
+        mx = fmaxf(mx, skv[q]);
+        tab[D + x] = lo;
+        const float vlo = DT<T>::to_f(bnd[2 * D + x]), vhi = DT<T>::to_f(bnd[3 * D + x]);
+        const float vs = (vhi - vlo) * inv_levels;
+        tab[2 * D + x] = vs > 0.f ? vs : 1.f;
+        tab[3 * D + x] = vlo;
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      const float inv = 1.f / mx;
+#pragma unroll
+      for (int q = 0; q < D / 32; ++q) tab[lane + 32 * q] = skv[q] * inv;
+      if (lane == 0) tab[4 * D] = mx;
+    }
+    __syncthreads();
+  }
 
   for (int item = warp; item < n_units * NTT; item += kWarps) {
     const int ui = item / NTT, tt = item % NTT;
@@ -275,6 +322,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
     // ---- K side: q' = q * s_k / smax (A fragments), qz = q . lo_k ----
     uint32_t afr[NKS][2];
     float smax = 1.f, qz = 0.f;
+    const float* tab = tabs + ui * TAB;
     if constexpr (KIND == 0) {
 #pragma unroll
       for (int ks = 0; ks < NKS; ++ks) {
@@ -282,33 +330,19 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
         afr[ks][1] = qw[2 * ks + 1];
       }
     } else {
-      // two sweeps over the page's K bounds (smem) keep register pressure low:
-      // (1) smax = max_d s_d (shared by the 4 lanes of a row) and qz = q . lo_k,
-      // (2) q' = q * s / smax packed straight into the A fragments.
-      const uint32_t* klo = reinterpret_cast<const uint32_t*>(bnd + j * QR);
-      const uint32_t* khi = reinterpret_cast<const uint32_t*>(bnd + D + j * QR);
-      float mx = 0.f;
+      const float4* kn4 = reinterpret_cast<const float4*>(tab + j * QR);
+      const float4* kl4 = reinterpret_cast<const float4*>(tab + D + j * QR);
 #pragma unroll
-      for (int i = 0; i < QR / 2; ++i) {
-        const float2 lo = DT<T>::to_f2(klo[i]), hi = DT<T>::to_f2(khi[i]), qv = DT<T>::to_f2(qw[i]);
-        float s0 = (hi.x - lo.x) * inv_levels, s1 = (hi.y - lo.y) * inv_levels;
-        mx = fmaxf(mx, fmaxf(s0 > 0.f ? s0 : 1.f, s1 > 0.f ? s1 : 1.f));
-        qz = fmaf(qv.x, lo.x, qz);
-        qz = fmaf(qv.y, lo.y, qz);
+      for (int ks = 0; ks < NKS; ++ks) {
+        const float4 f = kn4[ks], l = kl4[ks];
+        const float2 q0 = DT<T>::to_f2(qw[2 * ks]), q1 = DT<T>::to_f2(qw[2 * ks + 1]);
+        afr[ks][0] = pack2<MT>(q0.x * f.x, q0.y * f.y);
+        afr[ks][1] = pack2<MT>(q1.x * f.z, q1.y * f.w);
+        qz = fmaf(q0.x, l.x, fmaf(q0.y, l.y, fmaf(q1.x, l.z, fmaf(q1.y, l.w, qz))));
       }
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
       qz += __shfl_xor_sync(0xffffffffu, qz, 1);
       qz += __shfl_xor_sync(0xffffffffu, qz, 2);
-      smax = mx;
-      const float f = inv_levels / mx;
-#pragma unroll
-      for (int i = 0; i < QR / 2; ++i) {
-        const float2 lo = DT<T>::to_f2(klo[i]), hi = DT<T>::to_f2(khi[i]), qv = DT<T>::to_f2(qw[i]);
-        const float d0 = hi.x - lo.x, d1 = hi.y - lo.y;
-        const float s0 = d0 > 0.f ? d0 * f : 1.f / mx, s1 = d1 > 0.f ? d1 * f : 1.f / mx;
-        afr[i / 2][i % 2] = pack2<MT>(qv.x * s0, qv.y * s1);
-      }
+      smax = tab[4 * D];
     }
 
     // ---- S = q' K^T for the tile's two n-tiles of 8 tokens ----
@@ -412,12 +446,11 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
       mma16816<MT>(c, pfr[0], 0u, pfr[1], 0u, b0, b1);
       float add0 = c[0], add1 = c[1];
       if constexpr (KIND != 0) {
-        // channels 8cn+2j, +1 are adjacent in the permuted bounds (vbound_pos)
-        const float2 lo = DT<T>::to_f2(*reinterpret_cast<const uint32_t*>(bnd + 2 * D + j * QR + 2 * cn));
-        const float2 hi = DT<T>::to_f2(*reinterpret_cast<const uint32_t*>(bnd + 3 * D + j * QR + 2 * cn));
-        const float s0 = (hi.x - lo.x) * inv_levels, s1 = (hi.y - lo.y) * inv_levels;
-        add0 = fmaf(s0 > 0.f ? s0 : 1.f, c[0], lo.x * prow);
-        add1 = fmaf(s1 > 0.f ? s1 : 1.f, c[1], lo.y * prow);
+        // channels 8cn+2j, +1 are adjacent in the V table (vbound order)
+        const float2 sv = *reinterpret_cast<const float2*>(tab + 2 * D + j * QR + 2 * cn);
+        const float2 lo = *reinterpret_cast<const float2*>(tab + 3 * D + j * QR + 2 * cn);
+        add0 = fmaf(sv.x, c[0], lo.x * prow);
+        add1 = fmaf(sv.y, c[1], lo.y * prow);
       }
       o[2 * cn] = fmaf(o[2 * cn], alpha, add0);
       o[2 * cn + 1] = fmaf(o[2 * cn + 1], alpha, add1);
@@ -496,7 +529,6 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams prm
       for (int idx = lane; idx < G * ps; idx += 32) stg[sp * G * ps + idx] = __ldcg(wsp + (int64_t)sp * kMaxRows * ps + idx);
   }
   __syncthreads();
-  SK_STAMP(6);
   for (int rr = warp; rr < G; rr += kWarps) {
     const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)rr * prm.q_rs;
     float dot = 0.f;
@@ -547,7 +579,7 @@ __host__ __device__ constexpr int slot_used(int kind, int D, int P) {
 template <typename T, int KIND, int D, int P>
 int launch_one(const DecodeParams& prm, dim3 grid, size_t smem_min, cudaStream_t st) {
   constexpr int SLOT = slot_used(KIND, D, P);
-  size_t smem = (size_t)prm.pps * SLOT;
+  size_t smem = (((size_t)prm.pps * SLOT + 15) & ~(size_t)15) + (size_t)prm.pps * (4 * D + 4) * 4;
   if (smem < smem_min) smem = smem_min;
   if (smem > 220 * 1024) {
     set_error("decode: pages_per_split too large for shared memory");
