@@ -480,24 +480,33 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(DecodeParams prm
   SK_STAMP(3);
   const int part_stride = 2 + D;
   float* part = prm.ws_part + ((int64_t)s * prm.max_splits + split) * kMaxRows * part_stride;
+  // per-(warp, row) rescale factors once, then one FMA chain per output
+  float* sm_f = sm_o + kWarps * kMaxRows * D;  // [kWarps][8]
+  if (tid < G) {
+    const int rr = tid;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sm_m[w * kMaxRows + rr]);
+    float L = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const float f = M == -INFINITY ? 0.f : exp2f(sm_m[w * kMaxRows + rr] - M);
+      sm_f[w * kMaxRows + rr] = f;
+      L += f * sm_l[w * kMaxRows + rr];
+    }
+    if (split < n_used) {
+      part[rr * part_stride] = M;
+      part[rr * part_stride + 1] = L;
+    }
+  }
+  __syncthreads();
   if (split < n_used) {
     for (int i = tid; i < G * D; i += kDecThreads) {
-      int rr = i / D, c = i % D;
-      float M = -INFINITY;
+      const int rr = i / D, c = i % D;
+      float O = 0.f;
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sm_m[w * kMaxRows + rr]);
-      float L = 0.f, O = 0.f;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        float f = M == -INFINITY ? 0.f : exp2f(sm_m[w * kMaxRows + rr] - M);
-        L += f * sm_l[w * kMaxRows + rr];
-        O += f * sm_o[(w * kMaxRows + rr) * D + c];
-      }
+      for (int w = 0; w < kWarps; ++w) O = fmaf(sm_f[w * kMaxRows + rr], sm_o[(w * kMaxRows + rr) * D + c], O);
       part[rr * part_stride + 2 + c] = O;
-      if (c == 0) {
-        part[rr * part_stride] = M;
-        part[rr * part_stride + 1] = L;
-      }
     }
   }
   const T* kn = reinterpret_cast<const T*>(prm.k_new) + s * prm.new_ss;
@@ -661,7 +670,7 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   prm.ws_part = static_cast<float*>(workspace);
   prm.ws_ticket = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(workspace) +
                                               (int64_t)n_streams * max_splits * kMaxRows * (2 + pool->head_dim) * 4);
-  size_t smem_merge = (size_t)kWarps * kMaxRows * (2 + pool->head_dim) * 4;
+  size_t smem_merge = (size_t)kWarps * kMaxRows * (3 + pool->head_dim) * 4;
   size_t smem_comb = ((size_t)max_splits * group_rows * (2 + pool->head_dim) + 2 * group_rows) * 4;
   size_t smem = smem_merge > smem_comb ? smem_merge : smem_comb;
   dim3 grid(max_splits, n_streams);
