@@ -34,7 +34,7 @@ constexpr int kDecThreads = 256;
 // Debug timeline: %globaltimer stamps at phase boundaries for the first
 // CTA(s) of stream 0 (build with -DSK_DECODE_TIMING; read via sk_debug_times).
 #ifdef SK_DECODE_TIMING
-__device__ unsigned long long g_dec_times[64][10];
+__device__ unsigned long long g_dec_times[64][32];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -47,6 +47,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #else
 #define SK_STAMP(i) \
   do {              \
+  } while (0)
+#endif
+#ifdef SK_DECODE_TIMING
+#define SK_WSTAMP(i)                                                                                   \
+  do {                                                                                                 \
+    if ((threadIdx.x & 31) == 0 && blockIdx.y == 0 && blockIdx.x < 64)                               \
+      g_dec_times[blockIdx.x][(i) + (threadIdx.x >> 5)] = gtimer();                                    \
+  } while (0)
+#else
+#define SK_WSTAMP(i) \
+  do {               \
   } while (0)
 #endif
 constexpr int kWarps = kDecThreads / 32;
@@ -150,7 +161,10 @@ __device__ __forceinline__ bool contains(const int32_t* a, int n, int x) {
 // per-warp chains + many resident warps hide the MMA / shuffle latencies
 // (one warp per page serialised ~3.5k dependent instructions).
 template <typename T, int KIND, int D, int P>
-__global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(DecodeParams prm) {
+#ifndef SK_DEC_MINB
+#define SK_DEC_MINB 2
+#endif
+__global__ void __launch_bounds__(kDecThreads, SK_DEC_MINB) decode_kernel(DecodeParams prm) {
   using MT = typename std::conditional<KIND == 0, T, __half>::type;
   constexpr int NKS = D / 16;   // QK k-steps
   constexpr int NCN = D / 8;    // PV n-tiles (8 channels)
@@ -306,6 +320,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(DecodeParams prm
     }
     __syncthreads();
   }
+  SK_STAMP(9);
 
   for (int item = warp; item < n_units * NTT; item += kWarps) {
     const int ui = item / NTT, tt = item % NTT;
@@ -315,6 +330,9 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(DecodeParams prm
     const uint8_t* pg = smem + ui * SLOT_USED;
     const int tok_in_page = min(P, n_tok - p * P);
     if (16 * tt >= tok_in_page) continue;  // tile past the open page's tokens
+#if defined(SK_DBG) && SK_DBG == 4
+    continue;
+#endif
     const uint8_t* kc = pg;
     const uint8_t* vc = pg + P * RB;
     const T* bnd = reinterpret_cast<const T*>(pg + 2 * P * RB);
@@ -366,7 +384,11 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(DecodeParams prm
         for (int ks = 0; ks < NKS; ++ks) {
           int ri0 = 2 * ks, ri1 = 2 * ks + 1;
           uint32_t b0 = nib2h(wd[ri0 / 4], ri0 % 4), b1 = nib2h(wd[ri1 / 4], ri1 % 4);
+#if defined(SK_DBG) && SK_DBG == 1
+          c[0] += __uint_as_float(b0 ^ afr[ks][0]); c[1] += __uint_as_float(b1 ^ afr[ks][1]);
+#else
           mma16816<MT>(c, afr[ks][0], 0u, afr[ks][1], 0u, b0, b1);
+#endif
         }
       } else if constexpr (KIND == 2) {
         uint32_t wd[D / 16];
@@ -410,8 +432,13 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(DecodeParams prm
     float psum = 0.f;
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
+#if defined(SK_DBG) && SK_DBG == 3
+      float p0 = attend ? (sc[h2][0] - m_new) : 0.f;
+      float p1 = attend ? (sc[h2][1] - m_new) : 0.f;
+#else
       float p0 = attend ? exp2f(sc[h2][0] - m_new) : 0.f;
       float p1 = attend ? exp2f(sc[h2][1] - m_new) : 0.f;
+#endif
       uint32_t pk = pack2<MT>(p0, p1);
       float2 pr = unpack2<MT>(pk);  // the rounded values the MMA sees
       psum += pr.x + pr.y;
@@ -443,7 +470,11 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(DecodeParams prm
         b0 = w.x;
         b1 = w.y;
       }
+#if defined(SK_DBG) && SK_DBG == 2
+      c[0] = __uint_as_float(b0 ^ pfr[0]); c[1] = __uint_as_float(b1 ^ pfr[1]);
+#else
       mma16816<MT>(c, pfr[0], 0u, pfr[1], 0u, b0, b1);
+#endif
       float add0 = c[0], add1 = c[1];
       if constexpr (KIND != 0) {
         // channels 8cn+2j, +1 are adjacent in the V table (vbound order)
@@ -457,6 +488,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(DecodeParams prm
     }
   }
 
+  SK_WSTAMP(11);
   // ---- merge the 8 warps of this CTA (rows < kMaxRows) ----
   __syncthreads();  // page buffers are reused as the merge area
   SK_STAMP(2);

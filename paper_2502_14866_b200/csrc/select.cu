@@ -181,10 +181,22 @@ __device__ void topk_cta(const double* scores, int n, int K, int32_t* sel_out, i
   for (int shift = 56; shift >= 0; shift -= 8) {
     hist[tid] = 0;  // kSelThreads == 256
     __syncthreads();
-    for (int i = tid; i < n; i += blockDim.x) {
-      if (is_pin(i, n)) continue;
-      uint64_t key = order_key(scores[i]);
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
+    // warp-aggregated: lanes holding the same bin elect one leader per bin,
+    // so a pass where every key shares its top byte costs one shared atomic
+    // per warp instead of n serialised ones on the same address
+    for (int base = 0; base < n; base += blockDim.x) {
+      const int i = base + tid;
+      bool live = false;
+      uint32_t bin = 256u + lane;  // unique dummy bin for inactive lanes
+      if (i < n && !is_pin(i, n)) {
+        const uint64_t key = order_key(scores[i]);
+        if ((key & mask) == prefix) {
+          live = true;
+          bin = uint32_t(key >> shift) & 255u;
+        }
+      }
+      const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+      if (live && (__ffs(peers) - 1) == lane) atomicAdd(&hist[bin], uint32_t(__popc(peers)));
     }
     __syncthreads();
     if (warp == 0) {
@@ -279,7 +291,9 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(PoolView pv, const 
   double* scores = ws_scores + (int64_t)s * ws_pages;
   int pin[3];
   const bool trivial = K >= n_pages || K <= pins_of(n_pages, pin);
+#if !(defined(SK_DBG) && SK_DBG == 6)
   if (!trivial) score_pages_cta<T, RMAX, LP>(pv, s, n_tok, q + s * q_ss, q_rs, rmask, scores);
+#endif
   // last CTA of this stream runs the top-k
   __shared__ uint32_t is_last;
   __syncthreads();
@@ -291,6 +305,9 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(PoolView pv, const 
   }
   __syncthreads();
   if (!is_last) return;
+#if defined(SK_DBG) && SK_DBG == 5
+  return;
+#endif
   __threadfence();
   extern __shared__ double s_scores[];
   const double* src = scores;

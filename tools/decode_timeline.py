@@ -7,6 +7,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
+np.set_printoptions(linewidth=220, suppress=True)
 import torch
 
 import paper_2502_14866_b200 as sk
@@ -34,8 +35,8 @@ abi = pool.abi()
 _lib.check(lib.sk_select_pages(C.byref(abi), HKV, 4, q.data_ptr(), 4 * D, D, e._row_mask.data_ptr(),
                                pool.tokens.data_ptr(), None, 64, n_pages, sel.data_ptr(), cnt.data_ptr(), 64,
                                ws.data_ptr(), ws.numel(), st))
-names = ["start", "prologue", "staged", "items", "merged", "preticket", "ticket", "hdr", "selstg", "sync1"]
-for pps in (2,):
+names = ["start", "prologue", "staged", "items", "merged", "preticket", "ticket", "hdr", "selstg", "sync1", "tables"] + [f"w{i}" for i in range(8)]
+for pps in (2, 4):
     ms = -(-69 // pps)
     wsd = torch.zeros(lib.sk_decode_workspace(HKV, 4, D, ms), dtype=torch.uint8, device="cuda")
     out = torch.empty((H, D), dtype=torch.float16, device="cuda")
@@ -45,7 +46,7 @@ for pps in (2,):
                                       pool.tokens.data_ptr(), C.c_float(1 / math.sqrt(D)), out.data_ptr(), 4 * D, D,
                                       _lib.SK_F16, pps, ms, 0, wsd.data_ptr(), wsd.numel(), st))
         torch.cuda.synchronize()
-    buf = np.zeros((64, 10), np.uint64)
+    buf = np.zeros((64, 32), np.uint64)
     assert lib.sk_debug_decode_times(buf.ctypes.data) == 0
     n = int((buf[:, 0] > 0).sum())
     t0 = int(buf[:n, 0].min())
@@ -53,6 +54,6 @@ for pps in (2,):
     rel[buf[:n] == 0] = np.nan
     print(f"pps={pps} CTAs(stream0)={n}  columns: {names}")
     for i in range(0, n, max(1, n // 5)):
-        print("  cta", i, np.round(rel[i, :10], 2))
-    print("  median", np.round(np.nanmedian(rel[:, :10], axis=0), 2))
-    print("  max   ", np.round(np.nanmax(rel[:, :10], axis=0), 2))
+        print("  cta", i, np.round(rel[i, :19], 2))
+    print("  median", np.round(np.nanmedian(rel[:, :19], axis=0), 2))
+    print("  max   ", np.round(np.nanmax(rel[:, :19], axis=0), 2))
