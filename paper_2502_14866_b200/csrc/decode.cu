@@ -1,70 +1,52 @@
-// K3 -- split-KV decode attention over the selected pages (+ fused append).
+// K3 -- split-KV decode attention over the selected pages (+ append).
 //
 // Replaces the per-head page loop of Engine.decode_step (reference
 // engine.py:257-285), PhysicalPage.dequantize (cache.py:97-102) and
 // merge_block (attn.py:191-229).
 //
-// One CTA = one (stream, split); 4 warps each walk whole pages of the
-// stream's page union (the selection for retrieval rows + the sink/local
-// window for streaming rows, each page carrying the mask of group rows that
-// attend it).  Per page a warp runs m16n8k16 tensor-core MMAs directly on
-// the stored codes, using the dequantisation algebra
-//     q . khat_t = sum_d (q_d s_d) c_td + sum_d q_d lo_d
-//     sum_t p_t vhat_tc = s_c sum_t p_t c_tc + lo_c sum_t p_t
-// so codes are unpacked to exact fp16 integers with one LOP3 + one HSUB2 per
-// two codes (fragment-native layout written by K1, sk_layout.cuh) and never
-// materialised as floats.  Group rows sit in the MMA's M dimension (GQA
-// rows share every page load).  Online softmax in fp32 (exp2 domain); warps
-// merge in shared memory, splits merge in the last CTA of the stream
-// (atomic ticket) together with the new token's raw K/V, then -- if asked --
-// that CTA appends the new token to its page (K1's page rebuild).
+// Work decomposition (latency-first: a 128k decode step reads ~5 MB, less
+// than a microsecond of HBM time, so the kernel is built around the number
+// of dependent memory round trips, not bandwidth):
+//   * one thread-block CLUSTER of kCl CTAs per stream (= one KV head of one
+//     sequence); the stream's page union -- the selection for retrieval
+//     rows plus the sink/local window for streaming rows, each page carrying
+//     the mask of group rows that attend it -- is dealt round-robin to the
+//     cluster's warps, one whole page per warp;
+//   * a warp issues every load of its page straight into registers
+//     (128-bit, coalesced: K1 writes the codes in the m16n8k16 fragment
+//     order, sk_layout.cuh) before doing any math, then runs QK and PV as
+//     m16n8k16 tensor-core MMAs on the stored codes through the
+//     dequantisation algebra
+//         q . khat_t = sum_d (q_d s_d) c_td + sum_d q_d lo_d
+//         sum_t p_t vhat_tc = s_c sum_t p_t c_tc + lo_c sum_t p_t
+//     (codes -> exact fp16 integers with one LOP3 + one HSUB2 per two);
+//     group rows sit in the MMA's M dimension, so GQA rows share each load;
+//   * one online-softmax state per (warp, row); warps merge in shared
+//     memory, the kCl CTAs merge through distributed shared memory into
+//     cluster rank 0, which adds the new token's raw K/V in-register and
+//     writes the output.  No global workspace, atomics or grid fences.
+// Round trips on the critical path: {tokens, selection, q} -> page table ->
+// page data -> cluster barrier.
+#include <cooperative_groups.h>
+
 #include "append_impl.cuh"
 
 namespace sk {
 int append_launch(const sk_pool* pool, int n_streams, const void* k_src, const void* v_src, int64_t ss, int64_t ts,
                   int32_t* tokens, int m, int max_pages_touched, cudaStream_t st);
 }  // namespace sk
-#include "sk_sm100.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sk {
 namespace {
 
 constexpr int kDecThreads = 256;
-
-// Debug timeline: %globaltimer stamps at phase boundaries for the first
-// CTA(s) of stream 0 (build with -DSK_DECODE_TIMING; read via sk_debug_times).
-#ifdef SK_DECODE_TIMING
-__device__ unsigned long long g_dec_times[64][32];
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define SK_STAMP(i)                                                                        \
-  do {                                                                                     \
-    if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < 64) g_dec_times[blockIdx.x][(i) + 1] = gtimer(); \
-  } while (0)
-#else
-#define SK_STAMP(i) \
-  do {              \
-  } while (0)
-#endif
-#ifdef SK_DECODE_TIMING
-#define SK_WSTAMP(i)                                                                                   \
-  do {                                                                                                 \
-    if ((threadIdx.x & 31) == 0 && blockIdx.y == 0 && blockIdx.x < 64)                               \
-      g_dec_times[blockIdx.x][(i) + (threadIdx.x >> 5)] = gtimer();                                    \
-  } while (0)
-#else
-#define SK_WSTAMP(i) \
-  do {               \
-  } while (0)
-#endif
 constexpr int kWarps = kDecThreads / 32;
-constexpr int kMaxRows = 8;
-constexpr int kMaxExtra = 64;
+constexpr int kCl = 8;         // CTAs per stream (cluster size, portable)
+constexpr int kMaxRows = 8;    // group rows (query heads per KV head)
+constexpr int kMaxExtra = 64;  // sink + local pages
 constexpr int kMaxSel = 2048;  // selection entries staged in smem
-constexpr int kMaxPps = 16;    // pages per split (CTA)
 
 struct DecodeParams {
   PoolView pv;
@@ -78,34 +60,28 @@ struct DecodeParams {
   const int32_t* sel;
   const int32_t* sel_count;
   int sel_stride;
-  int32_t* tokens;
+  const int32_t* tokens;
   float scale_log2;
   void* out;
   int64_t out_ss, out_rs;
   int out_dtype;
-  int pps;
-  int fuse_append;
-  float* ws_part;
-  uint32_t* ws_ticket;
-  int max_splits;
 };
 
-// m16n8k16 MMA, fp32 accumulate.  MT = __half or __nv_bfloat16 operands.
+// m16n8k16 MMA, fp32 accumulate; rows 8..15 of A are zero (group rows <= 8).
 template <typename MT>
-__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
   if constexpr (std::is_same<MT, __half>::value) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};"
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
   } else {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};"
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
   }
 }
 
@@ -138,6 +114,9 @@ __device__ __forceinline__ uint32_t byte2h(uint32_t w, int r2) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+__device__ __forceinline__ uint4 ldg16(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+__device__ __forceinline__ uint2 ldg8(const void* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
+
 // Binary search in an ascending int list.
 __device__ __forceinline__ bool contains(const int32_t* a, int n, int x) {
   int lo = 0, hi = n;
@@ -150,77 +129,277 @@ __device__ __forceinline__ bool contains(const int32_t* a, int n, int x) {
   return false;
 }
 
-// KIND: 0 raw pages (MMA in T), 1 nibble codes, 2 byte codes (MMA in fp16).
-//
-// Work decomposition.  A CTA (8 warps) owns `pps` consecutive units (pages)
-// of one stream's union.  All of them are staged into shared memory with
-// one CTA-wide cp.async sweep, then each page is cut into P/16 token tiles
-// of 16 tokens and the (page, tile) items are dealt to the warps: a warp
-// runs QK for its 16 tokens (2 n-tiles x D/16 k-steps) and one PV k-step
-// over all D/8 channel tiles, keeping its own online-softmax state.  Short
-// per-warp chains + many resident warps hide the MMA / shuffle latencies
-// (one warp per page serialised ~3.5k dependent instructions).
+// Per-(warp, row) online-softmax state + the thread's output channels
+// (row r = lane/4, channels 8*cn + 2*j + e, j = lane%4).
+template <int D>
+struct RowState {
+  float m, l;
+  float o[D / 4];
+};
+
+// One whole page for one warp.  KIND: 0 raw pages (MMA in T), 1 nibble
+// codes, 2 byte codes (MMA in fp16).
 template <typename T, int KIND, int D, int P>
-#ifndef SK_DEC_MINB
-#define SK_DEC_MINB 2
-#endif
-__global__ void __launch_bounds__(kDecThreads, SK_DEC_MINB) decode_kernel(DecodeParams prm) {
+__device__ __forceinline__ void page_attend(const uint8_t* pg, int tok_in_page, bool attend,
+                                            const uint32_t (&qw)[D / 8], float sl2, float inv_levels,
+                                            RowState<D>& st) {
   using MT = typename std::conditional<KIND == 0, T, __half>::type;
-  constexpr int NKS = D / 16;   // QK k-steps
-  constexpr int NCN = D / 8;    // PV n-tiles (8 channels)
-  constexpr int NTT = P / 16;   // 16-token tiles per page
-  constexpr int QR = D / 4;     // q / o / bounds values per thread
-  constexpr int RB = KIND == 0 ? 2 * D : (KIND == 1 ? D / 2 : D);  // code row bytes
-  constexpr int SLOT_USED = 2 * P * RB + (KIND == 0 ? 0 : 8 * D);  // bytes of a slot the kernel reads
-  extern __shared__ __align__(16) uint8_t smem[];
-#ifdef SK_DECODE_TIMING
-  if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < 64) g_dec_times[blockIdx.x][0] = gtimer();
-#endif
+  constexpr int NKS = D / 16;  // QK k-steps
+  constexpr int NCN = D / 8;   // PV n-tiles (8 channels)
+  constexpr int NTT = P / 16;  // 16-token tiles
+  constexpr int RB = KIND == 0 ? 2 * D : (KIND == 1 ? D / 2 : D);
+  const int lane = threadIdx.x & 31, r = lane >> 2, j = lane & 3;
+  const uint8_t* kc = pg;
+  const uint8_t* vc = pg + P * RB;
+  const T* bnd = reinterpret_cast<const T*>(pg + 2 * P * RB);
+
+  // ---- issue the page's loads up front (one round trip) ----------------------
+  // K codes: tile tt, n-tile h2 -> token 16tt + 8h2 + r, this lane's chunk j
+  constexpr int KW = KIND == 1 ? D / 32 : (KIND == 2 ? D / 16 : D / 8);  // 32-bit words per (token, lane)
+  uint32_t kw[NTT][2][KW];
+#pragma unroll
+  for (int tt = 0; tt < NTT; ++tt)
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const uint8_t* src = kc + (16 * tt + 8 * h2 + r) * RB + j * (RB / 4);
+      if constexpr (KW == 2) {
+        uint2 v = ldg8(src);
+        kw[tt][h2][0] = v.x; kw[tt][h2][1] = v.y;
+      } else {
+#pragma unroll
+        for (int i = 0; i < KW / 4; ++i) {
+          uint4 v = ldg16(src + 16 * i);
+          kw[tt][h2][4 * i] = v.x; kw[tt][h2][4 * i + 1] = v.y; kw[tt][h2][4 * i + 2] = v.z; kw[tt][h2][4 * i + 3] = v.w;
+        }
+      }
+    }
+  // K / V bounds of this lane's D/4 dims / channels: contiguous at j*(D/4)
+  uint32_t kb_lo[D / 8], kb_hi[D / 8], vb_lo[D / 8], vb_hi[D / 8];
+  if constexpr (KIND != 0) {
+#pragma unroll
+    for (int i = 0; i < D / 32; ++i) {
+      uint4 a = ldg16(bnd + j * (D / 4) + 8 * i), b = ldg16(bnd + D + j * (D / 4) + 8 * i);
+      uint4 c = ldg16(bnd + 2 * D + j * (D / 4) + 8 * i), d = ldg16(bnd + 3 * D + j * (D / 4) + 8 * i);
+      kb_lo[4 * i] = a.x; kb_lo[4 * i + 1] = a.y; kb_lo[4 * i + 2] = a.z; kb_lo[4 * i + 3] = a.w;
+      kb_hi[4 * i] = b.x; kb_hi[4 * i + 1] = b.y; kb_hi[4 * i + 2] = b.z; kb_hi[4 * i + 3] = b.w;
+      vb_lo[4 * i] = c.x; vb_lo[4 * i + 1] = c.y; vb_lo[4 * i + 2] = c.z; vb_lo[4 * i + 3] = c.w;
+      vb_hi[4 * i] = d.x; vb_hi[4 * i + 1] = d.y; vb_hi[4 * i + 2] = d.z; vb_hi[4 * i + 3] = d.w;
+    }
+  }
+  // V codes of this lane: (cn, lane) chunk of the whole page (KIND 1/2)
+  constexpr int VW = KIND == 1 ? P / 32 : P / 16;  // 32-bit words per (cn, lane)
+  uint32_t vw[NCN][KIND == 0 ? 1 : VW];
+  if constexpr (KIND != 0) {
+#pragma unroll
+    for (int cn = 0; cn < NCN; ++cn) {
+      const uint8_t* src = vc + (32 * cn + lane) * (VW * 4);
+      if constexpr (VW == 1) {
+        vw[cn][0] = __ldg(reinterpret_cast<const uint32_t*>(src));
+      } else if constexpr (VW == 2) {
+        uint2 v = ldg8(src);
+        vw[cn][0] = v.x; vw[cn][1] = v.y;
+      } else {
+#pragma unroll
+        for (int i = 0; i < VW / 4; ++i) {
+          uint4 v = ldg16(src + 16 * i);
+          vw[cn][4 * i] = v.x; vw[cn][4 * i + 1] = v.y; vw[cn][4 * i + 2] = v.z; vw[cn][4 * i + 3] = v.w;
+        }
+      }
+    }
+  }
+
+  // ---- K side: q' = q * s_k / smax (A fragments), qz = q . lo_k ----------------
+  uint32_t afr[NKS][2];
+  float smax = 1.f, qz = 0.f;
+  if constexpr (KIND == 0) {
+#pragma unroll
+    for (int ks = 0; ks < NKS; ++ks) {
+      afr[ks][0] = qw[2 * ks];
+      afr[ks][1] = qw[2 * ks + 1];
+    }
+  } else {
+    float sk[D / 4];
+    float mx = 0.f;
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) {
+      const float2 lo = DT<T>::to_f2(kb_lo[i]), hi = DT<T>::to_f2(kb_hi[i]);
+      float a = (hi.x - lo.x) * inv_levels, b = (hi.y - lo.y) * inv_levels;
+      a = a > 0.f ? a : 1.f;
+      b = b > 0.f ? b : 1.f;
+      sk[2 * i] = a;
+      sk[2 * i + 1] = b;
+      mx = fmaxf(mx, fmaxf(a, b));
+      const float2 q = DT<T>::to_f2(qw[i]);
+      qz = fmaf(q.x, lo.x, fmaf(q.y, lo.y, qz));
+    }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    qz += __shfl_xor_sync(0xffffffffu, qz, 1);
+    qz += __shfl_xor_sync(0xffffffffu, qz, 2);
+    smax = mx;
+    const float inv = 1.f / mx;
+#pragma unroll
+    for (int ks = 0; ks < NKS; ++ks) {
+      // register ri = 2ks + h holds dims 16ks + 8h + 2j + {0,1} (kbound order)
+      const float2 q0 = DT<T>::to_f2(qw[2 * ks]), q1 = DT<T>::to_f2(qw[2 * ks + 1]);
+      afr[ks][0] = pack2<MT>(q0.x * (sk[4 * ks] * inv), q0.y * (sk[4 * ks + 1] * inv));
+      afr[ks][1] = pack2<MT>(q1.x * (sk[4 * ks + 2] * inv), q1.y * (sk[4 * ks + 3] * inv));
+    }
+  }
+
+  // ---- S = q' K^T for every tile ------------------------------------------------
+  float sc[NTT][2][2];
+#pragma unroll
+  for (int tt = 0; tt < NTT; ++tt)
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < NKS; ++ks) {
+        uint32_t b0, b1;
+        const int ri0 = 2 * ks, ri1 = 2 * ks + 1;
+        if constexpr (KIND == 1) {
+          b0 = nib2h(kw[tt][h2][ri0 / 4], ri0 % 4);
+          b1 = nib2h(kw[tt][h2][ri1 / 4], ri1 % 4);
+        } else if constexpr (KIND == 2) {
+          b0 = byte2h(kw[tt][h2][ks], 0);
+          b1 = byte2h(kw[tt][h2][ks], 1);
+        } else {
+          b0 = kw[tt][h2][2 * ks];
+          b1 = kw[tt][h2][2 * ks + 1];
+        }
+        mma16816<MT>(c, afr[ks][0], afr[ks][1], b0, b1);
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int t = 16 * tt + 8 * h2 + 2 * j + e;
+        const float v = (c[e] * smax + qz) * sl2;
+        sc[tt][h2][e] = t < tok_in_page ? v : -INFINITY;
+      }
+    }
+
+  // ---- page max, rescale, probabilities -----------------------------------------
+  float tmax = -INFINITY;
+#pragma unroll
+  for (int tt = 0; tt < NTT; ++tt)
+    tmax = fmaxf(tmax, fmaxf(fmaxf(sc[tt][0][0], sc[tt][0][1]), fmaxf(sc[tt][1][0], sc[tt][1][1])));
+  tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+  tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+  const float m_new = attend ? fmaxf(st.m, tmax) : st.m;
+  const float alpha = attend ? exp2f(st.m - m_new) : 1.f;  // exp2(-inf) = 0
+  uint32_t pfr[NTT][2];
+  float psum = 0.f;
+#pragma unroll
+  for (int tt = 0; tt < NTT; ++tt)
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const float p0 = attend ? exp2f(sc[tt][h2][0] - m_new) : 0.f;
+      const float p1 = attend ? exp2f(sc[tt][h2][1] - m_new) : 0.f;
+      const uint32_t pk = pack2<MT>(p0, p1);
+      const float2 pr = unpack2<MT>(pk);  // the rounded values the MMA sees
+      psum += pr.x + pr.y;
+      pfr[tt][h2] = pk;
+    }
+  st.l = st.l * alpha + psum;  // per-thread partial (tokens of lane j)
+  st.m = m_new;
+  float prow = psum;
+  prow += __shfl_xor_sync(0xffffffffu, prow, 1);
+  prow += __shfl_xor_sync(0xffffffffu, prow, 2);
+
+  // ---- O = alpha O + s_v (P C_v) + lo_v sum(P) ------------------------------------
+#pragma unroll
+  for (int cn = 0; cn < NCN; ++cn) {
+    float c[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t vraw[KIND == 0 ? NTT * 2 : 1];
+    if constexpr (KIND == 0) {
+      const uint8_t* src = vc + (32 * cn + lane) * (P / 2);
+#pragma unroll
+      for (int i = 0; i < NTT / 2; ++i) {
+        uint4 v = ldg16(src + 16 * i);
+        vraw[4 * i] = v.x; vraw[4 * i + 1] = v.y; vraw[4 * i + 2] = v.z; vraw[4 * i + 3] = v.w;
+      }
+      if constexpr (NTT % 2) {
+        uint2 v = ldg8(src + 16 * (NTT / 2));
+        vraw[NTT * 2 - 2] = v.x; vraw[NTT * 2 - 1] = v.y;
+      }
+    }
+#pragma unroll
+    for (int tt = 0; tt < NTT; ++tt) {
+      uint32_t b0, b1;
+      const int ri0 = 2 * tt, ri1 = 2 * tt + 1;
+      if constexpr (KIND == 1) {
+        b0 = nib2h(vw[cn][ri0 / 4], ri0 % 4);
+        b1 = nib2h(vw[cn][ri1 / 4], ri1 % 4);
+      } else if constexpr (KIND == 2) {
+        b0 = byte2h(vw[cn][tt], 0);
+        b1 = byte2h(vw[cn][tt], 1);
+      } else {
+        b0 = vraw[2 * tt];
+        b1 = vraw[2 * tt + 1];
+      }
+      mma16816<MT>(c, pfr[tt][0], pfr[tt][1], b0, b1);
+    }
+    float add0 = c[0], add1 = c[1];
+    if constexpr (KIND != 0) {
+      // channels 8cn+2j, +1 sit in V-bound register cn (vbound order)
+      const float2 lo = DT<T>::to_f2(vb_lo[cn]), hi = DT<T>::to_f2(vb_hi[cn]);
+      float sa = (hi.x - lo.x) * inv_levels, sb = (hi.y - lo.y) * inv_levels;
+      sa = sa > 0.f ? sa : 1.f;
+      sb = sb > 0.f ? sb : 1.f;
+      add0 = fmaf(sa, c[0], lo.x * prow);
+      add1 = fmaf(sb, c[1], lo.y * prow);
+    }
+    st.o[2 * cn] = fmaf(st.o[2 * cn], alpha, add0);
+    st.o[2 * cn + 1] = fmaf(st.o[2 * cn + 1], alpha, add1);
+  }
+}
+
+template <typename T, int KIND, int D, int P>
+__global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_constant__ DecodeParams prm) {
+  constexpr int QR = D / 4;
   __shared__ int s_sel[kMaxSel];
   __shared__ int s_extra[kMaxExtra];
-  __shared__ int s_page[kMaxPps];
-  __shared__ uint32_t s_um[kMaxPps];
-  __shared__ int s_nextra, s_nunits;
-  __shared__ uint32_t s_last;
+  __shared__ int s_nextra;
+  __shared__ float s_m[kWarps][kMaxRows], s_l[kWarps][kMaxRows];
+  __shared__ __align__(16) float s_o[kWarps][kMaxRows][D];
+  // the CTA's partial, read by cluster rank 0 through DSMEM
+  __shared__ float c_m[kMaxRows], c_l[kMaxRows];
+  __shared__ __align__(16) float c_o[kMaxRows][D];
+  __shared__ float s_fac[kWarps > kCl ? kWarps : kCl][kMaxRows], s_self[kMaxRows], s_L[kMaxRows];
 
+  cg::cluster_group cluster = cg::this_cluster();
   const PoolView& pv = prm.pv;
-  const int s = blockIdx.y, split = blockIdx.x;
+  const int s = blockIdx.y;
+  const int rank = blockIdx.x;  // == cluster rank (the cluster spans grid.x)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = lane >> 2, j = lane & 3;
   const int G = prm.G;
-  const int pps = prm.pps;
-  const int u_begin = split * pps;
-  const int32_t* sel = prm.sel + (int64_t)s * prm.sel_stride;
-  // ---- one parallel round of header loads (no dependent global chains) ----
+
+  // ---- round trip 1: header, selection, q (all independent) -----------------
   const int n_tok = prm.tokens[s];
   const uint32_t rm_raw = prm.row_mask[s];
   const int cnt_raw = prm.sel_count[s];
+  const int32_t* sel = prm.sel + (int64_t)s * prm.sel_stride;
   const int sel_w = min(prm.sel_stride, kMaxSel);
-  if (n_tok < 0) s_sel[0] = 0;  // keep n_tok live for the stamp below
-  SK_STAMP(6);
-  for (int i = tid; i < sel_w; i += kDecThreads) s_sel[i] = sel[i];
-  SK_STAMP(7);
+  for (int i = tid; i < sel_w; i += kDecThreads) s_sel[i] = __ldg(sel + i);
   const bool row_ok = r < G;
-  uint32_t qw[QR / 2];  // the thread's q values, packed pairs in the input dtype (exact)
+  uint32_t qw[D / 8];  // this lane's q values of row r (pairs, input dtype)
   {
     const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)(row_ok ? r : 0) * prm.q_rs;
 #pragma unroll
     for (int ri = 0; ri < D / 8; ++ri) {
-      int d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j;
-      qw[ri] = *reinterpret_cast<const uint32_t*>(qrow + d);
+      const int d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j;
+      qw[ri] = row_ok ? __ldg(reinterpret_cast<const uint32_t*>(qrow + d)) : 0u;
     }
   }
-  const int n_pages = (n_tok + P - 1) / P;
+  const int n_pages = (n_tok + pv.P - 1) / pv.P;
   const uint32_t gmask = (G >= 32) ? 0xffffffffu : ((1u << G) - 1u);
   const uint32_t rmask = rm_raw & gmask;
   const uint32_t smask = gmask & ~rmask;
-  const int nsel = rmask ? cnt_raw : 0;
+  const int nsel = rmask ? min(cnt_raw, sel_w) : 0;
   const int sink_end = min(pv.sink, n_pages), local_start = max(n_pages - pv.local, 0);
   __syncthreads();
-  SK_STAMP(8);
-  // ---- the stream's page union from smem: selection + sink/local extras ----
-  // warp 0: each lane tests one sink/local candidate against the staged
-  // selection (binary search in smem), ballots keep the ascending order.
+  // ---- the stream's page union: selection + sink/local pages it lacks ---------
   if (warp == 0) {
     int ne = 0;
     if (smask) {
@@ -237,406 +416,145 @@ __global__ void __launch_bounds__(kDecThreads, SK_DEC_MINB) decode_kernel(Decode
       }
       ne = min(ne, kMaxExtra);
     }
-    __syncwarp();
-    const int U0 = nsel + ne;
-    const int nu = max(0, min(U0, u_begin + pps) - u_begin);
-    if (lane < nu) {
-      const int u = u_begin + lane;
-      int pg;
-      uint32_t um;
-      if (u < nsel) {
-        pg = s_sel[u];
-        um = rmask | ((smask && (pg < sink_end || pg >= local_start)) ? smask : 0u);
-      } else {
-        pg = s_extra[u - nsel];
-        um = smask;
-      }
-      s_page[lane] = pg;
-      s_um[lane] = um;
-    }
-    if (lane == 0) {
-      s_nextra = ne;
-      s_nunits = nu;
-    }
+    if (lane == 0) s_nextra = ne;
   }
   __syncthreads();
-  SK_STAMP(0);
   const int U = nsel + s_nextra;
-  const int n_used = (U + pps - 1) / pps;
-  const int n_units = s_nunits;
 
-  // ---- stage the CTA's pages in smem (one cp.async sweep) -------------------
-  for (int i = 0; i < n_units; ++i) {
-    const uint8_t* src = pv.slot_ptr(s, s_page[i]);
-    uint8_t* dst = smem + i * SLOT_USED;
-    for (int c = tid; c < SLOT_USED / 16; c += kDecThreads) cp_async16(dst + 16 * c, src + 16 * c);
-  }
-  cp_async_commit();
-
-  // ---- per-thread row state: row r (lane/4), dims/channels of j (lane%4) ----
-  if (!row_ok) {
+  // ---- this warp's pages: unit u = rank + kCl * (warp + kWarps * i) -----------
+  RowState<D> st;
+  st.m = -INFINITY;
+  st.l = 0.f;
 #pragma unroll
-    for (int ri = 0; ri < D / 8; ++ri) qw[ri] = 0u;
-  }
-  float o[QR];
-#pragma unroll
-  for (int i = 0; i < QR; ++i) o[i] = 0.f;
-  float m_run = -INFINITY, l_run = 0.f;
+  for (int i = 0; i < QR; ++i) st.o[i] = 0.f;
   const float sl2 = prm.scale_log2;
   const float inv_levels = KIND == 0 ? 1.f : 1.f / float((1 << pv.bits) - 1);
-  cp_async_wait<0>();
-  __syncthreads();
-  SK_STAMP(1);
-  // ---- per-page dequantisation tables, once per page (warp w -> page w) ----
-  // tab[0:D)  = s_k / smax  (K bounds order)   tab[D:2D)  = lo_k
-  // tab[2D:3D) = s_v         (V bounds order)   tab[3D:4D) = lo_v   tab[4D] = smax
-  constexpr int TAB = 4 * D + 4;
-  float* tabs = reinterpret_cast<float*>(smem + ((prm.pps * SLOT_USED + 15) & ~15));
-  if constexpr (KIND != 0) {
-    for (int i = warp; i < n_units; i += kWarps) {
-      const T* bnd = reinterpret_cast<const T*>(smem + i * SLOT_USED + 2 * P * RB);
-      float* tab = tabs + i * TAB;
-      float mx = 0.f;
-      float skv[D / 32];
-#pragma unroll
-      for (int q = 0; q < D / 32; ++q) {
-        const int x = lane + 32 * q;
-        const float lo = DT<T>::to_f(bnd[x]), hi = DT<T>::to_f(bnd[D + x]);
-        const float sv = (hi - lo) * inv_levels;
-        skv[q] = sv > 0.f ? sv : 1.f;
-        mx = fmaxf(mx, skv[q]);
-        tab[D + x] = lo;
-        const float vlo = DT<T>::to_f(bnd[2 * D + x]), vhi = DT<T>::to_f(bnd[3 * D + x]);
-        const float vs = (vhi - vlo) * inv_levels;
-        tab[2 * D + x] = vs > 0.f ? vs : 1.f;
-        tab[3 * D + x] = vlo;
-      }
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      const float inv = 1.f / mx;
-#pragma unroll
-      for (int q = 0; q < D / 32; ++q) tab[lane + 32 * q] = skv[q] * inv;
-      if (lane == 0) tab[4 * D] = mx;
-    }
-    __syncthreads();
-  }
-  SK_STAMP(9);
-
-  for (int item = warp; item < n_units * NTT; item += kWarps) {
-    const int ui = item / NTT, tt = item % NTT;
-    const int p = s_page[ui];
-    const uint32_t um = s_um[ui];
-    const bool attend = row_ok && ((um >> r) & 1u);
-    const uint8_t* pg = smem + ui * SLOT_USED;
-    const int tok_in_page = min(P, n_tok - p * P);
-    if (16 * tt >= tok_in_page) continue;  // tile past the open page's tokens
-#if defined(SK_DBG) && SK_DBG == 4
-    continue;
-#endif
-    const uint8_t* kc = pg;
-    const uint8_t* vc = pg + P * RB;
-    const T* bnd = reinterpret_cast<const T*>(pg + 2 * P * RB);
-
-    // ---- K side: q' = q * s_k / smax (A fragments), qz = q . lo_k ----
-    uint32_t afr[NKS][2];
-    float smax = 1.f, qz = 0.f;
-    const float* tab = tabs + ui * TAB;
-    if constexpr (KIND == 0) {
-#pragma unroll
-      for (int ks = 0; ks < NKS; ++ks) {
-        afr[ks][0] = qw[2 * ks];  // raw pages: q is the A operand as is
-        afr[ks][1] = qw[2 * ks + 1];
-      }
+  for (int u = rank + kCl * warp; u < U; u += kCl * kWarps) {
+    int pg;
+    uint32_t um;
+    if (u < nsel) {
+      pg = s_sel[u];
+      um = rmask | ((smask && (pg < sink_end || pg >= local_start)) ? smask : 0u);
     } else {
-      const float4* kn4 = reinterpret_cast<const float4*>(tab + j * QR);
-      const float4* kl4 = reinterpret_cast<const float4*>(tab + D + j * QR);
-#pragma unroll
-      for (int ks = 0; ks < NKS; ++ks) {
-        const float4 f = kn4[ks], l = kl4[ks];
-        const float2 q0 = DT<T>::to_f2(qw[2 * ks]), q1 = DT<T>::to_f2(qw[2 * ks + 1]);
-        afr[ks][0] = pack2<MT>(q0.x * f.x, q0.y * f.y);
-        afr[ks][1] = pack2<MT>(q1.x * f.z, q1.y * f.w);
-        qz = fmaf(q0.x, l.x, fmaf(q0.y, l.y, fmaf(q1.x, l.z, fmaf(q1.y, l.w, qz))));
-      }
-      qz += __shfl_xor_sync(0xffffffffu, qz, 1);
-      qz += __shfl_xor_sync(0xffffffffu, qz, 2);
-      smax = tab[4 * D];
+      pg = s_extra[u - nsel];
+      um = smask;
     }
-
-    // ---- S = q' K^T for the tile's two n-tiles of 8 tokens ----
-    float sc[2][2];
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      const int nt = 2 * tt + h2;
-      const int tok = 8 * nt + r;  // B operand: n = lane/4
-      float c[4] = {0.f, 0.f, 0.f, 0.f};
-      if constexpr (KIND == 1) {
-        uint32_t wd[D / 32];
-        const uint8_t* src = kc + tok * (D / 2) + j * (D / 8);
-        if constexpr (D == 128) {
-          uint4 v = *reinterpret_cast<const uint4*>(src);
-          wd[0] = v.x; wd[1] = v.y; wd[2] = v.z; wd[3] = v.w;
-        } else {
-          uint2 v = *reinterpret_cast<const uint2*>(src);
-          wd[0] = v.x; wd[1] = v.y;
-        }
-#pragma unroll
-        for (int ks = 0; ks < NKS; ++ks) {
-          int ri0 = 2 * ks, ri1 = 2 * ks + 1;
-          uint32_t b0 = nib2h(wd[ri0 / 4], ri0 % 4), b1 = nib2h(wd[ri1 / 4], ri1 % 4);
-#if defined(SK_DBG) && SK_DBG == 1
-          c[0] += __uint_as_float(b0 ^ afr[ks][0]); c[1] += __uint_as_float(b1 ^ afr[ks][1]);
-#else
-          mma16816<MT>(c, afr[ks][0], 0u, afr[ks][1], 0u, b0, b1);
-#endif
-        }
-      } else if constexpr (KIND == 2) {
-        uint32_t wd[D / 16];
-        const uint4* src = reinterpret_cast<const uint4*>(kc + tok * D + j * (D / 4));
-#pragma unroll
-        for (int i = 0; i < D / 64; ++i) {
-          uint4 v = src[i];
-          wd[4 * i] = v.x; wd[4 * i + 1] = v.y; wd[4 * i + 2] = v.z; wd[4 * i + 3] = v.w;
-        }
-#pragma unroll
-        for (int ks = 0; ks < NKS; ++ks) {
-          uint32_t b0 = byte2h(wd[ks], 0), b1 = byte2h(wd[ks], 1);
-          mma16816<MT>(c, afr[ks][0], 0u, afr[ks][1], 0u, b0, b1);
-        }
-      } else {
-        uint32_t wd[D / 8];
-        const uint4* src = reinterpret_cast<const uint4*>(kc + tok * D * 2 + j * (D / 2));
-#pragma unroll
-        for (int i = 0; i < D / 32; ++i) {
-          uint4 v = src[i];
-          wd[4 * i] = v.x; wd[4 * i + 1] = v.y; wd[4 * i + 2] = v.z; wd[4 * i + 3] = v.w;
-        }
-#pragma unroll
-        for (int ks = 0; ks < NKS; ++ks) mma16816<MT>(c, afr[ks][0], 0u, afr[ks][1], 0u, wd[2 * ks], wd[2 * ks + 1]);
-      }
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        int t = 8 * nt + 2 * j + e;
-        float v = (c[e] * smax + qz) * sl2;
-        sc[h2][e] = t < tok_in_page ? v : -INFINITY;
-      }
-    }
-
-    // ---- online softmax for row r over the 16 tokens (4 lanes j share a row) ----
-    float tmax = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
-    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
-    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
-    const float m_new = attend ? fmaxf(m_run, tmax) : m_run;
-    const float alpha = attend ? exp2f(m_run - m_new) : 1.f;  // exp2(-inf) = 0
-    uint32_t pfr[2];
-    float psum = 0.f;
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-#if defined(SK_DBG) && SK_DBG == 3
-      float p0 = attend ? (sc[h2][0] - m_new) : 0.f;
-      float p1 = attend ? (sc[h2][1] - m_new) : 0.f;
-#else
-      float p0 = attend ? exp2f(sc[h2][0] - m_new) : 0.f;
-      float p1 = attend ? exp2f(sc[h2][1] - m_new) : 0.f;
-#endif
-      uint32_t pk = pack2<MT>(p0, p1);
-      float2 pr = unpack2<MT>(pk);  // the rounded values the MMA sees
-      psum += pr.x + pr.y;
-      pfr[h2] = pk;
-    }
-    l_run = l_run * alpha + psum;  // per-thread partial (tokens of lane j)
-    m_run = m_new;
-    float prow = psum;
-    prow += __shfl_xor_sync(0xffffffffu, prow, 1);
-    prow += __shfl_xor_sync(0xffffffffu, prow, 2);
-
-    // ---- O += P V over the tile's 16 tokens: one k-step per channel n-tile ----
-    const int ri0 = 2 * tt, ri1 = 2 * tt + 1;
-#pragma unroll
-    for (int cn = 0; cn < NCN; ++cn) {
-      float c[4] = {0.f, 0.f, 0.f, 0.f};
-      const int vl = 32 * cn + lane;  // (cn, lane) chunk
-      uint32_t b0, b1;
-      if constexpr (KIND == 1) {
-        const uint32_t w = reinterpret_cast<const uint32_t*>(vc + vl * (P / 8))[ri0 / 4];
-        b0 = nib2h(w, ri0 % 4);
-        b1 = nib2h(w, ri1 % 4);
-      } else if constexpr (KIND == 2) {
-        const uint32_t w = reinterpret_cast<const uint32_t*>(vc + vl * (P / 4))[tt];
-        b0 = byte2h(w, 0);
-        b1 = byte2h(w, 1);
-      } else {
-        const uint2 w = reinterpret_cast<const uint2*>(vc + vl * (P / 2))[tt];
-        b0 = w.x;
-        b1 = w.y;
-      }
-#if defined(SK_DBG) && SK_DBG == 2
-      c[0] = __uint_as_float(b0 ^ pfr[0]); c[1] = __uint_as_float(b1 ^ pfr[1]);
-#else
-      mma16816<MT>(c, pfr[0], 0u, pfr[1], 0u, b0, b1);
-#endif
-      float add0 = c[0], add1 = c[1];
-      if constexpr (KIND != 0) {
-        // channels 8cn+2j, +1 are adjacent in the V table (vbound order)
-        const float2 sv = *reinterpret_cast<const float2*>(tab + 2 * D + j * QR + 2 * cn);
-        const float2 lo = *reinterpret_cast<const float2*>(tab + 3 * D + j * QR + 2 * cn);
-        add0 = fmaf(sv.x, c[0], lo.x * prow);
-        add1 = fmaf(sv.y, c[1], lo.y * prow);
-      }
-      o[2 * cn] = fmaf(o[2 * cn], alpha, add0);
-      o[2 * cn + 1] = fmaf(o[2 * cn + 1], alpha, add1);
-    }
+    const bool attend = row_ok && ((um >> r) & 1u);
+    const uint8_t* slot = pv.slot_ptr(s, pg);  // round trip 2 (page table)
+    page_attend<T, KIND, D, P>(slot, min(P, n_tok - pg * P), attend, qw, sl2, inv_levels, st);
   }
 
-  SK_WSTAMP(11);
-  // ---- merge the 8 warps of this CTA (rows < kMaxRows) ----
-  __syncthreads();  // page buffers are reused as the merge area
-  SK_STAMP(2);
-  float* sm_m = reinterpret_cast<float*>(smem);  // [kWarps][8]
-  float* sm_l = sm_m + kWarps * kMaxRows;        // [kWarps][8]
-  float* sm_o = sm_l + kWarps * kMaxRows;        // [kWarps][8][D]
+  // ---- merge the CTA's warps ---------------------------------------------------
   {
-    float lt = l_run;
+    float lt = st.l;
     lt += __shfl_xor_sync(0xffffffffu, lt, 1);
     lt += __shfl_xor_sync(0xffffffffu, lt, 2);
     if (j == 0) {
-      sm_m[warp * kMaxRows + r] = m_run;
-      sm_l[warp * kMaxRows + r] = lt;
+      s_m[warp][r] = st.m;
+      s_l[warp][r] = lt;
     }
 #pragma unroll
-    for (int cn = 0; cn < NCN; ++cn)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) sm_o[(warp * kMaxRows + r) * D + 8 * cn + 2 * j + e] = o[2 * cn + e];
+    for (int cn = 0; cn < D / 8; ++cn)
+      *reinterpret_cast<float2*>(&s_o[warp][r][8 * cn + 2 * j]) = make_float2(st.o[2 * cn], st.o[2 * cn + 1]);
   }
   __syncthreads();
-  SK_STAMP(3);
-  const int part_stride = 2 + D;
-  float* part = prm.ws_part + ((int64_t)s * prm.max_splits + split) * kMaxRows * part_stride;
-  // per-(warp, row) rescale factors once, then one FMA chain per output
-  float* sm_f = sm_o + kWarps * kMaxRows * D;  // [kWarps][8]
   if (tid < G) {
-    const int rr = tid;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sm_m[w * kMaxRows + rr]);
+    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_m[w][tid]);
     float L = 0.f;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-      const float f = M == -INFINITY ? 0.f : exp2f(sm_m[w * kMaxRows + rr] - M);
-      sm_f[w * kMaxRows + rr] = f;
-      L += f * sm_l[w * kMaxRows + rr];
+      const float f = M == -INFINITY ? 0.f : exp2f(s_m[w][tid] - M);
+      s_fac[w][tid] = f;
+      L = fmaf(f, s_l[w][tid], L);
     }
-    if (split < n_used) {
-      part[rr * part_stride] = M;
-      part[rr * part_stride + 1] = L;
-    }
-  }
-  __syncthreads();
-  if (split < n_used) {
-    for (int i = tid; i < G * D; i += kDecThreads) {
-      const int rr = i / D, c = i % D;
-      float O = 0.f;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) O = fmaf(sm_f[w * kMaxRows + rr], sm_o[(w * kMaxRows + rr) * D + c], O);
-      part[rr * part_stride + 2 + c] = O;
-    }
-  }
-  const T* kn = reinterpret_cast<const T*>(prm.k_new) + s * prm.new_ss;
-  const T* vn = reinterpret_cast<const T*>(prm.v_new) + s * prm.new_ss;
-  // ---- last CTA of the stream: merge splits + the new token, write ----
-  __syncthreads();
-  SK_STAMP(4);
-  if (tid == 0) {
-    __threadfence();
-    uint32_t t = atomicAdd(prm.ws_ticket + s, 1u);
-    s_last = (t == gridDim.x - 1);
-    if (s_last) prm.ws_ticket[s] = 0;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  SK_STAMP(5);
-  __threadfence();
-  // Parallel merge of the n_used split partials (m, l, O[D]) + the new token:
-  // stage the G rows of every split in smem with independent coalesced loads,
-  // then one warp per row reduces (max, factors, denominator) and one thread
-  // per (row, channel) sums the rescaled partial outputs.
-  const int ps = part_stride;
-  float* stg = reinterpret_cast<float*>(smem);  // [n_used][G * ps]
-  float* row_l = stg + n_used * G * ps;         // [G]
-  float* row_f = row_l + G;                     // [G] factor of the new token
-  {
-    const float* wsp = prm.ws_part + (int64_t)s * prm.max_splits * kMaxRows * ps;
-    for (int sp = warp; sp < n_used; sp += kWarps)
-      for (int idx = lane; idx < G * ps; idx += 32) stg[sp * G * ps + idx] = __ldcg(wsp + (int64_t)sp * kMaxRows * ps + idx);
-  }
-  __syncthreads();
-  for (int rr = warp; rr < G; rr += kWarps) {
-    const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)rr * prm.q_rs;
-    float dot = 0.f;
-    for (int c = lane; c < D; c += 32) dot = fmaf(DT<T>::to_f(qrow[c]), DT<T>::to_f(kn[c]), dot);
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
-    const float s_self = dot * sl2;
-    float M = s_self;
-    for (int sp = lane; sp < n_used; sp += 32) M = fmaxf(M, stg[(sp * G + rr) * ps]);
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-    float L = 0.f;
-    for (int sp = lane; sp < n_used; sp += 32) {
-      float* cell = stg + (sp * G + rr) * ps;
-      const float pm = cell[0];
-      const float f = pm == -INFINITY ? 0.f : exp2f(pm - M);
-      L = fmaf(f, cell[1], L);
-      cell[0] = f;  // the split's rescale factor for the output pass
-    }
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
-    if (lane == 0) {
-      const float fs = exp2f(s_self - M);
-      row_l[rr] = L + fs;
-      row_f[rr] = fs;
-    }
+    c_m[tid] = M;
+    c_l[tid] = L;
   }
   __syncthreads();
   for (int i = tid; i < G * D; i += kDecThreads) {
     const int rr = i / D, c = i % D;
-    float O = row_f[rr] * DT<T>::to_f(vn[c]);
-    for (int sp = 0; sp < n_used; ++sp) {
-      const float* cell = stg + (sp * G + rr) * ps;
-      O = fmaf(cell[0], cell[2 + c], O);
-    }
-    O /= row_l[rr];
-    const int64_t oi = s * prm.out_ss + (int64_t)rr * prm.out_rs + c;
-    if (prm.out_dtype == SK_F32) reinterpret_cast<float*>(prm.out)[oi] = O;
-    else if (prm.out_dtype == SK_F16) reinterpret_cast<__half*>(prm.out)[oi] = __float2half_rn(O);
-    else reinterpret_cast<__nv_bfloat16*>(prm.out)[oi] = __float2bfloat16_rn(O);
+    float O = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) O = fmaf(s_fac[w][rr], s_o[w][rr][c], O);
+    c_o[rr][c] = O;
   }
-}
+  cluster.sync();  // every CTA's partial is visible cluster-wide
 
-__host__ __device__ constexpr int slot_used(int kind, int D, int P) {
-  return 2 * P * (kind == 0 ? 2 * D : (kind == 1 ? D / 2 : D)) + (kind == 0 ? 0 : 8 * D);
+  // ---- cluster rank 0: merge the kCl partials + the new token, write ----------
+  if (rank == 0) {
+    const T* kn = reinterpret_cast<const T*>(prm.k_new) + s * prm.new_ss;
+    const T* vn = reinterpret_cast<const T*>(prm.v_new) + s * prm.new_ss;
+    for (int rr = warp; rr < G; rr += kWarps) {
+      const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)rr * prm.q_rs;
+      float dot = 0.f;
+      for (int c = lane; c < D; c += 32) dot = fmaf(DT<T>::to_f(qrow[c]), DT<T>::to_f(kn[c]), dot);
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+      const float s_new = dot * sl2;
+      float pm = -INFINITY, pl = 0.f;
+      if (lane < kCl) {
+        pm = *cluster.map_shared_rank(&c_m[rr], lane);
+        pl = *cluster.map_shared_rank(&c_l[rr], lane);
+      }
+      float M = fmaxf(s_new, pm);
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+      const float f = (lane < kCl && pm != -INFINITY) ? exp2f(pm - M) : 0.f;
+      float L = f * pl;
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+      if (lane < kCl) s_fac[lane][rr] = f;
+      if (lane == 0) {
+        const float fs = exp2f(s_new - M);
+        s_self[rr] = fs;
+        s_L[rr] = L + fs;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < G * D; i += kDecThreads) {
+      const int rr = i / D, c = i % D;
+      float O = s_self[rr] * DT<T>::to_f(vn[c]);
+#pragma unroll
+      for (int cr = 0; cr < kCl; ++cr) O = fmaf(s_fac[cr][rr], *cluster.map_shared_rank(&c_o[rr][c], cr), O);
+      O /= s_L[rr];
+      const int64_t oi = s * prm.out_ss + (int64_t)rr * prm.out_rs + c;
+      if (prm.out_dtype == SK_F32) reinterpret_cast<float*>(prm.out)[oi] = O;
+      else if (prm.out_dtype == SK_F16) reinterpret_cast<__half*>(prm.out)[oi] = __float2half_rn(O);
+      else reinterpret_cast<__nv_bfloat16*>(prm.out)[oi] = __float2bfloat16_rn(O);
+    }
+  }
+  cluster.sync();  // keep every CTA's shared memory alive until rank 0 has read it
 }
 
 template <typename T, int KIND, int D, int P>
-int launch_one(const DecodeParams& prm, dim3 grid, size_t smem_min, cudaStream_t st) {
-  constexpr int SLOT = slot_used(KIND, D, P);
-  size_t smem = (((size_t)prm.pps * SLOT + 15) & ~(size_t)15) + (size_t)prm.pps * (4 * D + 4) * 4;
-  if (smem < smem_min) smem = smem_min;
-  if (smem > 220 * 1024) {
-    set_error("decode: pages_per_split too large for shared memory");
-    return SK_EINVAL;
+int launch_one(const DecodeParams& prm, int n_streams, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kCl, n_streams, 1);
+  cfg.blockDim = dim3(kDecThreads, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, KIND, D, P>, prm);
+  if (e != cudaSuccess) {
+    set_error(std::string("decode_kernel: ") + cudaGetErrorString(e));
+    return SK_ECUDA;
   }
-  auto kern = decode_kernel<T, KIND, D, P>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, kDecThreads, smem, st>>>(prm);
   SK_CHECK_LAUNCH("decode_kernel");
   return SK_OK;
 }
 
 template <typename T, int KIND>
-int launch_kind(const DecodeParams& prm, dim3 grid, size_t smem, cudaStream_t st) {
+int launch_kind(const DecodeParams& prm, int n_streams, cudaStream_t st) {
   const int D = prm.pv.D, P = prm.pv.P;
-#define SK_DEC(DD, PP) if (D == DD && P == PP) return launch_one<T, KIND, DD, PP>(prm, grid, smem, st)
+#define SK_DEC(DD, PP) if (D == DD && P == PP) return launch_one<T, KIND, DD, PP>(prm, n_streams, st)
   SK_DEC(128, 64);
   SK_DEC(128, 32);
   SK_DEC(128, 128);
@@ -652,8 +570,11 @@ int launch_kind(const DecodeParams& prm, dim3 grid, size_t smem, cudaStream_t st
 }  // namespace sk
 
 extern "C" int64_t sk_decode_workspace(int32_t n_streams, int32_t group_rows, int32_t head_dim, int32_t max_splits) {
+  (void)n_streams;
   (void)group_rows;
-  return (int64_t)n_streams * max_splits * sk::kMaxRows * (2 + head_dim) * 4 + (int64_t)n_streams * 4 + 256;
+  (void)head_dim;
+  (void)max_splits;
+  return 256;  // the cluster merge needs no global workspace
 }
 
 extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
@@ -666,17 +587,18 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   using namespace sk;
   int rc = check_pool(pool);
   if (rc) return rc;
-  SK_CHECK_ARG(n_streams >= 1, "decode: no streams");
+  (void)workspace;
+  (void)workspace_bytes;
+  SK_CHECK_ARG(n_streams >= 1 && n_streams <= 65535, "decode: stream count must be in [1, 65535]");
   SK_CHECK_ARG(group_rows >= 1 && group_rows <= kMaxRows, "decode: group size must be in [1, 8]");
-  SK_CHECK_ARG(pages_per_split >= 1 && pages_per_split <= kMaxPps && max_splits >= 1, "decode: bad split geometry");
-  SK_CHECK_ARG(sel_stride <= kMaxSel, "decode: selection wider than 2048 pages");
+  SK_CHECK_ARG(pages_per_split >= 1 && max_splits >= 1, "decode: bad split geometry");
+  SK_CHECK_ARG(sel_stride >= 1 && sel_stride <= kMaxSel, "decode: selection width must be in [1, 2048]");
   SK_CHECK_ARG(pool->sink + pool->local <= kMaxExtra, "decode: sink + local window too large");
   SK_CHECK_ARG(out_dtype == SK_F16 || out_dtype == SK_BF16 || out_dtype == SK_F32, "decode: bad out dtype");
-  SK_CHECK_ARG(workspace_bytes >= sk_decode_workspace(n_streams, group_rows, pool->head_dim, max_splits),
-               "decode: workspace too small");
-  SK_CHECK_ARG(q && k_new && v_new && row_mask && sel && sel_count && tokens && out && workspace,
-               "decode: NULL pointer");
+  SK_CHECK_ARG(q && k_new && v_new && row_mask && sel && sel_count && tokens && out, "decode: NULL pointer");
   SK_CHECK_ARG(q_row_stride % 2 == 0 && q_stream_stride % 2 == 0, "decode: q strides must be even");
+  SK_CHECK_ARG(reinterpret_cast<uintptr_t>(pool->arena) % 16 == 0 && pool->slot_bytes % 16 == 0,
+               "decode: arena slots must be 16-byte aligned");
   DecodeParams prm;
   prm.pv = make_view(*pool);
   prm.G = group_rows;
@@ -696,38 +618,19 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   prm.out_ss = out_stream_stride;
   prm.out_rs = out_row_stride;
   prm.out_dtype = out_dtype;
-  prm.pps = pages_per_split;
-  prm.fuse_append = fuse_append;
-  prm.max_splits = max_splits;
-  prm.ws_part = static_cast<float*>(workspace);
-  prm.ws_ticket = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(workspace) +
-                                              (int64_t)n_streams * max_splits * kMaxRows * (2 + pool->head_dim) * 4);
-  size_t smem_merge = (size_t)kWarps * kMaxRows * (3 + pool->head_dim) * 4;
-  size_t smem_comb = ((size_t)max_splits * group_rows * (2 + pool->head_dim) + 2 * group_rows) * 4;
-  size_t smem = smem_merge > smem_comb ? smem_merge : smem_comb;
-  dim3 grid(max_splits, n_streams);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int kind = pool->bits == 0 ? 0 : (pool->bits <= 4 ? 1 : 2);
+  const int kind = pool->bits == 0 ? 0 : (pool->bits <= 4 ? 1 : 2);
   int rc2;
   if (pool->dtype == SK_F16) {
-    rc2 = kind == 0 ? launch_kind<__half, 0>(prm, grid, smem, st)
-                    : (kind == 1 ? launch_kind<__half, 1>(prm, grid, smem, st) : launch_kind<__half, 2>(prm, grid, smem, st));
+    rc2 = kind == 0 ? launch_kind<__half, 0>(prm, n_streams, st)
+                    : (kind == 1 ? launch_kind<__half, 1>(prm, n_streams, st) : launch_kind<__half, 2>(prm, n_streams, st));
   } else {
-    rc2 = kind == 0 ? launch_kind<__nv_bfloat16, 0>(prm, grid, smem, st)
-                    : (kind == 1 ? launch_kind<__nv_bfloat16, 1>(prm, grid, smem, st)
-                                 : launch_kind<__nv_bfloat16, 2>(prm, grid, smem, st));
+    rc2 = kind == 0 ? launch_kind<__nv_bfloat16, 0>(prm, n_streams, st)
+                    : (kind == 1 ? launch_kind<__nv_bfloat16, 1>(prm, n_streams, st)
+                                 : launch_kind<__nv_bfloat16, 2>(prm, n_streams, st));
   }
   if (rc2 != SK_OK || !fuse_append) return rc2;
   // the new token is appended by K1's one-token kernel right behind the
   // attention (stream order: every read of its page has completed)
   return append_launch(pool, n_streams, k_new, v_new, new_stream_stride, 0, tokens, 1, 1, st);
-}
-
-extern "C" int sk_debug_decode_times(unsigned long long* host_out) {
-#ifdef SK_DECODE_TIMING
-  return cudaMemcpyFromSymbol(host_out, sk::g_dec_times, sizeof(sk::g_dec_times)) == cudaSuccess ? 0 : -2;
-#else
-  (void)host_out;
-  return -3;
-#endif
 }

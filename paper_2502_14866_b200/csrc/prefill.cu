@@ -200,26 +200,43 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       mbar_wait(&sm.s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
       float s[64];
-#pragma unroll
-      for (int c = 0; c < 64; c += 32) {
-        uint32_t r[32];
-        tmem_ld_x32(trow + (j & 1) * 64 + c, r);
+      {
+        uint32_t r[64];
+        tmem_ld_x32(trow + (j & 1) * 64, r);
+        tmem_ld_x32(trow + (j & 1) * 64 + 32, r + 32);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(r[i]);
+        for (int i = 0; i < 64; ++i) s[i] = __uint_as_float(r[i]);
       }
       const uint32_t fl = w.flags;
       const bool active = fl & half_bit;
       const int col0 = w.block() * 64;
-      uint64_t emask = ~0ull;
-      if (fl & 8u) emask = prm.row_masks[(int64_t)(w.mask_base + w.i) * 128 + row];
       const int lim = (fl & 4u) ? pos - col0 : 64;  // columns c <= lim visible
-      float mx = -INFINITY;
+      float mx;
+      if (active && lim >= 63 && !(fl & 8u)) {
+        // fast path (almost every block): the whole row is visible; the
+        // max is taken on raw scores (scale > 0 commutes with max)
+        float t[8];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        bool ok = active && i <= lim && ((emask >> i) & 1ull);
-        s[i] = ok ? s[i] * sl2 : -INFINITY;
-        mx = fmaxf(mx, s[i]);
+        for (int g = 0; g < 8; ++g) t[g] = fmax3(s[8 * g], s[8 * g + 1], s[8 * g + 2]);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) t[g] = fmax3(t[g], s[8 * g + 3], s[8 * g + 4]);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) t[g] = fmax3(t[g], s[8 * g + 5], s[8 * g + 6]);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) t[g] = fmaxf(t[g], s[8 * g + 7]);
+        mx = fmax3(fmax3(t[0], t[1], t[2]), fmax3(t[3], t[4], t[5]), fmaxf(t[6], t[7])) * sl2;
+      } else {
+        uint64_t emask = ~0ull;
+        if (fl & 8u) emask = prm.row_masks[(int64_t)(w.mask_base + w.i) * 128 + row];
+        mx = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const bool ok = active && i <= lim && ((emask >> i) & 1ull);
+          s[i] = ok ? s[i] : -INFINITY;
+          mx = fmaxf(mx, s[i]);
+        }
+        mx *= sl2;
       }
       // lazy rescale: only when the max grows by more than 2^threshold
       float m_new = fmaxf(m_run, mx);
@@ -244,16 +261,17 @@ __global__ void __launch_bounds__(kPfThreads, 1)
           m_run = m_new;
         }
       }
+      // p = 2^(s*scale - m): one FFMA + one MUFU.EX2 per element (-inf -> 0)
       const float shift = m_run == -INFINITY ? 0.f : m_run;
-      float rs = 0.f;
+      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
       uint32_t pk[32];
 #pragma unroll
       for (int i = 0; i < 64; i += 2) {
-        float p0 = exp2f(s[i] - shift), p1 = exp2f(s[i + 1] - shift);
-        rs += p0 + p1;
+        const float p0 = fast_exp2(fmaf(s[i], sl2, -shift)), p1 = fast_exp2(fmaf(s[i + 1], sl2, -shift));
+        rs4[(i / 2) & 3] += p0 + p1;
         pk[i / 2] = kBF16 ? pack_bf162(p0, p1) : pack_half2(p0, p1);
       }
-      l_run += rs;
+      l_run += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
       if (j >= 2) mbar_wait(&sm.p_empty[j & 1], ((j >> 1) - 1) & 1);
       uint8_t* prow = sm.p[j & 1] + row * 128;
 #pragma unroll

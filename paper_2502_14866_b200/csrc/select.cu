@@ -150,7 +150,6 @@ __device__ void score_pages_cta(const PoolView& pv, int s, int n_tok, const T* q
     for (int off = 16; off >= 1; off >>= 1) mine = fmax(mine, __shfl_xor_sync(0xffffffffu, mine, off));
     if (lane == 0) scores[p] = mine;
   }
-  if (lane == 0) __threadfence();  // publish before the CTA's ticket
 }
 
 // Phase 2: top-k of one stream (whole CTA).  `scores` may point to shared
@@ -291,24 +290,22 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(PoolView pv, const 
   double* scores = ws_scores + (int64_t)s * ws_pages;
   int pin[3];
   const bool trivial = K >= n_pages || K <= pins_of(n_pages, pin);
-#if !(defined(SK_DBG) && SK_DBG == 6)
   if (!trivial) score_pages_cta<T, RMAX, LP>(pv, s, n_tok, q + s * q_ss, q_rs, rmask, scores);
-#endif
   // last CTA of this stream runs the top-k
   __shared__ uint32_t is_last;
+  // CTA ticket: bar.sync orders the CTA's score stores before thread 0's
+  // acq_rel fence + relaxed atomic (the release pattern of CUTLASS's
+  // generic barrier; a seq_cst __threadfence per CTA serialises the grid)
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     uint32_t t = atomicAdd(ws_ticket + s, 1u);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     is_last = (t == gridDim.x - 1);
     if (is_last) ws_ticket[s] = 0;  // re-arm for the next invocation
   }
   __syncthreads();
   if (!is_last) return;
-#if defined(SK_DBG) && SK_DBG == 5
-  return;
-#endif
-  __threadfence();
   extern __shared__ double s_scores[];
   const double* src = scores;
   if (stage_smem && !trivial) {

@@ -16,7 +16,6 @@ from paper_2502_14866_b200.selector import _Workspace
 ctx = int(os.environ.get("SK_CTX", 131072))
 H, HKV, D = 32, 8, 128
 lib = _lib.load()
-st = torch.cuda.current_stream().cuda_stream
 
 
 def make(gates):
@@ -29,17 +28,32 @@ def make(gates):
     return e
 
 
-def time_it(fn, n=20):
+def time_it(fn, n=32):
+    """Per-call device time of n calls captured in one CUDA graph (no host
+    launch overhead in the measurement; L2 warm after the first call)."""
     fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(n):
+                fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(n):
-        fn()
+    for _ in range(5):
+        g.replay()
     b.record()
     torch.cuda.synchronize()
-    return a.elapsed_time(b) / n * 1e3
+    return a.elapsed_time(b) / (5 * n) * 1e3
 
+
+tiny = torch.zeros(1, device="cuda")
+print("graph node floor (1-element torch add) us", round(time_it(lambda: tiny.add_(1)), 2))
 
 for name, gates in [("balanced", [0.9 - 0.001 * h if h % 4 < 2 else 0.1 + 0.001 * h for h in range(H)]),
                     ("all-retrieval", [0.9] * H)]:
@@ -58,11 +72,11 @@ for name, gates in [("balanced", [0.9 - 0.001 * h if h % 4 < 2 else 0.1 + 0.001 
     def sel_call():
         rc = lib.sk_select_pages(C.byref(abi), HKV, g, q.data_ptr(), g * D, D, e._row_mask.data_ptr(),
                                  pool.tokens.data_ptr(), None, kp, n_pages, sel.data_ptr(), cnt.data_ptr(), kp,
-                                 ws.data_ptr(), ws.numel(), st)
+                                 ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
         _lib.check(rc)
 
     print(name, "select us", round(time_it(sel_call), 2))
-    for pps in (1, 2, 4):
+    for pps in (2,):
         for fuse in (0, 1):
             units = 64 + 5
             ms = -(-units // pps)
@@ -73,7 +87,7 @@ for name, gates in [("balanced", [0.9 - 0.001 * h if h % 4 < 2 else 0.1 + 0.001 
                 rc = lib.sk_decode_attn(C.byref(abi), HKV, g, q.data_ptr(), g * D, D, kn.data_ptr(), kn.data_ptr(), D,
                                         e._row_mask.data_ptr(), sel.data_ptr(), cnt.data_ptr(), kp,
                                         pool.tokens.data_ptr(), C.c_float(1 / math.sqrt(D)), out.data_ptr(), g * D, D,
-                                        _lib.SK_F16, pps, ms, fuse, wsd.data_ptr(), wsd.numel(), st)
+                                        _lib.SK_F16, pps, ms, fuse, wsd.data_ptr(), wsd.numel(), torch.cuda.current_stream().cuda_stream)
                 _lib.check(rc)
 
             print(name, f"decode pps={pps} splits={ms} fuse={fuse} us", round(time_it(dec_call), 2))
