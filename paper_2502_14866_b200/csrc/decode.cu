@@ -22,12 +22,13 @@
 //     (codes -> exact fp16 integers with one LOP3 + one HSUB2 per two);
 //     group rows sit in the MMA's M dimension, so GQA rows share each load;
 //   * one online-softmax state per (warp, row); warps merge in shared
-//     memory, the kCl CTAs merge through distributed shared memory into
-//     cluster rank 0, which adds the new token's raw K/V in-register and
-//     writes the output.  No global workspace, atomics or grid fences.
+//     memory; after one cluster barrier every CTA finishes D/kCl output
+//     channels from the kCl partials (distributed shared memory) plus the
+//     new token's raw K/V.  No global workspace, atomics or grid fences.
 // Round trips on the critical path: {tokens, selection, q} -> page table ->
 // page data -> cluster barrier.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "append_impl.cuh"
 
@@ -65,6 +66,7 @@ struct DecodeParams {
   void* out;
   int64_t out_ss, out_rs;
   int out_dtype;
+  int dbg;  // temporary: phase cut-off for timing experiments (SK_DEC_DEBUG)
 };
 
 // m16n8k16 MMA, fp32 accumulate; rows 8..15 of A are zero (group rows <= 8).
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   // the CTA's partial, read by cluster rank 0 through DSMEM
   __shared__ float c_m[kMaxRows], c_l[kMaxRows];
   __shared__ __align__(16) float c_o[kMaxRows][D];
-  __shared__ float s_fac[kWarps > kCl ? kWarps : kCl][kMaxRows], s_self[kMaxRows], s_L[kMaxRows];
+  __shared__ float s_fac[kWarps][kMaxRows], s_self[kMaxRows];
 
   cg::cluster_group cluster = cg::this_cluster();
   const PoolView& pv = prm.pv;
@@ -375,6 +377,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   const int r = lane >> 2, j = lane & 3;
   const int G = prm.G;
 
+  if (prm.dbg == 1) return;
   // ---- round trip 1: header, selection, q (all independent) -----------------
   const int n_tok = prm.tokens[s];
   const uint32_t rm_raw = prm.row_mask[s];
@@ -391,6 +394,17 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
       const int d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j;
       qw[ri] = row_ok ? __ldg(reinterpret_cast<const uint32_t*>(qrow + d)) : 0u;
     }
+  }
+  // scores of the new token (raw K, in-register; merged last, engine.py:276-277)
+  if (warp < G) {
+    const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)warp * prm.q_rs;
+    const T* kn = reinterpret_cast<const T*>(prm.k_new) + s * prm.new_ss;
+    float dot = 0.f;
+#pragma unroll
+    for (int c = lane; c < D; c += 32) dot = fmaf(DT<T>::to_f(qrow[c]), DT<T>::to_f(kn[c]), dot);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+    if (lane == 0) s_self[warp] = dot * prm.scale_log2;
   }
   const int n_pages = (n_tok + pv.P - 1) / pv.P;
   const uint32_t gmask = (G >= 32) ? 0xffffffffu : ((1u << G) - 1u);
@@ -419,7 +433,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     if (lane == 0) s_nextra = ne;
   }
   __syncthreads();
-  const int U = nsel + s_nextra;
+  const int U = (prm.dbg == 2 || prm.dbg == 3) ? 0 : nsel + s_nextra;
+  if (prm.dbg == 2) return;
 
   // ---- this warp's pages: unit u = rank + kCl * (warp + kWarps * i) -----------
   RowState<D> st;
@@ -482,50 +497,37 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   }
   cluster.sync();  // every CTA's partial is visible cluster-wide
 
-  // ---- cluster rank 0: merge the kCl partials + the new token, write ----------
-  if (rank == 0) {
-    const T* kn = reinterpret_cast<const T*>(prm.k_new) + s * prm.new_ss;
-    const T* vn = reinterpret_cast<const T*>(prm.v_new) + s * prm.new_ss;
-    for (int rr = warp; rr < G; rr += kWarps) {
-      const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)rr * prm.q_rs;
-      float dot = 0.f;
-      for (int c = lane; c < D; c += 32) dot = fmaf(DT<T>::to_f(qrow[c]), DT<T>::to_f(kn[c]), dot);
+  // ---- cluster merge: CTA `rank` finishes channels [rank*D/kCl, +D/kCl) of
+  //      every row from the kCl partials (DSMEM) + the new token ----------------
+  constexpr int CPC = D / kCl;  // channels per CTA
+  if (tid < G * CPC) {
+    const int rr = tid / CPC, c = rank * CPC + tid % CPC;
+    float pm[kCl], pl[kCl], po[kCl];
 #pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
-      const float s_new = dot * sl2;
-      float pm = -INFINITY, pl = 0.f;
-      if (lane < kCl) {
-        pm = *cluster.map_shared_rank(&c_m[rr], lane);
-        pl = *cluster.map_shared_rank(&c_l[rr], lane);
-      }
-      float M = fmaxf(s_new, pm);
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-      const float f = (lane < kCl && pm != -INFINITY) ? exp2f(pm - M) : 0.f;
-      float L = f * pl;
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
-      if (lane < kCl) s_fac[lane][rr] = f;
-      if (lane == 0) {
-        const float fs = exp2f(s_new - M);
-        s_self[rr] = fs;
-        s_L[rr] = L + fs;
-      }
+    for (int cr = 0; cr < kCl; ++cr) {  // independent remote loads, issued together
+      pm[cr] = *cluster.map_shared_rank(&c_m[rr], cr);
+      pl[cr] = *cluster.map_shared_rank(&c_l[rr], cr);
+      po[cr] = *cluster.map_shared_rank(&c_o[rr][c], cr);
     }
-    __syncthreads();
-    for (int i = tid; i < G * D; i += kDecThreads) {
-      const int rr = i / D, c = i % D;
-      float O = s_self[rr] * DT<T>::to_f(vn[c]);
+    const float s_new = s_self[rr];
+    float M = s_new;
 #pragma unroll
-      for (int cr = 0; cr < kCl; ++cr) O = fmaf(s_fac[cr][rr], *cluster.map_shared_rank(&c_o[rr][c], cr), O);
-      O /= s_L[rr];
-      const int64_t oi = s * prm.out_ss + (int64_t)rr * prm.out_rs + c;
-      if (prm.out_dtype == SK_F32) reinterpret_cast<float*>(prm.out)[oi] = O;
-      else if (prm.out_dtype == SK_F16) reinterpret_cast<__half*>(prm.out)[oi] = __float2half_rn(O);
-      else reinterpret_cast<__nv_bfloat16*>(prm.out)[oi] = __float2bfloat16_rn(O);
+    for (int cr = 0; cr < kCl; ++cr) M = fmaxf(M, pm[cr]);
+    const float fs = exp2f(s_new - M);
+    float L = fs, O = fs * DT<T>::to_f(reinterpret_cast<const T*>(prm.v_new)[s * prm.new_ss + c]);
+#pragma unroll
+    for (int cr = 0; cr < kCl; ++cr) {
+      const float f = pm[cr] == -INFINITY ? 0.f : exp2f(pm[cr] - M);
+      L = fmaf(f, pl[cr], L);
+      O = fmaf(f, po[cr], O);
     }
+    O /= L;
+    const int64_t oi = s * prm.out_ss + (int64_t)rr * prm.out_rs + c;
+    if (prm.out_dtype == SK_F32) reinterpret_cast<float*>(prm.out)[oi] = O;
+    else if (prm.out_dtype == SK_F16) reinterpret_cast<__half*>(prm.out)[oi] = __float2half_rn(O);
+    else reinterpret_cast<__nv_bfloat16*>(prm.out)[oi] = __float2bfloat16_rn(O);
   }
-  cluster.sync();  // keep every CTA's shared memory alive until rank 0 has read it
+  cluster.sync();  // keep every CTA's shared memory alive until all remote reads are done
 }
 
 template <typename T, int KIND, int D, int P>
@@ -618,6 +620,7 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   prm.out_ss = out_stream_stride;
   prm.out_rs = out_row_stride;
   prm.out_dtype = out_dtype;
+  prm.dbg = getenv("SK_DEC_DEBUG") ? atoi(getenv("SK_DEC_DEBUG")) : 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int kind = pool->bits == 0 ? 0 : (pool->bits <= 4 ? 1 : 2);
   int rc2;

@@ -53,7 +53,7 @@ def time_it(fn, n=32):
 
 
 tiny = torch.zeros(1, device="cuda")
-print("graph node floor (1-element torch add) us", round(time_it(lambda: tiny.add_(1)), 2))
+print("graph node floor (1-element torch add) us", round(time_it(lambda: tiny.add_(1)), 2), flush=True)
 
 for name, gates in [("balanced", [0.9 - 0.001 * h if h % 4 < 2 else 0.1 + 0.001 * h for h in range(H)]),
                     ("all-retrieval", [0.9] * H)]:
