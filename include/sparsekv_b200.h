@@ -152,23 +152,24 @@ int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t group_rows, c
  * Replaces blockwise_attention (attn.py:245-324) driven by Engine.prefill's
  * schedules (engine.py:152-168).  q [n_q][n_heads][D], k/v [n_kv][n_kv_heads][D]
  * token-major (device, `dtype`), out like q.  Query row i sees key columns
- * <= n_kv - n_q + i.  Each work item is one 128-row query block of one head
- * (two of the reference's 64-row query tiles) and a list of segments of
+ * <= n_kv - n_q + i.  Each work item is one 256-row query block of one head
+ * (four of the reference's 64-row query tiles, computed as two 128-row
+ * tensor-core tiles sharing one K/V stream) and a list of segments of
  * consecutive 64-key blocks; the host builds items and segments from the
  * per-(head, query tile) schedules (the paper's block iterator,
  * PAPER.md:296-297) and orders items heaviest first.
  *
  * Segment = 3 x uint32: { first_block, count | flags << 24, mask_base } with
- *   flags bit 0: query rows [0,64) of the block attend these key blocks
- *   flags bit 1: query rows [64,128) attend them
- *   flags bit 2: apply the element-wise causal mask (column > row position)
- *   flags bit 3: explicit per-row column masks: block first_block+i uses
- *                row_masks[(mask_base + i) * 128 + row] (bit c = column c
- *                allowed; generic tile sizes).
+ *   flags bits 0..3: query rows [64q, 64q+64) of the item (quarter q) attend
+ *                    these key blocks
+ *   flags bit 4:     apply the element-wise causal mask (column > row position)
+ *   flags bit 5:     explicit per-row column masks: block first_block+i uses
+ *                    row_masks[(mask_base + i) * 256 + row] (bit c = column c
+ *                    allowed; generic tile sizes).
  */
 typedef struct sk_prefill_item {
   int32_t head;      /* query head */
-  int32_t row0;      /* first query row of the 128-row block */
+  int32_t row0;      /* first query row of the 256-row block */
   int32_t seg_begin; /* first segment (index into segs, in units of segments) */
   int32_t seg_count; /* number of segments */
 } sk_prefill_item;

@@ -3,7 +3,7 @@ block-sparse prefill entry point.
 
 API mirrors the reference ``sparsekv.attn`` (attn.py:23-324).  The hot
 path, :func:`blockwise_attention`, validates the schedules on the host,
-compiles them into 128-row work items over 64-key block segments and runs
+compiles them into 256-row work items over 64-key block segments and runs
 the tcgen05 prefill kernel (csrc/prefill.cu) -- there is no CPU fallback.
 Inputs may be numpy arrays or torch tensors; they are computed in the
 device dtype (fp16 by default, bf16 optional) and returned in the caller's
@@ -154,7 +154,7 @@ def merge_block(state: SoftmaxState, scores, values) -> SoftmaxState:
                         alpha[:, None] * state.running_output + probs @ values)
 
 
-# -- prefill plan: schedules -> 128-row work items over 64-key segments --------
+# -- prefill plan: schedules -> 256-row work items over 64-key segments --------
 
 
 def _segments_of(tiles: Sequence[int]) -> tuple:
@@ -171,22 +171,29 @@ def _inside(segs, x) -> bool:
     return any(a <= x < b for a, b in segs)
 
 
-def _item_segments(seg_a, seg_b, row0: int, n: int, s: int) -> list:
-    """Union of the two 64-row halves' tile segments with per-half and
-    causal flags (native 64x64 tiling; tiles == 64-key blocks)."""
+ITEM_ROWS = 256  # query rows per K4 work item: two 128-row tcgen05 tiles = four reference q-tiles
+F_CAUSAL, F_MASKS = 1 << 4, 1 << 5  # segment flags above the four per-quarter bits
+
+
+def _item_segments(quarters, row0: int, n: int, s: int) -> list:
+    """Union of the four 64-row quarters' tile segments with per-quarter
+    and causal flags (native 64x64 tiling; tiles == 64-key blocks)."""
     cb = max(0, (row0 + s - n - 63) // 64 + 1)  # first block whose last column passes row0's position
     pts = {cb}
-    for segs in (seg_a, seg_b or ()):
-        for a, b in segs:
+    for segs in quarters:
+        for a, b in segs or ():
             pts.update((a, b))
-    pts = sorted(p for p in pts)
+    pts = sorted(pts)
     out = []
     for x, y in zip(pts, pts[1:]):
-        fa = _inside(seg_a, x)
-        fb = bool(seg_b) and _inside(seg_b, x)
-        if not (fa or fb):
+        fl = 0
+        for qi, segs in enumerate(quarters):
+            if segs and _inside(segs, x):
+                fl |= 1 << qi
+        if not fl:
             continue
-        fl = int(fa) | (int(fb) << 1) | (int(x >= cb) << 2)
+        if x >= cb:
+            fl |= F_CAUSAL
         if out and out[-1][0] + out[-1][1] == x and out[-1][2] == fl:
             out[-1][1] += y - x
         else:
@@ -239,10 +246,9 @@ def plan_from_segments(head_segments, n_heads: int, n: int, s: int) -> PrefillPl
             sg = head_segments(h, qt)
             visited[h] += sum(b - a for a, b in sg)
             total[h] += diagonal_tile(qt, 64, 64, n, s) + 1
-        for i in range(0, n_qt, 2):
-            seg_a = head_segments(h, i)
-            seg_b = head_segments(h, i + 1) if i + 1 < n_qt else None
-            its = _item_segments(seg_a, seg_b, 64 * i, n, s)
+        for i in range(0, n_qt, ITEM_ROWS // 64):
+            quarters = [head_segments(h, i + k) if i + k < n_qt else None for k in range(ITEM_ROWS // 64)]
+            its = _item_segments(quarters, 64 * i, n, s)
             items.append((h, 64 * i, len(segs), len(its)))
             segs.extend((a, c, f, 0) for a, c, f in its)
     return _finish_plan(items, segs, None, visited, total)
@@ -265,8 +271,8 @@ def plan_generic(schedules, n_heads: int, n: int, s: int, tq: int, tk: int) -> P
             allow_tile[qt, tiles] = True
             visited[h] += len(tiles)
             total[h] += diagonal_tile(qt, tq, tk, n, s) + 1
-        for row0 in range(0, n, 128):
-            rows = np.arange(row0, min(row0 + 128, n))
+        for row0 in range(0, n, ITEM_ROWS):
+            rows = np.arange(row0, min(row0 + ITEM_ROWS, n))
             pos = rows + (s - n)
             tile_of_col = np.minimum(cols // tk, allow_tile.shape[1] - 1)
             ok = allow_tile[rows // tq][:, tile_of_col] & (cols[None, :] < s) & (cols[None, :] <= pos[:, None])
@@ -276,9 +282,9 @@ def plan_generic(schedules, n_heads: int, n: int, s: int, tq: int, tk: int) -> P
             for b in np.nonzero(blk_any)[0]:
                 bits = ok[:, b * 64:(b + 1) * 64]
                 words = (bits.astype(np.uint64) << np.arange(64, dtype=np.uint64)[None, :]).sum(axis=1, dtype=np.uint64)
-                block_masks = np.zeros(128, np.uint64)
+                block_masks = np.zeros(ITEM_ROWS, np.uint64)
                 block_masks[:len(rows)] = words
-                segs.append((int(b), 1, 3 | 8, len(masks) // 128))
+                segs.append((int(b), 1, 0xF | F_MASKS, len(masks) // ITEM_ROWS))
                 masks.extend(block_masks.tolist())
                 nseg += 1
             items.append((h, row0, first_seg, nseg))

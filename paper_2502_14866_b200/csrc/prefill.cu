@@ -7,19 +7,25 @@
 // causal mask on tiles that cross the diagonal (attn.py:315-319) and an
 // online softmax over the visited tiles (attn.py:191-229).
 //
-// One CTA = one 128-row query block of one head (two reference query tiles;
-// per-64-row "half" flags keep their schedules distinct).  Warp roles:
-//   warp 0      TMA producer: Q once, then K/V 64-key blocks into a
-//               NS-stage ring (SWIZZLE_128B, mbarrier complete_tx)
-//   warp 1      MMA issuer (one elected thread): S_j = Q K_j^T into a
-//               double-buffered TMEM tile (M=128, N=64, K=D), and
-//               O += P_j V_j (M=128, N=D, K=64; V is an MN-major operand)
-//   warps 2..5  softmax: one thread per query row reads S from TMEM
-//               (tcgen05.ld 32x32b), masks, exp2, writes P (fp16/bf16)
-//               into a swizzled K-major smem tile for the PV MMA; O is
-//               rescaled in TMEM only when the running max grows by more
-//               than 2^8 (exact: the stale max is a shared reference point)
-// S_{j+1} is issued before PV_j so the tensor core overlaps the softmax.
+// One CTA = one 256-row query block of one head: two 128-row tcgen05 tiles
+// (four reference query tiles; per-64-row "quarter" flags on every segment
+// keep their schedules distinct) that share one K/V stream.  Warp roles:
+//   warp 0      TMA producer: both Q tiles once, then K/V 64-key blocks into
+//               a kNS-stage ring (SWIZZLE_128B, mbarrier complete_tx)
+//   warp 1      MMA issuer (one elected thread), per key block j:
+//                 S_t,j = Q_t K_j^T   (M=128, N=64, K=D) for t = 0, 1 into
+//                 double-buffered TMEM, then O_t += P_t,j-1 V_j-1 (M=128,
+//                 N=D, K=64; V is an MN-major operand), so the tensor core
+//                 always has the other tile's work while one tile's softmax
+//                 runs (FA4-style ping-pong)
+//   warps 2..5  softmax of tile 0, warps 6..9 softmax of tile 1: one thread
+//               per query row reads S from TMEM (tcgen05.ld 32x32b), masks
+//               only blocks that need it, exp2 with the scale folded into
+//               one FFMA2 per pair, writes P (fp16/bf16) into a swizzled
+//               K-major smem tile; O is rescaled in TMEM only when the
+//               running max grows by more than 2^8 (exact: the stale max is a
+//               shared reference point)
+// TMEM: S[tile][buf] at columns tile*128 + buf*64, O[tile] at 256 + tile*128.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <mutex>
@@ -30,23 +36,25 @@
 namespace sk {
 namespace {
 
-constexpr int kNS = 3;            // K/V pipeline stages
-constexpr int kPfThreads = 192;   // 6 warps
+constexpr int kNS = 3;             // K/V pipeline stages
+constexpr int kPfThreads = 320;    // 10 warps
+constexpr int kItemRows = 256;     // two 128-row tiles
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr uint32_t kFlagCausal = 1u << 4, kFlagMasks = 1u << 5;
 
 template <int D>
 struct PfSmem {
   static constexpr int NC = D / 64;  // 128-byte column chunks
-  alignas(1024) uint8_t q[NC][128 * 128];
+  alignas(1024) uint8_t q[2][NC][128 * 128];
   alignas(1024) uint8_t kv[kNS][2][NC][64 * 128];
-  alignas(1024) uint8_t p[2][128 * 128];
+  alignas(1024) uint8_t p[2][2][128 * 128];
   uint64_t q_full;
   uint64_t kv_full[kNS];
   uint64_t kv_empty[kNS];
-  uint64_t s_full[2];
-  uint64_t p_full[2];
-  uint64_t p_empty[2];
-  uint64_t o_done;
+  uint64_t s_full[2][2];
+  uint64_t p_full[2][2];
+  uint64_t p_empty[2][2];
+  uint64_t o_done[2];
   uint32_t tmem_base;
 };
 
@@ -87,6 +95,28 @@ struct SegWalk {
   }
 };
 
+// packed fp32x2 helpers (FFMA2 / FADD2 on sm_100)
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(uint64_t r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 template <typename T, int D>
 __global__ void __launch_bounds__(kPfThreads, 1)
     prefill_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -94,8 +124,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   using Sm = PfSmem<D>;
   constexpr int NC = Sm::NC;
   constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
-  constexpr uint32_t kTmemCols = 256;  // S[2] (2 x 64) + O (D <= 128)
-  constexpr uint32_t kOCol = 128;
+  constexpr uint32_t kTmemCols = 512;
+  constexpr uint32_t kOCol = 256;
   extern __shared__ uint8_t smem_raw[];
   Sm& sm = *reinterpret_cast<Sm*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
@@ -111,12 +141,14 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       mbar_init(&sm.kv_full[i], 1);
       mbar_init(&sm.kv_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.s_full[i], 1);
-      mbar_init(&sm.p_full[i], 4);
-      mbar_init(&sm.p_empty[i], 1);
+    for (int t = 0; t < 2; ++t) {
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&sm.s_full[t][b], 1);
+        mbar_init(&sm.p_full[t][b], 4);
+        mbar_init(&sm.p_empty[t][b], 1);
+      }
+      mbar_init(&sm.o_done[t], 1);
     }
-    mbar_init(&sm.o_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(&sm.tmem_base);
@@ -131,8 +163,9 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       tma_prefetch_desc(&tq);
       tma_prefetch_desc(&tk);
       tma_prefetch_desc(&tv);
-      mbar_arrive_expect_tx(&sm.q_full, NC * 128 * 128);
-      for (int c = 0; c < NC; ++c) tma_load_3d(sm.q[c], &tq, &sm.q_full, 64 * c, item.head, item.row0);
+      mbar_arrive_expect_tx(&sm.q_full, 2 * NC * 128 * 128);
+      for (int t = 0; t < 2; ++t)
+        for (int c = 0; c < NC; ++c) tma_load_3d(sm.q[t][c], &tq, &sm.q_full, 64 * c, item.head, item.row0 + 128 * t);
       int j = 0;
       for (SegWalk w(prm.segs, item.seg_begin, item.seg_count); !w.done(); w.next(), ++j) {
         const int st = j % kNS;
@@ -152,83 +185,91 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     constexpr uint32_t idesc_o = make_idesc_f16(128, D, kBF16, false, true);
     mbar_wait(&sm.q_full, 0);
     tc_fence_after();
-    auto issue_s = [&](int jj) {
+    auto issue_pv = [&](int jj) {  // O_t += P_t,jj V_jj for both tiles
       const int st = jj % kNS;
-      mbar_wait(&sm.kv_full[st], (jj / kNS) & 1);
-      tc_fence_after();
-      if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          uint64_t a = make_sdesc_sw128(smem_u32(sm.q[kk / 4]) + (kk % 4) * 32, 16, 1024);
-          uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][0][kk / 4]) + (kk % 4) * 32, 16, 1024);
-          mma_f16_ss(tmem + (jj & 1) * 64, a, b, idesc_s, kk > 0);
+      for (int t = 0; t < 2; ++t) {
+        mbar_wait(&sm.p_full[t][jj & 1], (jj >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            uint64_t a = make_sdesc_sw128(smem_u32(sm.p[t][jj & 1]) + kk * 32, 16, 1024);
+            uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][1][0]) + kk * 2048, 64 * 128, 1024);
+            mma_f16_ss(tmem + kOCol + t * 128, a, b, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&sm.p_empty[t][jj & 1]);
+          mma_commit(&sm.o_done[t]);
+          if (t == 1) mma_commit(&sm.kv_empty[st]);
         }
-        mma_commit(&sm.s_full[jj & 1]);
+        __syncwarp();
       }
-      __syncwarp();
     };
-    if (n_blocks > 0) issue_s(0);
     for (int j = 0; j < n_blocks; ++j) {
-      if (j + 1 < n_blocks) issue_s(j + 1);
-      mbar_wait(&sm.p_full[j & 1], (j >> 1) & 1);
+      const int st = j % kNS;
+      mbar_wait(&sm.kv_full[st], (j / kNS) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const int st = j % kNS;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          uint64_t a = make_sdesc_sw128(smem_u32(sm.p[j & 1]) + kk * 32, 16, 1024);
-          uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][1][0]) + kk * 2048, 64 * 128, 1024);
-          mma_f16_ss(tmem + kOCol, a, b, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        for (int t = 0; t < 2; ++t) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            uint64_t a = make_sdesc_sw128(smem_u32(sm.q[t][kk / 4]) + (kk % 4) * 32, 16, 1024);
+            uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][0][kk / 4]) + (kk % 4) * 32, 16, 1024);
+            mma_f16_ss(tmem + t * 128 + (j & 1) * 64, a, b, idesc_s, kk > 0);
+          }
+          mma_commit(&sm.s_full[t][j & 1]);
         }
-        mma_commit(&sm.kv_empty[st]);
-        mma_commit(&sm.p_empty[j & 1]);
-        mma_commit(&sm.o_done);
       }
       __syncwarp();
+      if (j > 0) issue_pv(j - 1);
     }
+    if (n_blocks > 0) issue_pv(n_blocks - 1);
   } else {
     // ------------------------------ softmax -----------------------------------
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = quarter * 32 + lane;
+    const int t = (warp - 2) >> 2;   // tile of this warpgroup
+    const int quarter = warp & 3;    // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;  // row within the tile
     const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
-    const int pos = item.row0 + row + (prm.n_kv - prm.n_q);
-    const uint32_t half_bit = row < 64 ? 1u : 2u;
+    const uint32_t s_col = t * 128, o_col = kOCol + t * 128;
+    const int pos = item.row0 + 128 * t + row + (prm.n_kv - prm.n_q);
+    const uint32_t q_bit = 1u << (2 * t + (row >> 6));
     const float sl2 = prm.scale_log2;
     float m_run = -INFINITY, l_run = 0.f;
     int j = 0;
     for (SegWalk w(prm.segs, item.seg_begin, item.seg_count); !w.done(); w.next(), ++j) {
-      mbar_wait(&sm.s_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&sm.s_full[t][j & 1], (j >> 1) & 1);
       tc_fence_after();
       float s[64];
       {
         uint32_t r[64];
-        tmem_ld_x32(trow + (j & 1) * 64, r);
-        tmem_ld_x32(trow + (j & 1) * 64 + 32, r + 32);
+        tmem_ld_x32(trow + s_col + (j & 1) * 64, r);
+        tmem_ld_x32(trow + s_col + (j & 1) * 64 + 32, r + 32);
         tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 64; ++i) s[i] = __uint_as_float(r[i]);
       }
       const uint32_t fl = w.flags;
-      const bool active = fl & half_bit;
+      const bool active = fl & q_bit;
       const int col0 = w.block() * 64;
-      const int lim = (fl & 4u) ? pos - col0 : 64;  // columns c <= lim visible
+      const int lim = (fl & kFlagCausal) ? pos - col0 : 64;  // columns c <= lim visible
       float mx;
-      if (active && lim >= 63 && !(fl & 8u)) {
-        // fast path (almost every block): the whole row is visible; the
-        // max is taken on raw scores (scale > 0 commutes with max)
-        float t[8];
+      if (active && lim >= 63 && !(fl & kFlagMasks)) {
+        // fast path (almost every block): the whole row is visible; the max
+        // is taken on raw scores (scale > 0 commutes with max)
+        float tm[8];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) t[g] = fmax3(s[8 * g], s[8 * g + 1], s[8 * g + 2]);
+        for (int g = 0; g < 8; ++g) tm[g] = fmax3(s[8 * g], s[8 * g + 1], s[8 * g + 2]);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) t[g] = fmax3(t[g], s[8 * g + 3], s[8 * g + 4]);
+        for (int g = 0; g < 8; ++g) tm[g] = fmax3(tm[g], s[8 * g + 3], s[8 * g + 4]);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) t[g] = fmax3(t[g], s[8 * g + 5], s[8 * g + 6]);
+        for (int g = 0; g < 8; ++g) tm[g] = fmax3(tm[g], s[8 * g + 5], s[8 * g + 6]);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) t[g] = fmaxf(t[g], s[8 * g + 7]);
-        mx = fmax3(fmax3(t[0], t[1], t[2]), fmax3(t[3], t[4], t[5]), fmaxf(t[6], t[7])) * sl2;
+        for (int g = 0; g < 8; ++g) tm[g] = fmaxf(tm[g], s[8 * g + 7]);
+        mx = fmax3(fmax3(tm[0], tm[1], tm[2]), fmax3(tm[3], tm[4], tm[5]), fmaxf(tm[6], tm[7])) * sl2;
       } else {
         uint64_t emask = ~0ull;
-        if (fl & 8u) emask = prm.row_masks[(int64_t)(w.mask_base + w.i) * 128 + row];
+        if (fl & kFlagMasks) emask = prm.row_masks[(int64_t)(w.mask_base + w.i) * kItemRows + 128 * t + row];
         mx = -INFINITY;
 #pragma unroll
         for (int i = 0; i < 64; ++i) {
@@ -239,21 +280,21 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         mx *= sl2;
       }
       // lazy rescale: only when the max grows by more than 2^threshold
-      float m_new = fmaxf(m_run, mx);
-      bool need = (m_run != -INFINITY) && (m_new > m_run + kRescaleThreshold);
+      const float m_new = fmaxf(m_run, mx);
+      const bool need = (m_run != -INFINITY) && (m_new > m_run + kRescaleThreshold);
       if (m_run == -INFINITY) m_run = m_new;
       if (__any_sync(0xffffffffu, need)) {
-        if (j > 0) mbar_wait(&sm.o_done, (j - 1) & 1);  // PV_{j-1} landed in O
+        if (j > 0) mbar_wait(&sm.o_done[t], (j - 1) & 1);  // PV_{j-1} landed in O
         tc_fence_after();
         const float alpha = need ? exp2f(m_run - m_new) : 1.f;
 #pragma unroll
         for (int c = 0; c < D; c += 16) {
           uint32_t r[16];
-          tmem_ld_x16(trow + kOCol + c, r);
+          tmem_ld_x16(trow + o_col + c, r);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-          tmem_st_x16(trow + kOCol + c, r);
+          tmem_st_x16(trow + o_col + c, r);
         }
         tmem_wait_st();
         if (need) {
@@ -261,19 +302,24 @@ __global__ void __launch_bounds__(kPfThreads, 1)
           m_run = m_new;
         }
       }
-      // p = 2^(s*scale - m): one FFMA + one MUFU.EX2 per element (-inf -> 0)
+      // p = 2^(s*scale - m): one FFMA2 per pair + one MUFU.EX2 each (-inf -> 0)
       const float shift = m_run == -INFINITY ? 0.f : m_run;
-      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+      const uint64_t sl2x2 = f2_pack(sl2, sl2), nsh = f2_pack(-shift, -shift);
+      uint64_t rs[4] = {0ull, 0ull, 0ull, 0ull};
       uint32_t pk[32];
 #pragma unroll
       for (int i = 0; i < 64; i += 2) {
-        const float p0 = fast_exp2(fmaf(s[i], sl2, -shift)), p1 = fast_exp2(fmaf(s[i + 1], sl2, -shift));
-        rs4[(i / 2) & 3] += p0 + p1;
+        const float2 e = f2_unpack(f2_fma(f2_pack(s[i], s[i + 1]), sl2x2, nsh));
+        const float p0 = fast_exp2(e.x), p1 = fast_exp2(e.y);
+        rs[(i / 2) & 3] = f2_add(rs[(i / 2) & 3], f2_pack(p0, p1));
         pk[i / 2] = kBF16 ? pack_bf162(p0, p1) : pack_half2(p0, p1);
       }
-      l_run += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
-      if (j >= 2) mbar_wait(&sm.p_empty[j & 1], ((j >> 1) - 1) & 1);
-      uint8_t* prow = sm.p[j & 1] + row * 128;
+      {
+        const float2 a = f2_unpack(f2_add(f2_add(rs[0], rs[1]), f2_add(rs[2], rs[3])));
+        l_run += a.x + a.y;
+      }
+      if (j >= 2) mbar_wait(&sm.p_empty[t][j & 1], ((j >> 1) - 1) & 1);
+      uint8_t* prow = sm.p[t][j & 1] + row * 128;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         uint4 v = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
@@ -282,20 +328,20 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.p_full[j & 1]);
+      if (lane == 0) mbar_arrive(&sm.p_full[t][j & 1]);
     }
     // epilogue: O / l -> out
     if (n_blocks > 0) {
-      mbar_wait(&sm.o_done, (n_blocks - 1) & 1);
+      mbar_wait(&sm.o_done[t], (n_blocks - 1) & 1);
       tc_fence_after();
     }
-    const int grow = item.row0 + row;
+    const int grow = item.row0 + 128 * t + row;
     const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
     T* orow = reinterpret_cast<T*>(prm.out) + ((int64_t)grow * prm.n_heads + item.head) * D;
 #pragma unroll
     for (int c = 0; c < D; c += 16) {
       uint32_t r[16];
-      tmem_ld_x16(trow + kOCol + c, r);
+      tmem_ld_x16(trow + o_col + c, r);
       tmem_wait_ld();
       uint32_t pk[8];
 #pragma unroll

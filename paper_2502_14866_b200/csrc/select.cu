@@ -25,6 +25,8 @@
 //   where the candidates' keys differ; ties go to the lower page index
 //   (selector.py:106); union with the pins; ascending compaction by a
 //   block-wide scan over page order.
+#include <cstdlib>
+
 #include "sk_common.cuh"
 #include "sk_sm100.cuh"
 
@@ -424,6 +426,8 @@ int select_dispatch(const PoolView& pv, int n_streams, const void* q, int64_t q_
   }
   dim3 grid((max_pages + kPagesPerCta - 1) / kPagesPerCta, n_streams);
   const T* qt = static_cast<const T*>(q);
+  const int dbg = getenv("SK_SEL_DEBUG") ? atoi(getenv("SK_SEL_DEBUG")) : 0;  // temporary timing switch
+  if (dbg != 2) {
 #define SK_SCORE(LPV)                                                                                       \
   do {                                                                                                      \
     cudaFuncSetAttribute(score_kernel<T, LPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
@@ -438,6 +442,8 @@ int select_dispatch(const PoolView& pv, int n_streams, const void* q, int64_t q_
   else SK_SCORE(32);
 #undef SK_SCORE
   SK_CHECK_LAUNCH("score_kernel");
+  }
+  if (dbg == 1) return SK_OK;
   const int stage = max_pages < kTopkStage ? max_pages : kTopkStage;
   const size_t tsmem = (size_t)stage * 8;
   cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
