@@ -31,6 +31,7 @@
 #include <cstdlib>
 
 #include "append_impl.cuh"
+#include "sk_sm100.cuh"
 
 namespace sk {
 int append_launch(const sk_pool* pool, int n_streams, const void* k_src, const void* v_src, int64_t ss, int64_t ts,
@@ -69,21 +70,22 @@ struct DecodeParams {
   int dbg;  // temporary: phase cut-off for timing experiments (SK_DEC_DEBUG)
 };
 
-// m16n8k16 MMA, fp32 accumulate; rows 8..15 of A are zero (group rows <= 8).
+// m16n8k16 MMA, fp32 accumulate.
 template <typename MT>
-__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+__device__ __forceinline__ void mma16816_full(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                              uint32_t b0, uint32_t b1) {
   if constexpr (std::is_same<MT, __half>::value) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};"
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
   } else {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};"
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
   }
 }
 
@@ -131,93 +133,112 @@ __device__ __forceinline__ bool contains(const int32_t* a, int n, int x) {
   return false;
 }
 
-// Per-(warp, row) online-softmax state + the thread's output channels
-// (row r = lane/4, channels 8*cn + 2*j + e, j = lane%4).
+// movmatrix: transpose an 8x8 b16 matrix held in the standard fragment
+// layout (thread l holds row l/4, columns 2(l%4), 2(l%4)+1).
+__device__ __forceinline__ uint32_t transpose8x8(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+// Per-(warp) online-softmax state of the thread's two group rows 2j, 2j+1
+// and its output channels 16*ct + g + 8*h (g = lane/4, j = lane%4).
 template <int D>
 struct RowState {
-  float m, l;
-  float o[D / 4];
+  float m[2], l[2];
+  float o[D / 16][4];  // [ct][2h + e]: channel 16ct + g + 8h, row 2j + e
 };
 
-// One whole page for one warp.  KIND: 0 raw pages (MMA in T), 1 nibble
-// codes, 2 byte codes (MMA in fp16).
+// One whole page for one warp, computed TRANSPOSED so that the 16-row MMA
+// dimension carries tokens (QK) and channels (PV) and the group rows (<= 8)
+// sit in N = 8: S^T = K q'^T and O^T += V^T P^T, half the m16n8k16 MMAs of
+// the rows-in-M form.  The A fragments are exactly the bytes K1 already
+// stores per (token, lane%4) and (channel tile, lane) (sk_layout.cuh); P goes
+// from the S^T accumulator to the P^T operand with one movmatrix per 8x8.
+// KIND: 0 raw pages (MMA in T), 1 nibble codes, 2 byte codes (MMA in fp16).
 template <typename T, int KIND, int D, int P>
-__device__ __forceinline__ void page_attend(const uint8_t* pg, int tok_in_page, bool attend,
+__device__ __forceinline__ void page_attend(const uint8_t* pg, int tok_in_page, uint32_t att_mask,
                                             const uint32_t (&qw)[D / 8], float sl2, float inv_levels,
                                             RowState<D>& st) {
   using MT = typename std::conditional<KIND == 0, T, __half>::type;
-  constexpr int NKS = D / 16;  // QK k-steps
-  constexpr int NCN = D / 8;   // PV n-tiles (8 channels)
-  constexpr int NTT = P / 16;  // 16-token tiles
+  constexpr int NKS = D / 16;  // QK k-steps (16 dims)
+  constexpr int NCT = D / 16;  // PV M-tiles (16 channels)
+  constexpr int NTT = P / 16;  // 16-token tiles (QK M-tiles, PV k-steps)
   constexpr int RB = KIND == 0 ? 2 * D : (KIND == 1 ? D / 2 : D);
-  const int lane = threadIdx.x & 31, r = lane >> 2, j = lane & 3;
+  constexpr int KW = KIND == 1 ? D / 32 : (KIND == 2 ? D / 16 : D / 8);  // words per (token, lane%4)
+  constexpr int VW = KIND == 1 ? P / 32 : (KIND == 2 ? P / 16 : P / 8);  // words per (cn, lane)
+  const int lane = threadIdx.x & 31, g = lane >> 2, j = lane & 3;
   const uint8_t* kc = pg;
   const uint8_t* vc = pg + P * RB;
   const T* bnd = reinterpret_cast<const T*>(pg + 2 * P * RB);
 
-  // ---- issue the page's loads up front (one round trip) ----------------------
-  // K codes: tile tt, n-tile h2 -> token 16tt + 8h2 + r, this lane's chunk j
-  constexpr int KW = KIND == 1 ? D / 32 : (KIND == 2 ? D / 16 : D / 8);  // 32-bit words per (token, lane)
-  uint32_t kw[NTT][2][KW];
+  // ---- loads, issued before any math (one round trip) ------------------------
+  // K codes of tokens 16tt + g + 8h (A rows), this lane's dim chunk j
+  uint32_t kw[KIND == 0 ? 1 : NTT][2][KW];
+  auto load_k = [&](int tt, uint32_t (&dst)[2][KW]) {
 #pragma unroll
-  for (int tt = 0; tt < NTT; ++tt)
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      const uint8_t* src = kc + (16 * tt + 8 * h2 + r) * RB + j * (RB / 4);
+    for (int h = 0; h < 2; ++h) {
+      const uint8_t* src = kc + (16 * tt + 8 * h + g) * RB + j * (RB / 4);
       if constexpr (KW == 2) {
-        uint2 v = ldg8(src);
-        kw[tt][h2][0] = v.x; kw[tt][h2][1] = v.y;
+        const uint2 v = ldg8(src);
+        dst[h][0] = v.x; dst[h][1] = v.y;
       } else {
 #pragma unroll
         for (int i = 0; i < KW / 4; ++i) {
-          uint4 v = ldg16(src + 16 * i);
-          kw[tt][h2][4 * i] = v.x; kw[tt][h2][4 * i + 1] = v.y; kw[tt][h2][4 * i + 2] = v.z; kw[tt][h2][4 * i + 3] = v.w;
+          const uint4 v = ldg16(src + 16 * i);
+          dst[h][4 * i] = v.x; dst[h][4 * i + 1] = v.y; dst[h][4 * i + 2] = v.z; dst[h][4 * i + 3] = v.w;
         }
       }
     }
-  // K / V bounds of this lane's D/4 dims / channels: contiguous at j*(D/4)
+  };
+  if constexpr (KIND != 0) {
+#pragma unroll
+    for (int tt = 0; tt < NTT; ++tt) load_k(tt, kw[tt]);
+  }
+  // bounds: K in kbound order (this lane's dims at j*D/4), V in vbound order
+  // (channels 16ct + g + 8h at (g/2)*D/4 + 4ct + 2h + g%2)
   uint32_t kb_lo[D / 8], kb_hi[D / 8], vb_lo[D / 8], vb_hi[D / 8];
   if constexpr (KIND != 0) {
 #pragma unroll
     for (int i = 0; i < D / 32; ++i) {
-      uint4 a = ldg16(bnd + j * (D / 4) + 8 * i), b = ldg16(bnd + D + j * (D / 4) + 8 * i);
-      uint4 c = ldg16(bnd + 2 * D + j * (D / 4) + 8 * i), d = ldg16(bnd + 3 * D + j * (D / 4) + 8 * i);
+      const uint4 a = ldg16(bnd + j * (D / 4) + 8 * i), b = ldg16(bnd + D + j * (D / 4) + 8 * i);
+      const uint4 c = ldg16(bnd + 2 * D + (g >> 1) * (D / 4) + 8 * i);
+      const uint4 d = ldg16(bnd + 3 * D + (g >> 1) * (D / 4) + 8 * i);
       kb_lo[4 * i] = a.x; kb_lo[4 * i + 1] = a.y; kb_lo[4 * i + 2] = a.z; kb_lo[4 * i + 3] = a.w;
       kb_hi[4 * i] = b.x; kb_hi[4 * i + 1] = b.y; kb_hi[4 * i + 2] = b.z; kb_hi[4 * i + 3] = b.w;
       vb_lo[4 * i] = c.x; vb_lo[4 * i + 1] = c.y; vb_lo[4 * i + 2] = c.z; vb_lo[4 * i + 3] = c.w;
       vb_hi[4 * i] = d.x; vb_hi[4 * i + 1] = d.y; vb_hi[4 * i + 2] = d.z; vb_hi[4 * i + 3] = d.w;
     }
   }
-  // V codes of this lane: (cn, lane) chunk of the whole page (KIND 1/2)
-  constexpr int VW = KIND == 1 ? P / 32 : P / 16;  // 32-bit words per (cn, lane)
-  uint32_t vw[NCN][KIND == 0 ? 1 : VW];
+  // V codes: chunk (cn, lane) of the whole page, cn = 2ct + h (KIND 1/2)
+  uint32_t vw[KIND == 0 ? 1 : 2 * NCT][VW];
   if constexpr (KIND != 0) {
 #pragma unroll
-    for (int cn = 0; cn < NCN; ++cn) {
+    for (int cn = 0; cn < 2 * NCT; ++cn) {
       const uint8_t* src = vc + (32 * cn + lane) * (VW * 4);
       if constexpr (VW == 1) {
         vw[cn][0] = __ldg(reinterpret_cast<const uint32_t*>(src));
       } else if constexpr (VW == 2) {
-        uint2 v = ldg8(src);
+        const uint2 v = ldg8(src);
         vw[cn][0] = v.x; vw[cn][1] = v.y;
       } else {
 #pragma unroll
         for (int i = 0; i < VW / 4; ++i) {
-          uint4 v = ldg16(src + 16 * i);
+          const uint4 v = ldg16(src + 16 * i);
           vw[cn][4 * i] = v.x; vw[cn][4 * i + 1] = v.y; vw[cn][4 * i + 2] = v.z; vw[cn][4 * i + 3] = v.w;
         }
       }
     }
   }
 
-  // ---- K side: q' = q * s_k / smax (A fragments), qz = q . lo_k ----------------
-  uint32_t afr[NKS][2];
+  // ---- K side: B = q'^T with q' = q * s_k / smax (row g), qz_r = q_r . lo_k --------
+  uint32_t bq[NKS][2];
   float smax = 1.f, qz = 0.f;
   if constexpr (KIND == 0) {
 #pragma unroll
     for (int ks = 0; ks < NKS; ++ks) {
-      afr[ks][0] = qw[2 * ks];
-      afr[ks][1] = qw[2 * ks + 1];
+      bq[ks][0] = qw[2 * ks];
+      bq[ks][1] = qw[2 * ks + 1];
     }
   } else {
     float sk[D / 4];
@@ -237,122 +258,161 @@ __device__ __forceinline__ void page_attend(const uint8_t* pg, int tok_in_page, 
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
     qz += __shfl_xor_sync(0xffffffffu, qz, 1);
-    qz += __shfl_xor_sync(0xffffffffu, qz, 2);
+    qz += __shfl_xor_sync(0xffffffffu, qz, 2);  // qz of row g
     smax = mx;
     const float inv = 1.f / mx;
 #pragma unroll
     for (int ks = 0; ks < NKS; ++ks) {
-      // register ri = 2ks + h holds dims 16ks + 8h + 2j + {0,1} (kbound order)
       const float2 q0 = DT<T>::to_f2(qw[2 * ks]), q1 = DT<T>::to_f2(qw[2 * ks + 1]);
-      afr[ks][0] = pack2<MT>(q0.x * (sk[4 * ks] * inv), q0.y * (sk[4 * ks + 1] * inv));
-      afr[ks][1] = pack2<MT>(q1.x * (sk[4 * ks + 2] * inv), q1.y * (sk[4 * ks + 3] * inv));
+      bq[ks][0] = pack2<MT>(q0.x * (sk[4 * ks] * inv), q0.y * (sk[4 * ks + 1] * inv));
+      bq[ks][1] = pack2<MT>(q1.x * (sk[4 * ks + 2] * inv), q1.y * (sk[4 * ks + 3] * inv));
+    }
+  }
+  // the S^T accumulator holds rows 2j, 2j+1: fetch their qz from lanes 8j, 8j+4
+  const float qz0 = __shfl_sync(0xffffffffu, qz, 8 * j), qz1 = __shfl_sync(0xffffffffu, qz, 8 * j + 4);
+
+  // ---- S^T = K q'^T: tile tt gives tokens 16tt + g (+8), rows 2j, 2j+1 -------------
+  float sc[NTT][4];
+#pragma unroll
+  for (int tt = 0; tt < NTT; ++tt) {
+    uint32_t kt[2][KW];
+    if constexpr (KIND == 0) load_k(tt, kt);
+    const uint32_t (&kr)[2][KW] = KIND == 0 ? kt : kw[KIND == 0 ? 0 : tt];
+    float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int ks = 0; ks < NKS; ++ks) {
+      uint32_t a0, a1, a2, a3;  // (tok g, dims lo) (tok g+8, lo) (tok g, hi) (tok g+8, hi)
+      const int ri0 = 2 * ks, ri1 = 2 * ks + 1;
+      if constexpr (KIND == 1) {
+        a0 = nib2h(kr[0][ri0 / 4], ri0 % 4);
+        a1 = nib2h(kr[1][ri0 / 4], ri0 % 4);
+        a2 = nib2h(kr[0][ri1 / 4], ri1 % 4);
+        a3 = nib2h(kr[1][ri1 / 4], ri1 % 4);
+      } else if constexpr (KIND == 2) {
+        a0 = byte2h(kr[0][ks], 0);
+        a1 = byte2h(kr[1][ks], 0);
+        a2 = byte2h(kr[0][ks], 1);
+        a3 = byte2h(kr[1][ks], 1);
+      } else {
+        a0 = kr[0][ri0];
+        a1 = kr[1][ri0];
+        a2 = kr[0][ri1];
+        a3 = kr[1][ri1];
+      }
+      mma16816_full<MT>(c, a0, a1, a2, a3, bq[ks][0], bq[ks][1]);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const bool ok = 16 * tt + 8 * h + g < tok_in_page;
+      sc[tt][2 * h] = ok ? (c[2 * h] * smax + qz0) * sl2 : -INFINITY;
+      sc[tt][2 * h + 1] = ok ? (c[2 * h + 1] * smax + qz1) * sl2 : -INFINITY;
     }
   }
 
-  // ---- S = q' K^T for every tile ------------------------------------------------
-  float sc[NTT][2][2];
+  // ---- per-row page max, rescale, probabilities -----------------------------------
+  float tmax[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+  for (int tt = 0; tt < NTT; ++tt) {
+    tmax[0] = fmax3(tmax[0], sc[tt][0], sc[tt][2]);
+    tmax[1] = fmax3(tmax[1], sc[tt][1], sc[tt][3]);
+  }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    tmax[e] = fmaxf(tmax[e], __shfl_xor_sync(0xffffffffu, tmax[e], 4));
+    tmax[e] = fmaxf(tmax[e], __shfl_xor_sync(0xffffffffu, tmax[e], 8));
+    tmax[e] = fmaxf(tmax[e], __shfl_xor_sync(0xffffffffu, tmax[e], 16));
+  }
+  bool att[2];
+  float alpha[2], m_new[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    att[e] = (att_mask >> (2 * j + e)) & 1u;
+    m_new[e] = att[e] ? fmaxf(st.m[e], tmax[e]) : st.m[e];
+    alpha[e] = att[e] ? exp2f(st.m[e] - m_new[e]) : 1.f;  // exp2(-inf) = 0
+  }
+  uint32_t pb[NTT][2];  // P^T B fragments: (tokens 2j.., row g) / (tokens 2j+8.., row g)
+  float psum[2] = {0.f, 0.f};
 #pragma unroll
   for (int tt = 0; tt < NTT; ++tt)
 #pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      float c[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int ks = 0; ks < NKS; ++ks) {
-        uint32_t b0, b1;
-        const int ri0 = 2 * ks, ri1 = 2 * ks + 1;
-        if constexpr (KIND == 1) {
-          b0 = nib2h(kw[tt][h2][ri0 / 4], ri0 % 4);
-          b1 = nib2h(kw[tt][h2][ri1 / 4], ri1 % 4);
-        } else if constexpr (KIND == 2) {
-          b0 = byte2h(kw[tt][h2][ks], 0);
-          b1 = byte2h(kw[tt][h2][ks], 1);
-        } else {
-          b0 = kw[tt][h2][2 * ks];
-          b1 = kw[tt][h2][2 * ks + 1];
-        }
-        mma16816<MT>(c, afr[ks][0], afr[ks][1], b0, b1);
-      }
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int t = 16 * tt + 8 * h2 + 2 * j + e;
-        const float v = (c[e] * smax + qz) * sl2;
-        sc[tt][h2][e] = t < tok_in_page ? v : -INFINITY;
-      }
+    for (int h = 0; h < 2; ++h) {
+      const float p0 = att[0] ? fast_exp2(sc[tt][2 * h] - m_new[0]) : 0.f;
+      const float p1 = att[1] ? fast_exp2(sc[tt][2 * h + 1] - m_new[1]) : 0.f;
+      const uint32_t pk = pack2<MT>(p0, p1);  // (token 16tt + 8h + g, rows 2j, 2j+1)
+      const float2 pr = unpack2<MT>(pk);     // the rounded values the MMA sees
+      psum[0] += pr.x;
+      psum[1] += pr.y;
+      pb[tt][h] = transpose8x8(pk);
     }
+  float prow[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    st.l[e] = st.l[e] * alpha[e] + psum[e];  // per-thread partial (tokens of lane g)
+    st.m[e] = m_new[e];
+    prow[e] = psum[e];
+    prow[e] += __shfl_xor_sync(0xffffffffu, prow[e], 4);
+    prow[e] += __shfl_xor_sync(0xffffffffu, prow[e], 8);
+    prow[e] += __shfl_xor_sync(0xffffffffu, prow[e], 16);
+  }
 
-  // ---- page max, rescale, probabilities -----------------------------------------
-  float tmax = -INFINITY;
+  // ---- O^T = alpha O^T + s_v (V^T P^T) + lo_v sum(P) -----------------------------
 #pragma unroll
-  for (int tt = 0; tt < NTT; ++tt)
-    tmax = fmaxf(tmax, fmaxf(fmaxf(sc[tt][0][0], sc[tt][0][1]), fmaxf(sc[tt][1][0], sc[tt][1][1])));
-  tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
-  tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
-  const float m_new = attend ? fmaxf(st.m, tmax) : st.m;
-  const float alpha = attend ? exp2f(st.m - m_new) : 1.f;  // exp2(-inf) = 0
-  uint32_t pfr[NTT][2];
-  float psum = 0.f;
-#pragma unroll
-  for (int tt = 0; tt < NTT; ++tt)
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      const float p0 = attend ? exp2f(sc[tt][h2][0] - m_new) : 0.f;
-      const float p1 = attend ? exp2f(sc[tt][h2][1] - m_new) : 0.f;
-      const uint32_t pk = pack2<MT>(p0, p1);
-      const float2 pr = unpack2<MT>(pk);  // the rounded values the MMA sees
-      psum += pr.x + pr.y;
-      pfr[tt][h2] = pk;
-    }
-  st.l = st.l * alpha + psum;  // per-thread partial (tokens of lane j)
-  st.m = m_new;
-  float prow = psum;
-  prow += __shfl_xor_sync(0xffffffffu, prow, 1);
-  prow += __shfl_xor_sync(0xffffffffu, prow, 2);
-
-  // ---- O = alpha O + s_v (P C_v) + lo_v sum(P) ------------------------------------
-#pragma unroll
-  for (int cn = 0; cn < NCN; ++cn) {
-    float c[4] = {0.f, 0.f, 0.f, 0.f};
-    uint32_t vraw[KIND == 0 ? NTT * 2 : 1];
+  for (int ct = 0; ct < NCT; ++ct) {
+    uint32_t vt[2][KIND == 0 ? NTT * 2 : 1];
     if constexpr (KIND == 0) {
-      const uint8_t* src = vc + (32 * cn + lane) * (P / 2);
 #pragma unroll
-      for (int i = 0; i < NTT / 2; ++i) {
-        uint4 v = ldg16(src + 16 * i);
-        vraw[4 * i] = v.x; vraw[4 * i + 1] = v.y; vraw[4 * i + 2] = v.z; vraw[4 * i + 3] = v.w;
-      }
-      if constexpr (NTT % 2) {
-        uint2 v = ldg8(src + 16 * (NTT / 2));
-        vraw[NTT * 2 - 2] = v.x; vraw[NTT * 2 - 1] = v.y;
+      for (int h = 0; h < 2; ++h) {
+        const uint8_t* src = vc + (32 * (2 * ct + h) + lane) * (P / 2);
+#pragma unroll
+        for (int i = 0; i < NTT / 2; ++i) {
+          const uint4 v = ldg16(src + 16 * i);
+          vt[h][4 * i] = v.x; vt[h][4 * i + 1] = v.y; vt[h][4 * i + 2] = v.z; vt[h][4 * i + 3] = v.w;
+        }
+        if constexpr (NTT % 2) {
+          const uint2 v = ldg8(src + 16 * (NTT / 2));
+          vt[h][NTT * 2 - 2] = v.x; vt[h][NTT * 2 - 1] = v.y;
+        }
       }
     }
+    float c[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int tt = 0; tt < NTT; ++tt) {
-      uint32_t b0, b1;
+      uint32_t a0, a1, a2, a3;  // (ch g, tok lo) (ch g+8, lo) (ch g, hi) (ch g+8, hi)
       const int ri0 = 2 * tt, ri1 = 2 * tt + 1;
       if constexpr (KIND == 1) {
-        b0 = nib2h(vw[cn][ri0 / 4], ri0 % 4);
-        b1 = nib2h(vw[cn][ri1 / 4], ri1 % 4);
+        a0 = nib2h(vw[2 * ct][ri0 / 4], ri0 % 4);
+        a1 = nib2h(vw[2 * ct + 1][ri0 / 4], ri0 % 4);
+        a2 = nib2h(vw[2 * ct][ri1 / 4], ri1 % 4);
+        a3 = nib2h(vw[2 * ct + 1][ri1 / 4], ri1 % 4);
       } else if constexpr (KIND == 2) {
-        b0 = byte2h(vw[cn][tt], 0);
-        b1 = byte2h(vw[cn][tt], 1);
+        a0 = byte2h(vw[2 * ct][tt], 0);
+        a1 = byte2h(vw[2 * ct + 1][tt], 0);
+        a2 = byte2h(vw[2 * ct][tt], 1);
+        a3 = byte2h(vw[2 * ct + 1][tt], 1);
       } else {
-        b0 = vraw[2 * tt];
-        b1 = vraw[2 * tt + 1];
+        a0 = vt[0][ri0];
+        a1 = vt[1][ri0];
+        a2 = vt[0][ri1];
+        a3 = vt[1][ri1];
       }
-      mma16816<MT>(c, pfr[tt][0], pfr[tt][1], b0, b1);
+      mma16816_full<MT>(c, a0, a1, a2, a3, pb[tt][0], pb[tt][1]);
     }
-    float add0 = c[0], add1 = c[1];
-    if constexpr (KIND != 0) {
-      // channels 8cn+2j, +1 sit in V-bound register cn (vbound order)
-      const float2 lo = DT<T>::to_f2(vb_lo[cn]), hi = DT<T>::to_f2(vb_hi[cn]);
-      float sa = (hi.x - lo.x) * inv_levels, sb = (hi.y - lo.y) * inv_levels;
-      sa = sa > 0.f ? sa : 1.f;
-      sb = sb > 0.f ? sb : 1.f;
-      add0 = fmaf(sa, c[0], lo.x * prow);
-      add1 = fmaf(sb, c[1], lo.y * prow);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float add0 = c[2 * h], add1 = c[2 * h + 1];
+      if constexpr (KIND != 0) {
+        // channel 16ct + 8h + g: vbound index (g/2)*D/4 + 2*(2ct+h) + g%2
+        const int wi = 2 * ct + h;  // register holding (cn = 2ct+h, e = 0/1)
+        const float2 lo = DT<T>::to_f2(vb_lo[wi]), hi = DT<T>::to_f2(vb_hi[wi]);
+        const float lo_c = (g & 1) ? lo.y : lo.x, hi_c = (g & 1) ? hi.y : hi.x;
+        float sc_ = (hi_c - lo_c) * inv_levels;
+        sc_ = sc_ > 0.f ? sc_ : 1.f;
+        add0 = fmaf(sc_, c[2 * h], lo_c * prow[0]);
+        add1 = fmaf(sc_, c[2 * h + 1], lo_c * prow[1]);
+      }
+      st.o[ct][2 * h] = fmaf(st.o[ct][2 * h], alpha[0], add0);
+      st.o[ct][2 * h + 1] = fmaf(st.o[ct][2 * h + 1], alpha[1], add1);
     }
-    st.o[2 * cn] = fmaf(st.o[2 * cn], alpha, add0);
-    st.o[2 * cn + 1] = fmaf(st.o[2 * cn + 1], alpha, add1);
   }
 }
 
@@ -374,7 +434,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   const int s = blockIdx.y;
   const int rank = blockIdx.x;  // == cluster rank (the cluster spans grid.x)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int r = lane >> 2, j = lane & 3;
+  const int r = lane >> 2, g = r, j = lane & 3;
   const int G = prm.G;
 
   if (prm.dbg == 1) return;
@@ -438,10 +498,15 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
 
   // ---- this warp's pages: unit u = rank + kCl * (warp + kWarps * i) -----------
   RowState<D> st;
-  st.m = -INFINITY;
-  st.l = 0.f;
 #pragma unroll
-  for (int i = 0; i < QR; ++i) st.o[i] = 0.f;
+  for (int e = 0; e < 2; ++e) {
+    st.m[e] = -INFINITY;
+    st.l[e] = 0.f;
+  }
+#pragma unroll
+  for (int ct = 0; ct < D / 16; ++ct)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) st.o[ct][i] = 0.f;
   const float sl2 = prm.scale_log2;
   const float inv_levels = KIND == 0 ? 1.f : 1.f / float((1 << pv.bits) - 1);
   for (int u = rank + kCl * warp; u < U; u += kCl * kWarps) {
@@ -454,23 +519,29 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
       pg = s_extra[u - nsel];
       um = smask;
     }
-    const bool attend = row_ok && ((um >> r) & 1u);
     const uint8_t* slot = pv.slot_ptr(s, pg);  // round trip 2 (page table)
-    page_attend<T, KIND, D, P>(slot, min(P, n_tok - pg * P), attend, qw, sl2, inv_levels, st);
+    page_attend<T, KIND, D, P>(slot, min(P, n_tok - pg * P), um & gmask, qw, sl2, inv_levels, st);
   }
 
   // ---- merge the CTA's warps ---------------------------------------------------
   {
-    float lt = st.l;
-    lt += __shfl_xor_sync(0xffffffffu, lt, 1);
-    lt += __shfl_xor_sync(0xffffffffu, lt, 2);
-    if (j == 0) {
-      s_m[warp][r] = st.m;
-      s_l[warp][r] = lt;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      float lt = st.l[e];
+      lt += __shfl_xor_sync(0xffffffffu, lt, 4);
+      lt += __shfl_xor_sync(0xffffffffu, lt, 8);
+      lt += __shfl_xor_sync(0xffffffffu, lt, 16);
+      if (g == 0) {
+        s_m[warp][2 * j + e] = st.m[e];
+        s_l[warp][2 * j + e] = lt;
+      }
     }
 #pragma unroll
-    for (int cn = 0; cn < D / 8; ++cn)
-      *reinterpret_cast<float2*>(&s_o[warp][r][8 * cn + 2 * j]) = make_float2(st.o[2 * cn], st.o[2 * cn + 1]);
+    for (int ct = 0; ct < D / 16; ++ct)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) s_o[warp][2 * j + e][16 * ct + 8 * h + g] = st.o[ct][2 * h + e];
   }
   __syncthreads();
   if (tid < G) {

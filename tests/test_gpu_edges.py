@@ -1,0 +1,165 @@
+"""B200 parity on the edge cases the reference's own tests exercise, against
+the pinned CPU oracle: ragged and non-square prefill (S > N), MHA and wide
+GQA groups, head_dim 64 and padded dims, bf16, all-streaming layers,
+degenerate budgets (all pages / pins only), decoding at 128k context, and
+KV-head shards recombining to the unsharded result."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2502_14866_b200 as sk
+from oracle import sparsekv_oracle as O
+from paper_2502_14866_b200.sharding import shard_decode_inputs, shard_heads, shard_prefill_inputs, shard_profiles
+
+pytestmark = pytest.mark.gpu
+
+ATOL = 2e-2
+MIN_COS = 0.9999
+
+
+def close(out, ref, atol=ATOL):
+    out = np.asarray(out, np.float64)
+    ref = np.asarray(ref, np.float64)
+    err = np.abs(out - ref).max()
+    assert err <= atol, f"max-abs {err:.3e}"
+    o = out.reshape(-1, out.shape[-1])
+    r = ref.reshape(-1, ref.shape[-1])
+    num = (o * r).sum(1)
+    den = np.linalg.norm(o, axis=1) * np.linalg.norm(r, axis=1)
+    cos = num[den > 0] / den[den > 0]
+    assert cos.size == 0 or cos.min() >= MIN_COS, f"min cosine {cos.min():.7f}"
+
+
+def fp16_vals(rng, *shape):
+    return rng.standard_normal(shape).astype(np.float16).astype(np.float32)
+
+
+def gates_for(h, rng):
+    return rng.uniform(0, 1, h).tolist()
+
+
+PREFILL_CASES = [
+    # n, s, h, h_kv, d, sparsity, sink, local
+    (200, 200, 8, 2, 128, 0.5, 1, 2),      # ragged N (not a multiple of 64 / 256)
+    (100, 300, 8, 2, 128, 0.5, 1, 2),      # history longer than the queries (attn.py:32-34)
+    (320, 320, 4, 4, 128, 0.5, 1, 1),      # MHA (Llama-2 style group of 1)
+    (256, 256, 8, 1, 128, 0.25, 2, 1),     # one KV head, group of 8
+    (192, 192, 8, 2, 64, 0.5, 1, 2),       # head_dim 64
+    (130, 130, 4, 2, 96, 0.5, 1, 1),       # head_dim 96 -> padded to 128 (scale uses 96)
+    (640, 640, 8, 2, 128, 1.0, 1, 3),      # every head streaming (all-Lambda layer)
+    (1, 65, 4, 2, 128, 0.5, 1, 1),         # a single query row
+]
+
+
+@pytest.mark.parametrize("case", PREFILL_CASES)
+def test_prefill_shapes_against_oracle(case):
+    n, s, h, h_kv, d, sp, sink, local = case
+    rng = np.random.default_rng(hash(case) % 2**32)
+    q, k, v = fp16_vals(rng, n, h, d), fp16_vals(rng, s, h_kv, d), fp16_vals(rng, s, h_kv, d)
+    gates = gates_for(h, rng)
+    eng = sk.Engine(sk.EngineConfig(quant_bits=4, sink_blocks=sink, local_blocks=local, target_sparsity=sp),
+                    sk.classify_heads(gates, sp, sink, local), device="cuda:0")
+    out = eng.prefill(sk.Workload(q, k, v))
+    ref_eng = O.OracleEngine(O.Config(quant_bits=4, sink_blocks=sink, local_blocks=local, target_sparsity=sp),
+                             O.assign_roles(gates, sp, sink, local))
+    ref = ref_eng.prefill(q, k, v)
+    close(out, ref)
+    assert {key: val for key, val in eng.ledger.tiles.items()} == ref_eng.tally.tiles
+
+
+def test_prefill_bf16_inputs():
+    rng = np.random.default_rng(5)
+    n = s = 384
+    h, h_kv, d = 8, 2, 128
+    q, k, v = fp16_vals(rng, n, h, d), fp16_vals(rng, s, h_kv, d), fp16_vals(rng, s, h_kv, d)
+    gates = gates_for(h, rng)
+    qt, kt, vt = (torch.from_numpy(a).to(torch.bfloat16).cuda() for a in (q, k, v))
+    eng = sk.Engine(sk.EngineConfig(), sk.classify_heads(gates, 0.5, 1, 2), device="cuda:0", dtype=torch.bfloat16)
+    out = eng.prefill(sk.Workload(qt, kt, vt)).float().cpu().numpy()
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731  (the oracle sees the bf16-rounded values)
+    ref = O.OracleEngine(O.Config(), O.assign_roles(gates, 0.5, 1, 2)).prefill(f(qt), f(kt), f(vt))
+    close(out, ref, atol=3e-2)
+
+
+DECODE_CASES = [
+    # s, h, h_kv, d, bits, budget, sparsity, steps
+    (2000, 4, 4, 128, 4, 512, 0.5, 6),       # MHA: streaming-only KV heads live in the ring pool
+    (3000, 8, 1, 128, 4, 1024, 0.25, 6),     # group of 8 rows per KV head
+    (1500, 8, 2, 64, 4, 512, 0.5, 6),        # head_dim 64
+    (1100, 8, 2, 128, 8, 8192, 0.5, 4),      # budget >= pages: every page, no scoring
+    (1100, 8, 2, 128, 4, 64, 0.5, 4),        # budget below the pins: pins only
+    (700, 8, 2, 128, None, 256, 0.5, 5),     # fp16 pages
+]
+
+
+@pytest.mark.parametrize("case", DECODE_CASES)
+def test_decode_shapes_against_oracle(case):
+    s, h, h_kv, d, bits, budget, sp, steps = case
+    rng = np.random.default_rng(abs(hash(case)) % 2**32)
+    gates = gates_for(h, rng)
+    k, v = fp16_vals(rng, s, h_kv, d), fp16_vals(rng, s, h_kv, d)
+    cfg = sk.EngineConfig(quant_bits=bits, budget_tokens=budget, reuse_interval=2, local_blocks=2,
+                          target_sparsity=sp)
+    eng = sk.Engine(cfg, sk.classify_heads(gates, sp, 1, 2), device="cuda:0")
+    eng.load_context(k, v)
+    ref = O.OracleEngine(O.Config(quant_bits=bits, budget_tokens=budget, reuse_interval=2, local_blocks=2,
+                                  target_sparsity=sp), O.assign_roles(gates, sp, 1, 2))
+    ref.load_context(k, v)
+    for t in range(steps):
+        qn, kn, vn = fp16_vals(rng, h, d), fp16_vals(rng, h_kv, d), fp16_vals(rng, h_kv, d)
+        res = eng.decode_step(qn, kn, vn)
+        rr = ref.decode_step(qn, kn, vn)
+        assert [tuple(tb.positions) for tb in res.index_tables] == rr.tables, f"step {t}"
+        assert res.invoked == rr.invoked
+        close(res.output, rr.output)
+    assert eng.ledger.tiles == ref.tally.tiles
+
+
+def test_decode_128k_selection_and_outputs():
+    """BASELINE cfg2 geometry for one layer (32/8/128, 128k tokens, budget
+    4096, reuse 4, KV4, balanced gates): 5 decode steps (two selection
+    steps) -- every index table bit-exact, outputs within tolerance."""
+    rng = np.random.default_rng(128)
+    s, h, h_kv, d = 131072, 32, 8, 128
+    gates = [0.9 - 0.001 * i if i % 4 < 2 else 0.1 + 0.001 * i for i in range(h)]
+    k, v = fp16_vals(rng, s, h_kv, d), fp16_vals(rng, s, h_kv, d)
+    cfg = sk.EngineConfig(quant_bits=4, budget_tokens=4096, reuse_interval=4, local_blocks=4)
+    eng = sk.Engine(cfg, sk.classify_heads(gates, 0.5, 1, 4), device="cuda:0")
+    eng.load_context(k, v)
+    ref = O.OracleEngine(O.Config(quant_bits=4, budget_tokens=4096, reuse_interval=4, local_blocks=4),
+                         O.assign_roles(gates, 0.5, 1, 4))
+    ref.load_context(k, v)
+    for t in range(5):
+        qn, kn, vn = fp16_vals(rng, h, d), fp16_vals(rng, h_kv, d), fp16_vals(rng, h_kv, d)
+        res = eng.decode_step(qn, kn, vn)
+        rr = ref.decode_step(qn, kn, vn)
+        assert [tuple(tb.positions) for tb in res.index_tables] == rr.tables, f"step {t}"
+        close(res.output, rr.output)
+    assert eng.ledger.selector_invocations == ref.tally.selector
+
+
+def test_kv_head_shards_recombine_bitwise():
+    """Two KV-head shards run as separate engines (what two ranks do) give,
+    concatenated by head, exactly the unsharded engine's prefill and decode
+    outputs: nothing in K1-K4 couples KV heads."""
+    rng = np.random.default_rng(9)
+    n = s = 512
+    h, h_kv, d = 8, 4, 128
+    gates = gates_for(h, rng)
+    prof = sk.classify_heads(gates, 0.5, 1, 2)
+    q, k, v = fp16_vals(rng, n, h, d), fp16_vals(rng, s, h_kv, d), fp16_vals(rng, s, h_kv, d)
+    cfg = sk.EngineConfig(budget_tokens=256, reuse_interval=2)
+    full = sk.Engine(cfg, prof, device="cuda:0")
+    out_full = full.prefill(sk.Workload(q, k, v))
+    shards = [shard_heads(h, h_kv, r, 2) for r in range(2)]
+    engs = [sk.Engine(cfg, shard_profiles(prof, sh), device="cuda:0") for sh in shards]
+    outs = [e.prefill(sk.Workload(*shard_prefill_inputs(q, k, v, sh))) for e, sh in zip(engs, shards)]
+    np.testing.assert_array_equal(np.concatenate(outs, axis=1), out_full)
+    for t in range(4):
+        qn, kn, vn = fp16_vals(rng, h, d), fp16_vals(rng, h_kv, d), fp16_vals(rng, h_kv, d)
+        rf = full.decode_step(qn, kn, vn)
+        parts = [e.decode_step(*shard_decode_inputs(qn, kn, vn, sh)) for e, sh in zip(engs, shards)]
+        np.testing.assert_array_equal(np.concatenate([p.output for p in parts], axis=0), rf.output)
+        assert [tuple(tb.positions) for p in parts for tb in p.index_tables] == \
+            [tuple(tb.positions) for tb in rf.index_tables]
