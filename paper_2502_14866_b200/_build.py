@@ -18,11 +18,11 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(PKG, "libsparsekv_b200.so")
+OBJ = os.path.join(ROOT, "build", os.environ.get("SK_OBJ_DIR", "obj"))
+LIB = os.environ.get("SK_LIB_OUT") or os.path.join(PKG, "libsparsekv_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-                     "-I" + os.path.join(ROOT, "include")] + os.environ.get("SK_NVCC_EXTRA", "").split()
+                     "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + os.environ.get("SK_NVCC_EXTRA", "").split()
 
 
 def nvcc() -> str:
@@ -52,6 +52,10 @@ def build(force: bool = False, verbose: bool = True) -> str:
     """Compile every kernel for sm_100a and link the shared library."""
     os.makedirs(OBJ, exist_ok=True)
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    # A/B experiments: SK_SRC_OVERRIDE="prefill.cu=/path/alt.cu,..." swaps sources
+    for pair in filter(None, os.environ.get("SK_SRC_OVERRIDE", "").split(",")):
+        name, alt = pair.split("=")
+        sources = [alt if os.path.basename(x) == name else x for x in sources]
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(lambda s: _compile(s, force), sources))
     newest = max(os.path.getmtime(o) for o in objs)

@@ -15,7 +15,8 @@ SK_OK, SK_EINVAL, SK_ECUDA, SK_EUNSUPPORTED = 0, -1, -2, -3
 SK_F16, SK_BF16, SK_F32 = 0, 1, 2
 SK_KIND_DENSE, SK_KIND_STREAMING = 0, 1
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsparsekv_b200.so")
+LIB_PATH = os.environ.get("SK_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                       "libsparsekv_b200.so")
 
 # every symbol include/sparsekv_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ("sk_version", "sk_last_error", "sk_device_supported", "sk_slot_bytes", "sk_append_pages",

@@ -12,12 +12,12 @@
 // keep their schedules distinct) that share one K/V stream.  Warp roles:
 //   warp 0      TMA producer: both Q tiles once, then K/V 64-key blocks into
 //               a kNS-stage ring (SWIZZLE_128B, mbarrier complete_tx)
-//   warp 1      MMA issuer (one elected thread): S_t,j = Q_t K_j^T (M=128,
-//               N=64, K=D) into double-buffered TMEM and O_t += P_t,j V_j
-//               (M=128, N=D, K=64; V is an MN-major operand), issued as
-//               S_0,j+1 | PV_0,j | S_1,j+1 | PV_1,j so the tensor core always
-//               holds the other tile's work while one tile's softmax runs
-//               (FA4-style ping-pong)
+//   warp 1      MMA issuer (one elected thread), per key block j:
+//                 S_t,j = Q_t K_j^T   (M=128, N=64, K=D) for t = 0, 1 into
+//                 double-buffered TMEM, then O_t += P_t,j-1 V_j-1 (M=128,
+//                 N=D, K=64; V is an MN-major operand), so the tensor core
+//                 always has the other tile's work while one tile's softmax
+//                 runs (FA4-style ping-pong)
 //   warps 2..5  softmax of tile 0, warps 6..9 softmax of tile 1: one thread
 //               per query row reads S from TMEM (tcgen05.ld 32x32b), masks
 //               only blocks that need it, exp2 with the scale folded into
@@ -40,10 +40,6 @@ constexpr int kNS = 3;             // K/V pipeline stages
 constexpr int kPfThreads = 320;    // 10 warps
 constexpr int kItemRows = 256;     // two 128-row tiles
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-#ifndef SK_POLY_FROM
-#define SK_POLY_FROM 64  // off: measured neutral-to-worse on B200 at 25% and 37%
-#endif
-constexpr int kPolyFrom = SK_POLY_FROM;  // elements [kPolyFrom, 64) of a row use exp2_poly2
 constexpr uint32_t kFlagCausal = 1u << 4, kFlagMasks = 1u << 5;
 
 template <int D>
@@ -56,7 +52,6 @@ struct PfSmem {
   uint64_t kv_full[kNS];
   uint64_t kv_empty[kNS];
   uint64_t s_full[2][2];
-  uint64_t s_empty[2][2];
   uint64_t p_full[2][2];
   uint64_t p_empty[2][2];
   uint64_t o_done[2];
@@ -122,27 +117,6 @@ __device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
   return d;
 }
 
-// 2^x for a pair, x <= ~8, on the FMA pipe: Cody-Waite split x = n + f with
-// the 1.5*2^23 rounding trick (n lands in the low mantissa bits), a degree-3
-// minimax polynomial for 2^f on [-1/2, 1/2] (max relative error 7.5e-5, below
-// half an fp16 ulp of P), and n added straight into the exponent field.
-__device__ __forceinline__ float2 exp2_poly2(uint64_t x2) {
-  float2 x = f2_unpack(x2);
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
-  const uint64_t xc = f2_pack(x.x, x.y);
-  const uint64_t magic = f2_pack(12582912.f, 12582912.f);
-  const uint64_t j = f2_add(xc, magic);
-  const uint64_t n = f2_add(j, f2_pack(-12582912.f, -12582912.f));
-  const uint64_t f = f2_fma(n, f2_pack(-1.f, -1.f), xc);
-  uint64_t p = f2_fma(f2_pack(0.055171654f, 0.055171654f), f, f2_pack(0.24261115f, 0.24261115f));
-  p = f2_fma(p, f, f2_pack(0.69326097f, 0.69326097f));
-  p = f2_fma(p, f, f2_pack(0.99992806f, 0.99992806f));
-  const float2 pv = f2_unpack(p), jv = f2_unpack(j);
-  return make_float2(__int_as_float(__float_as_int(pv.x) + (__float_as_int(jv.x) << 23)),
-                     __int_as_float(__float_as_int(pv.y) + (__float_as_int(jv.y) << 23)));
-}
-
 template <typename T, int D>
 __global__ void __launch_bounds__(kPfThreads, 1)
     prefill_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -170,7 +144,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     for (int t = 0; t < 2; ++t) {
       for (int b = 0; b < 2; ++b) {
         mbar_init(&sm.s_full[t][b], 1);
-        mbar_init(&sm.s_empty[t][b], 4);
         mbar_init(&sm.p_full[t][b], 4);
         mbar_init(&sm.p_empty[t][b], 1);
       }
@@ -212,80 +185,46 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     constexpr uint32_t idesc_o = make_idesc_f16(128, D, kBF16, false, true);
     mbar_wait(&sm.q_full, 0);
     tc_fence_after();
-    // Issue order per key block j (FA4 ping-pong): S_0,j+1 | PV_0,j | S_1,j+1 |
-    // PV_1,j.  S runs one block ahead of the softmax that consumes it (its
-    // TMEM buffer is released by s_empty as soon as the softmax has loaded
-    // the scores), so while one tile's softmax works the tensor core always
-    // holds the other tile's S or PV.
-    auto issue_s = [&](int t, int jj) {  // S_t,jj = Q_t K_jj^T
+    auto issue_pv = [&](int jj) {  // O_t += P_t,jj V_jj for both tiles
       const int st = jj % kNS;
-      if (jj >= 2) mbar_wait(&sm.s_empty[t][jj & 1], ((jj >> 1) - 1) & 1);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        mbar_wait(&sm.p_full[t][jj & 1], (jj >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            uint64_t a = make_sdesc_sw128(smem_u32(sm.p[t][jj & 1]) + kk * 32, 16, 1024);
+            uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][1][0]) + kk * 2048, 64 * 128, 1024);
+            mma_f16_ss(tmem + kOCol + t * 128, a, b, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&sm.p_empty[t][jj & 1]);
+          mma_commit(&sm.o_done[t]);
+          if (t == 1) mma_commit(&sm.kv_empty[st]);
+        }
+        __syncwarp();
+      }
+    };
+    for (int j = 0; j < n_blocks; ++j) {
+      const int st = j % kNS;
+      mbar_wait(&sm.kv_full[st], (j / kNS) & 1);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          uint64_t a = make_sdesc_sw128(smem_u32(sm.q[t][kk / 4]) + (kk % 4) * 32, 16, 1024);
-          uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][0][kk / 4]) + (kk % 4) * 32, 16, 1024);
-          mma_f16_ss(tmem + t * 128 + (jj & 1) * 64, a, b, idesc_s, kk > 0);
-        }
-        mma_commit(&sm.s_full[t][jj & 1]);
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int t, int jj) {  // O_t += P_t,jj V_jj
-      const int st = jj % kNS;
-      mbar_wait(&sm.p_full[t][jj & 1], (jj >> 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
+        for (int t = 0; t < 2; ++t) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          uint64_t a = make_sdesc_sw128(smem_u32(sm.p[t][jj & 1]) + kk * 32, 16, 1024);
-          uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][1][0]) + kk * 2048, 64 * 128, 1024);
-          mma_f16_ss(tmem + kOCol + t * 128, a, b, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            uint64_t a = make_sdesc_sw128(smem_u32(sm.q[t][kk / 4]) + (kk % 4) * 32, 16, 1024);
+            uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][0][kk / 4]) + (kk % 4) * 32, 16, 1024);
+            mma_f16_ss(tmem + t * 128 + (j & 1) * 64, a, b, idesc_s, kk > 0);
+          }
+          mma_commit(&sm.s_full[t][j & 1]);
         }
-        mma_commit(&sm.p_empty[t][jj & 1]);
-        mma_commit(&sm.o_done[t]);
-        if (t == 1) mma_commit(&sm.kv_empty[st]);  // last reader of K_jj / V_jj
       }
       __syncwarp();
-    };
-    auto wait_kv = [&](int jj) { mbar_wait(&sm.kv_full[jj % kNS], (jj / kNS) & 1); };
-#ifndef SK_PF_ORDER
-#define SK_PF_ORDER 0
-#endif
-    if (SK_PF_ORDER == 0) {
-      // S_0,j S_1,j | PV_0,j-1 PV_1,j-1
-      for (int j = 0; j < n_blocks; ++j) {
-        wait_kv(j);
-        issue_s(0, j);
-        issue_s(1, j);
-        if (j > 0) {
-          issue_pv(0, j - 1);
-          issue_pv(1, j - 1);
-        }
-      }
-      if (n_blocks > 0) {
-        issue_pv(0, n_blocks - 1);
-        issue_pv(1, n_blocks - 1);
-      }
-    } else {
-      // S_0,j+1 | PV_0,j | S_1,j+1 | PV_1,j
-      if (n_blocks > 0) {
-        wait_kv(0);
-        issue_s(0, 0);
-        issue_s(1, 0);
-      }
-      for (int j = 0; j < n_blocks; ++j) {
-        const bool more = j + 1 < n_blocks;
-        if (more) {
-          wait_kv(j + 1);
-          issue_s(0, j + 1);
-        }
-        issue_pv(0, j);
-        if (more) issue_s(1, j + 1);
-        issue_pv(1, j);
-      }
+      if (j > 0) issue_pv(j - 1);
     }
+    if (n_blocks > 0) issue_pv(n_blocks - 1);
   } else {
     // ------------------------------ softmax -----------------------------------
     const int t = (warp - 2) >> 2;   // tile of this warpgroup
@@ -307,9 +246,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         tmem_ld_x32(trow + s_col + (j & 1) * 64, r);
         tmem_ld_x32(trow + s_col + (j & 1) * 64 + 32, r + 32);
         tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.s_empty[t][j & 1]);  // S buffer free for S_t,j+2
 #pragma unroll
         for (int i = 0; i < 64; ++i) s[i] = __uint_as_float(r[i]);
       }
@@ -371,22 +307,10 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       const uint64_t sl2x2 = f2_pack(sl2, sl2), nsh = f2_pack(-shift, -shift);
       uint64_t rs[4] = {0ull, 0ull, 0ull, 0ull};
       uint32_t pk[32];
-      const bool fast = active && lim >= 63 && !(fl & kFlagMasks);  // every s[i] finite
 #pragma unroll
       for (int i = 0; i < 64; i += 2) {
-        const uint64_t x2 = f2_fma(f2_pack(s[i], s[i + 1]), sl2x2, nsh);
-        float p0, p1;
-        if (kPolyFrom <= i && fast) {
-          // a quarter of the exponentials on the FMA pipe: MUFU.EX2 (16/clk/SM)
-          // would otherwise pace the loop at the tensor core's own rate
-          const float2 pp = exp2_poly2(x2);
-          p0 = pp.x;
-          p1 = pp.y;
-        } else {
-          const float2 e = f2_unpack(x2);
-          p0 = fast_exp2(e.x);
-          p1 = fast_exp2(e.y);
-        }
+        const float2 e = f2_unpack(f2_fma(f2_pack(s[i], s[i + 1]), sl2x2, nsh));
+        const float p0 = fast_exp2(e.x), p1 = fast_exp2(e.y);
         rs[(i / 2) & 3] = f2_add(rs[(i / 2) & 3], f2_pack(p0, p1));
         pk[i / 2] = kBF16 ? pack_bf162(p0, p1) : pack_half2(p0, p1);
       }
@@ -406,7 +330,11 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.p_full[t][j & 1]);
     }
-    // epilogue: O / l -> out
+    // epilogue: O / l -> out.  o_done completes one phase per PV; when the
+    // last S landed only PV_t,n-3 was certainly done, so the barrier may be
+    // two phases behind: wait for phase n-2 first (parity alone cannot tell
+    // phase n-1 from n-3), then for phase n-1.
+    if (n_blocks > 1) mbar_wait(&sm.o_done[t], (n_blocks - 2) & 1);
     if (n_blocks > 0) {
       mbar_wait(&sm.o_done[t], (n_blocks - 1) & 1);
       tc_fence_after();

@@ -1,14 +1,15 @@
 // K2 -- hierarchical page selection (LServe Eq. 2).
 //
 // Replaces score_pages / _stacked_stats / pinned_pages / select_pages
-// (reference selector.py:39-108).  Two kernels:
+// (reference selector.py:39-108) in ONE kernel, grid (page chunks, streams):
 //
-// score_kernel (many CTAs per stream, HBM-bound).  Each warp owns
-//   kPagesPerWarp physical pages; one lane issues a single 1-D bulk copy
-//   (cp.async.bulk, mbarrier completion) of their contiguous (k_min, k_max)
-//   rows into shared memory, so every byte of the selector's 33.6 MB at 128k
-//   is requested in the first few hundred cycles of the CTA.  Each lane then
-//   scores its D/32 channels of every logical page in fp64:
+// Scoring (HBM-bound).  Each warp owns kPagesPerWarp consecutive physical
+//   pages and streams their contiguous (k_min, k_max) rows through a
+//   double-buffered pair of shared-memory slots with 1-D bulk copies
+//   (cp.async.bulk, mbarrier completion): the copy of batch i+1 is in flight
+//   while batch i is scored, so the selector's 33.6 MB at 128k is read at
+//   close to HBM rate by ~1 CTA per SM.  Each lane scores its D/32 channels
+//   of every logical page in fp64:
 //       score(r, j) = sum_c q+_rc * kmax_jc + q-_rc * kmin_jc
 //   (q+ = max(q,0), q- = min(q,0): one of the two products is exactly 0, so
 //   each term equals the reference's max(q*kmax, q*kmin); fp16 products are
@@ -16,17 +17,14 @@
 //   the reference's BLAS centre/radius form bit-for-bit -- SURVEY Appendix
 //   A.4).  A multi-value butterfly reduces all (row, logical page) sums of
 //   the warp at once; the physical-page score is their max over retrieval
-//   rows and logical pages.  Only the stream's retrieval rows are computed
-//   (RMAX = 1, 2 or 4 rows per pass).
+//   rows and logical pages.  Only the stream's retrieval rows are computed.
 //
-// topk_kernel (one 1024-thread CTA per stream).  Radix select of the
-//   (K - |pins|)-th largest score among non-pinned pages on the order-
-//   preserving 64-bit image of the fp64 score, starting at the first byte
-//   where the candidates' keys differ; ties go to the lower page index
+// Top-k (the last CTA of each stream, found with an acq_rel ticket).  Radix
+//   select of the (K - |pins|)-th largest score among non-pinned pages on the
+//   order-preserving 64-bit image of the fp64 score, starting at the first
+//   byte where the candidates' keys differ; ties go to the lower page index
 //   (selector.py:106); union with the pins; ascending compaction by a
 //   block-wide scan over page order.
-#include <cstdlib>
-
 #include "sk_common.cuh"
 #include "sk_sm100.cuh"
 
@@ -35,11 +33,10 @@ namespace {
 
 constexpr int kScoreThreads = 256;
 constexpr int kScoreWarps = kScoreThreads / 32;
-constexpr int kPagesPerWarp = 4;
-constexpr int kPagesPerCta = kScoreWarps * kPagesPerWarp;
-constexpr int kTopkThreads = 1024;
+constexpr int kPagesPerWarp = 4;    // pages per bulk copy (one smem slot)
+constexpr int kBatchesPerWarp = 4;  // slots a warp streams through
+constexpr int kTopkThreads = kScoreThreads;
 constexpr int kTopkWarps = kTopkThreads / 32;
-constexpr int kTopkStage = 8192;  // keys staged in shared memory (64 KB)
 
 __device__ __forceinline__ int pins_of(int n, int* pin) {  // selector.py:75-78
   int c = 0;
@@ -98,42 +95,48 @@ __device__ __forceinline__ void to_f64x4(uint2 w, double* o) {
   o[3] = b.y;
 }
 
-// Score the warp's pages for retrieval rows [rbase, rbase + RMAX) and fold
-// them into best[].  LPC logical pages per butterfly pass (RMAX*LPC <= 16
-// keeps two 256-thread CTAs resident per SM).
-template <typename T, int RMAX, int LPC>
-__device__ __forceinline__ void score_rows(const uint8_t* sbuf, int np, int lp_per, int n_log_rel, int D,
-                                           const T* q, int64_t q_rs, uint32_t rmask, int rbase, int rows,
-                                           double (&best)[kPagesPerWarp]) {
-  constexpr int NV = RMAX * LPC;
-  const int lane = threadIdx.x & 31;
-  const int cpl = D / 32;  // channels per lane: 4 (D=128) or 2 (D=64)
-  double qp[RMAX][4], qm[RMAX][4];
-  {
-    uint32_t mbits = rmask;
-    for (int r = 0; r < rbase; ++r) mbits &= mbits - 1;
+// q+ / q- (fp64) of retrieval rows [rbase, rbase + RMAX) for this lane's channels
+template <typename T, int RMAX>
+__device__ __forceinline__ void load_rows(const T* q, int64_t q_rs, uint32_t rmask, int rbase, int rows, int D,
+                                          double (&qp)[RMAX][4], double (&qm)[RMAX][4]) {
+  const int lane = threadIdx.x & 31, cpl = D / 32;
+  uint32_t mbits = rmask;
+  for (int r = 0; r < rbase; ++r) mbits &= mbits - 1;
 #pragma unroll
-    for (int r = 0; r < RMAX; ++r) {
-      const int g = __ffs(mbits) - 1;
-      const bool ok = rbase + r < rows && g >= 0;
-      if (ok) mbits &= mbits - 1;
-      const T* qr = q + (int64_t)(ok ? g : 0) * q_rs + lane * cpl;
+  for (int r = 0; r < RMAX; ++r) {
+    const int g = __ffs(mbits) - 1;
+    const bool ok = rbase + r < rows && g >= 0;
+    if (ok) mbits &= mbits - 1;
+    const T* qr = q + (int64_t)(ok ? g : 0) * q_rs + lane * cpl;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const double x = (ok && c < cpl) ? (double)DT<T>::to_f(qr[c]) : 0.0;
-        qp[r][c] = x > 0.0 ? x : 0.0;
-        qm[r][c] = x < 0.0 ? x : 0.0;
-      }
+    for (int c = 0; c < 4; ++c) {
+      const double x = (ok && c < cpl) ? (double)DT<T>::to_f(qr[c]) : 0.0;
+      qp[r][c] = x > 0.0 ? x : 0.0;
+      qm[r][c] = x < 0.0 ? x : 0.0;
     }
   }
+}
+
+// Scores of the np pages staged in sbuf (nl_rel valid logical pages) for
+// rows [rbase, rbase + RMAX); lane 0 writes (first row chunk) or max-merges
+// (later chunks) each page's score into out[].  LPC logical pages per
+// butterfly pass (RMAX * LPC <= 16).
+template <typename T, int RMAX, int LPC>
+__device__ __forceinline__ void score_batch(const uint8_t* sbuf, int np, int lp_per, int nl_rel, int D,
+                                            const double (&qp)[RMAX][4], const double (&qm)[RMAX][4], int rbase,
+                                            int rows, double* out) {
+  constexpr int NV = RMAX * LPC;
+  const int lane = threadIdx.x & 31;
+  const int cpl = D / 32;
   const int row_bytes = 2 * D * 2;  // (k_min, k_max) of one logical page
   for (int pi = 0; pi < np; ++pi) {
+    double best = -INFINITY;
     for (int l0 = 0; l0 < lp_per; l0 += LPC) {
       double v[NV];
 #pragma unroll
       for (int jj = 0; jj < LPC; ++jj) {
         const int lrel = pi * lp_per + l0 + jj;
-        const T* st = reinterpret_cast<const T*>(sbuf + (int64_t)min(lrel, n_log_rel - 1) * row_bytes);
+        const T* st = reinterpret_cast<const T*>(sbuf + (int64_t)min(lrel, nl_rel - 1) * row_bytes);
         uint2 wmin, wmax;
         if (cpl == 4) {
           wmin = *reinterpret_cast<const uint2*>(st + lane * 4);
@@ -159,23 +162,41 @@ __device__ __forceinline__ void score_rows(const uint8_t* sbuf, int np, int lp_p
       Butterfly<NV, 16>::run(v, lane);
       const int idx = lane >> (6 - __ffs(NV));  // value index owned by this lane
       const int r = idx / LPC, jj = idx % LPC;
-      const bool valid = rbase + r < rows && l0 + jj < lp_per && pi * lp_per + l0 + jj < n_log_rel;
+      const bool valid = rbase + r < rows && l0 + jj < lp_per && pi * lp_per + l0 + jj < nl_rel;
       double mine = valid ? v[0] : -INFINITY;
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) mine = fmax(mine, __shfl_xor_sync(0xffffffffu, mine, off));
-      best[pi] = fmax(best[pi], mine);
+      best = fmax(best, mine);
     }
+    if (lane == 0) out[pi] = rbase == 0 ? best : fmax(out[pi], best);
   }
 }
 
+template <typename T, int RMAX, int LPC>
+__device__ __forceinline__ void score_rows(const uint8_t* sbuf, int np, int lp_per, int nl_rel, int D,
+                                           const T* q, int64_t q_rs, uint32_t rmask, int rows, double* out) {
+  for (int rb = 0; rb < rows; rb += RMAX) {
+    double qp[RMAX][4], qm[RMAX][4];
+    load_rows<T, RMAX>(q, q_rs, rmask, rb, rows, D, qp, qm);
+    score_batch<T, RMAX, LPC>(sbuf, np, lp_per, nl_rel, D, qp, qm, rb, rows, out);
+  }
+}
+
+__device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, int stage_cap, int32_t* sel_out,
+                         int32_t* sel_count);
+
 template <typename T, int LPC>
-__global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(PoolView pv, const T* __restrict__ q, int64_t q_ss,
-                                                              int64_t q_rs, const uint32_t* __restrict__ row_mask,
-                                                              const int32_t* __restrict__ tokens,
-                                                              const uint8_t* __restrict__ invoke, int K,
-                                                              double* ws_scores, int ws_pages) {
+__global__ void __launch_bounds__(kScoreThreads, 1) select_kernel(PoolView pv, const T* __restrict__ q, int64_t q_ss,
+                                                               int64_t q_rs, const uint32_t* __restrict__ row_mask,
+                                                               const int32_t* __restrict__ tokens,
+                                                               const uint8_t* __restrict__ invoke, int K,
+                                                               double* ws_scores, uint32_t* ws_ticket,
+                                                               int ws_pages, int pps, int32_t* sel_out_all,
+                                                               int32_t* sel_count_all, int sel_stride,
+                                                               int smem_bytes) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bar[kScoreWarps];
+  __shared__ uint64_t bar[kScoreWarps][2];
+  __shared__ uint32_t is_last;
   const int s = blockIdx.y;
   if (invoke != nullptr && invoke[s] == 0) return;
   const uint32_t rmask = row_mask[s];
@@ -184,48 +205,74 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(PoolView pv, co
   const int P = pv.P, L = pv.L, D = pv.D, LP = P / L;
   const int n_pages = (n_tok + P - 1) / P;
   const int n_log = (n_tok + L - 1) / L;
+  int32_t* sel_out = sel_out_all + (int64_t)s * sel_stride;
+  double* scores = ws_scores + (int64_t)s * ws_pages;
   int pin[3];
-  if (K >= n_pages || K <= pins_of(n_pages, pin)) return;  // trivial selection, no scores needed
+  const int npins = pins_of(n_pages, pin);
+  if (K >= n_pages || K <= npins) {  // selector.py:98-103: no scoring
+    if (blockIdx.x == 0) {
+      if (K >= n_pages) {
+        for (int i = threadIdx.x; i < n_pages; i += blockDim.x) sel_out[i] = i;
+      } else if (threadIdx.x == 0) {
+        for (int i = 0; i < npins; ++i) sel_out[i] = pin[i];
+      }
+      if (threadIdx.x == 0) sel_count_all[s] = K >= n_pages ? n_pages : npins;
+    }
+    return;
+  }
+  // ---- scoring: the warp streams kBatchesPerWarp batches of pps pages -------
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p0 = (blockIdx.x * kScoreWarps + warp) * kPagesPerWarp;
-  if (p0 >= n_pages) return;  // warp-level exit: nothing below synchronises the CTA
-  const int np = min(kPagesPerWarp, n_pages - p0);
-  const int lg0 = p0 * LP;
-  const int nl = min(np * LP, n_log - lg0);  // valid logical pages of this warp
   const uint32_t row_bytes = 2 * D * 2;
-  uint8_t* sbuf = smem + (size_t)warp * kPagesPerWarp * LP * row_bytes;
+  const uint32_t slot = (uint32_t)pps * LP * row_bytes;
+  const int wp0 = (blockIdx.x * kScoreWarps + warp) * pps * kBatchesPerWarp;  // warp's first page
+  const int nb = max(0, min(kBatchesPerWarp, (n_pages - wp0 + pps - 1) / pps));
+  uint8_t* wbuf = smem + (size_t)warp * 2 * slot;
+  auto issue = [&](int b) {  // lane 0: bulk copy of batch b into slot b&1
+    const int p0 = wp0 + b * pps;
+    const int nl = min(min(pps, n_pages - p0) * LP, n_log - p0 * LP);
+    mbar_arrive_expect_tx(&bar[warp][b & 1], nl * row_bytes);
+    bulk_g2s(wbuf + (b & 1) * slot, pv.stats_ptr(s, p0 * LP), nl * row_bytes, &bar[warp][b & 1]);
+  };
   if (lane == 0) {
-    mbar_init(&bar[warp], 1);
+    mbar_init(&bar[warp][0], 1);
+    mbar_init(&bar[warp][1], 1);
     fence_barrier_init();
-    mbar_arrive_expect_tx(&bar[warp], nl * row_bytes);
-    bulk_g2s(sbuf, pv.stats_ptr(s, lg0), nl * row_bytes, &bar[warp]);
+    if (nb > 0) issue(0);
+    if (nb > 1) issue(1);
   }
   __syncwarp();
   const T* qs = q + s * q_ss;
   const int rows = __popc(rmask);
-  double best[kPagesPerWarp];
-#pragma unroll
-  for (int i = 0; i < kPagesPerWarp; ++i) best[i] = -INFINITY;
-  mbar_wait(&bar[warp], 0);
-  if (rows == 1) {
-    score_rows<T, 1, (LPC < 16 ? LPC : 16)>(sbuf, np, LP, nl, D, qs, q_rs, rmask, 0, rows, best);
-  } else if (rows == 2) {
-    score_rows<T, 2, (LPC < 8 ? LPC : 8)>(sbuf, np, LP, nl, D, qs, q_rs, rmask, 0, rows, best);
-  } else {
-    for (int rb = 0; rb < rows; rb += 4)
-      score_rows<T, 4, (LPC < 4 ? LPC : 4)>(sbuf, np, LP, nl, D, qs, q_rs, rmask, rb, rows, best);
+  for (int b = 0; b < nb; ++b) {
+    const int p0 = wp0 + b * pps;
+    const int np = min(pps, n_pages - p0);
+    const int nl = min(np * LP, n_log - p0 * LP);
+    mbar_wait(&bar[warp][b & 1], (b >> 1) & 1);
+    const uint8_t* sb = wbuf + (b & 1) * slot;
+    if (rows == 1) score_rows<T, 1, (LPC < 16 ? LPC : 16)>(sb, np, LP, nl, D, qs, q_rs, rmask, rows, scores + p0);
+    else if (rows == 2) score_rows<T, 2, (LPC < 8 ? LPC : 8)>(sb, np, LP, nl, D, qs, q_rs, rmask, rows, scores + p0);
+    else score_rows<T, 4, (LPC < 4 ? LPC : 4)>(sb, np, LP, nl, D, qs, q_rs, rmask, rows, scores + p0);
+    __syncwarp();  // every lane is done with the slot before it is refilled
+    if (lane == 0 && b + 2 < nb) issue(b + 2);
   }
-  if (lane < np) {
-    double b = best[0];
-#pragma unroll
-    for (int i = 1; i < kPagesPerWarp; ++i)
-      if (lane == i) b = best[i];
-    ws_scores[(int64_t)s * ws_pages + p0 + lane] = b;
+  // ---- CTA ticket: the stream's last CTA runs the top-k --------------------------
+  // bar.sync orders the CTA's score stores before thread 0's acq_rel fence +
+  // relaxed atomic (the release pattern of CUTLASS's generic barrier)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    const uint32_t t = atomicAdd(ws_ticket + s, 1u);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    is_last = (t == gridDim.x - 1);
+    if (is_last) ws_ticket[s] = 0;  // re-arm for the next invocation
   }
+  __syncthreads();
+  if (!is_last) return;
+  topk_cta(n_pages, K, scores, reinterpret_cast<uint64_t*>(smem), smem_bytes / 8, sel_out, sel_count_all + s);
 }
 
-// Block-wide exclusive scan of one value per thread (1024 threads) in thread
-// order; returns the thread's exclusive prefix and the block total.
+// Block-wide exclusive scan of one value per thread (kTopkThreads threads)
+// in thread order; returns the thread's exclusive prefix and the block total.
 __device__ __forceinline__ uint32_t block_scan(uint32_t x, uint32_t* warp_tot, uint32_t& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t incl = x;
@@ -237,57 +284,35 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t x, uint32_t* warp_tot, u
   if (lane == 31) warp_tot[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    const uint32_t t = warp_tot[lane];
+    const uint32_t t = lane < kTopkWarps ? warp_tot[lane] : 0u;
     uint32_t ti = t;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const uint32_t o = __shfl_up_sync(0xffffffffu, ti, off);
       if (lane >= off) ti += o;
     }
-    warp_tot[lane] = ti - t;  // exclusive warp offsets
-    if (lane == 31) warp_tot[32] = ti;
+    if (lane < kTopkWarps) warp_tot[lane] = ti - t;  // exclusive warp offsets
+    if (lane == kTopkWarps - 1) warp_tot[kTopkWarps] = ti;
   }
   __syncthreads();
   const uint32_t res = warp_tot[warp] + incl - x;
-  total = warp_tot[32];
+  total = warp_tot[kTopkWarps];
   __syncthreads();
   return res;
 }
 
-__global__ void __launch_bounds__(kTopkThreads) topk_kernel(int P, const uint32_t* __restrict__ row_mask,
-                                                            const int32_t* __restrict__ tokens,
-                                                            const uint8_t* __restrict__ invoke, int K,
-                                                            const double* __restrict__ ws_scores, int ws_pages,
-                                                            int32_t* sel_out_all, int32_t* sel_count_all,
-                                                            int sel_stride) {
-  extern __shared__ uint64_t s_keys[];  // min(n, kTopkStage) keys
+// Top-k of one stream by the whole CTA (kTopkThreads threads); the trivial
+// cases (every page / pins only) are handled by the caller.
+__device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, int stage_cap, int32_t* sel_out,
+                         int32_t* sel_count) {
   __shared__ uint32_t hist[256];
   __shared__ uint32_t warp_tot[kTopkWarps + 1];
   __shared__ uint64_t s_max[kTopkWarps], s_min[kTopkWarps];
   __shared__ uint32_t sh_bin, sh_kk, sh_done;
-  const int s = blockIdx.x;
-  if (invoke != nullptr && invoke[s] == 0) return;
-  if (row_mask[s] == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n = (tokens[s] + P - 1) / P;
-  int32_t* sel_out = sel_out_all + (int64_t)s * sel_stride;
-  int32_t* sel_count = sel_count_all + s;
   int pin[3];
   const int npins = pins_of(n, pin);
-  if (K >= n) {  // selector.py:98-100 -- every page, no scoring
-    for (int i = tid; i < n; i += kTopkThreads) sel_out[i] = i;
-    if (tid == 0) *sel_count = n;
-    return;
-  }
-  if (K <= npins) {  // selector.py:101-103 -- pins only
-    if (tid == 0) {
-      for (int i = 0; i < npins; ++i) sel_out[i] = pin[i];
-      *sel_count = npins;
-    }
-    return;
-  }
-  const double* scores = ws_scores + (int64_t)s * ws_pages;
-  const bool staged = n <= kTopkStage;
+  const bool staged = n <= stage_cap;
   auto key_at = [&](int i) -> uint64_t {
     if (staged) return s_keys[i];
     return is_pin(i, n) ? 0ull : order_key(__ldcg(scores + i));
@@ -417,39 +442,34 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(int P, const uint32_
 template <typename T>
 int select_dispatch(const PoolView& pv, int n_streams, const void* q, int64_t q_ss, int64_t q_rs,
                     const uint32_t* row_mask, const int32_t* tokens, const uint8_t* invoke, int K, int max_pages,
-                    int32_t* sel_out, int32_t* sel_count, int sel_stride, double* scores, cudaStream_t st) {
+                    int32_t* sel_out, int32_t* sel_count, int sel_stride, double* scores, uint32_t* ticket,
+                    cudaStream_t st) {
   const int LP = pv.P / pv.L;
-  const size_t smem = (size_t)kPagesPerCta * LP * 2 * pv.D * 2;
+  const int pps = LP >= 16 ? 1 : 16 / LP;  // pages per bulk copy: 16 logical pages (8 KB at D=128)
+  const size_t slot = (size_t)pps * LP * 2 * pv.D * 2;
+  size_t smem = 2 * kScoreWarps * slot;
   if (smem > 200 * 1024) {
     set_error("select: page/logical-page geometry needs too much shared memory");
     return SK_EUNSUPPORTED;
   }
-  dim3 grid((max_pages + kPagesPerCta - 1) / kPagesPerCta, n_streams);
+  const int ppc = kScoreWarps * kBatchesPerWarp * pps;  // pages per CTA
+  dim3 grid((max_pages + ppc - 1) / ppc, n_streams);
   const T* qt = static_cast<const T*>(q);
-  const int dbg = getenv("SK_SEL_DEBUG") ? atoi(getenv("SK_SEL_DEBUG")) : 0;  // temporary timing switch
-  if (dbg != 2) {
-#define SK_SCORE(LPV)                                                                                       \
-  do {                                                                                                      \
-    cudaFuncSetAttribute(score_kernel<T, LPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
-    score_kernel<T, LPV><<<grid, kScoreThreads, smem, st>>>(pv, qt, q_ss, q_rs, row_mask, tokens, invoke, K, \
-                                                            scores, max_pages);                              \
+#define SK_SEL(LPV)                                                                                          \
+  do {                                                                                                       \
+    cudaFuncSetAttribute(select_kernel<T, LPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
+    select_kernel<T, LPV><<<grid, kScoreThreads, smem, st>>>(pv, qt, q_ss, q_rs, row_mask, tokens, invoke, K, \
+                                                             scores, ticket, max_pages, pps, sel_out,         \
+                                                             sel_count, sel_stride, (int)smem);               \
   } while (0)
-  if (LP == 1) SK_SCORE(1);
-  else if (LP == 2) SK_SCORE(2);
-  else if (LP == 4) SK_SCORE(4);
-  else if (LP == 8) SK_SCORE(8);
-  else if (LP == 16) SK_SCORE(16);
-  else SK_SCORE(32);
-#undef SK_SCORE
-  SK_CHECK_LAUNCH("score_kernel");
-  }
-  if (dbg == 1) return SK_OK;
-  const int stage = max_pages < kTopkStage ? max_pages : kTopkStage;
-  const size_t tsmem = (size_t)stage * 8;
-  cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-  topk_kernel<<<n_streams, kTopkThreads, tsmem, st>>>(pv.P, row_mask, tokens, invoke, K, scores, max_pages, sel_out,
-                                                      sel_count, sel_stride);
-  SK_CHECK_LAUNCH("topk_kernel");
+  if (LP == 1) SK_SEL(1);
+  else if (LP == 2) SK_SEL(2);
+  else if (LP == 4) SK_SEL(4);
+  else if (LP == 8) SK_SEL(8);
+  else if (LP == 16) SK_SEL(16);
+  else SK_SEL(32);
+#undef SK_SEL
+  SK_CHECK_LAUNCH("select_kernel");
   return SK_OK;
 }
 
@@ -457,7 +477,7 @@ int select_dispatch(const PoolView& pv, int n_streams, const void* q, int64_t q_
 }  // namespace sk
 
 extern "C" int64_t sk_select_workspace(int32_t n_streams, int32_t max_pages) {
-  return (int64_t)n_streams * max_pages * 8 + 256;
+  return (int64_t)n_streams * max_pages * 8 + (int64_t)n_streams * 4 + 256;  // scores + tickets
 }
 
 extern "C" int sk_select_pages(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
@@ -479,10 +499,12 @@ extern "C" int sk_select_pages(const sk_pool* pool, int32_t n_streams, int32_t g
   SK_CHECK_ARG(reinterpret_cast<uintptr_t>(pool->stats) % 16 == 0, "select: stats must be 16-byte aligned");
   PoolView pv = make_view(*pool);
   double* scores = static_cast<double*>(workspace);
+  uint32_t* ticket = reinterpret_cast<uint32_t*>(scores + (int64_t)n_streams * max_pages_hint);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (pool->dtype == SK_F16)
     return select_dispatch<__half>(pv, n_streams, q, q_stream_stride, q_row_stride, row_mask, tokens, invoke,
-                                   budget_pages, max_pages_hint, sel_out, sel_count, sel_stride, scores, st);
+                                   budget_pages, max_pages_hint, sel_out, sel_count, sel_stride, scores, ticket, st);
   return select_dispatch<__nv_bfloat16>(pv, n_streams, q, q_stream_stride, q_row_stride, row_mask, tokens, invoke,
-                                        budget_pages, max_pages_hint, sel_out, sel_count, sel_stride, scores, st);
+                                        budget_pages, max_pages_hint, sel_out, sel_count, sel_stride, scores, ticket,
+                                        st);
 }
