@@ -25,6 +25,8 @@
 //   byte where the candidates' keys differ; ties go to the lower page index
 //   (selector.py:106); union with the pins; ascending compaction by a
 //   block-wide scan over page order.
+#include <cstdlib>
+
 #include "sk_common.cuh"
 #include "sk_sm100.cuh"
 
@@ -33,7 +35,6 @@ namespace {
 
 constexpr int kScoreThreads = 256;
 constexpr int kScoreWarps = kScoreThreads / 32;
-constexpr int kPagesPerWarp = 4;    // pages per bulk copy (one smem slot)
 constexpr int kBatchesPerWarp = 4;  // slots a warp streams through
 constexpr int kTopkThreads = kScoreThreads;
 constexpr int kTopkWarps = kTopkThreads / 32;
@@ -172,12 +173,72 @@ __device__ __forceinline__ void score_batch(const uint8_t* sbuf, int np, int lp_
   }
 }
 
+// Grouped form for LP = P/L logical pages per physical page with RMAX * LP
+// dividing 32: PG = 32 / (RMAX * LP) physical pages share one butterfly, so
+// the dependent shuffle chain (5 butterfly levels + log2(32/PG) max levels)
+// is paid once per PG pages instead of once per page.
+template <typename T, int RMAX, int LP>
+__device__ __forceinline__ void score_batch_grouped(const uint8_t* sbuf, int np, int nl_rel, int D,
+                                                    const double (&qp)[RMAX][4], const double (&qm)[RMAX][4],
+                                                    int rbase, int rows, double* out) {
+  constexpr int PG = 32 / (RMAX * LP);
+  constexpr int NV = 32;
+  const int lane = threadIdx.x & 31;
+  const int cpl = D / 32;
+  const int row_bytes = 2 * D * 2;
+  for (int g0 = 0; g0 < np; g0 += PG) {
+    double v[NV];
+#pragma unroll
+    for (int pg = 0; pg < PG; ++pg) {
+#pragma unroll
+      for (int lp = 0; lp < LP; ++lp) {
+        const int lrel = (g0 + pg) * LP + lp;
+        const T* st = reinterpret_cast<const T*>(sbuf + (int64_t)min(lrel, nl_rel - 1) * row_bytes);
+        uint2 wmin, wmax;
+        if (cpl == 4) {
+          wmin = *reinterpret_cast<const uint2*>(st + lane * 4);
+          wmax = *reinterpret_cast<const uint2*>(st + D + lane * 4);
+        } else {
+          wmin = make_uint2(*reinterpret_cast<const uint32_t*>(st + lane * 2), 0u);
+          wmax = make_uint2(*reinterpret_cast<const uint32_t*>(st + D + lane * 2), 0u);
+        }
+        double kmin[4], kmax[4];
+        to_f64x4<T>(wmin, kmin);
+        to_f64x4<T>(wmax, kmax);
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) {
+          double acc = 0.0;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            acc = fma(qp[r][c], kmax[c], acc);
+            acc = fma(qm[r][c], kmin[c], acc);
+          }
+          v[(pg * RMAX + r) * LP + lp] = acc;
+        }
+      }
+    }
+    Butterfly<NV, 16>::run(v, lane);  // lane l now holds value l
+    const int pg = lane / (RMAX * LP), r = (lane / LP) % RMAX, lp = lane % LP;
+    const bool valid = rbase + r < rows && g0 + pg < np && (g0 + pg) * LP + lp < nl_rel;
+    double mine = valid ? v[0] : -INFINITY;
+#pragma unroll
+    for (int off = 1; off < RMAX * LP; off <<= 1) mine = fmax(mine, __shfl_xor_sync(0xffffffffu, mine, off));
+    if (lane % (RMAX * LP) == 0 && g0 + pg < np) out[g0 + pg] = rbase == 0 ? mine : fmax(out[g0 + pg], mine);
+  }
+}
+
 template <typename T, int RMAX, int LPC>
 __device__ __forceinline__ void score_rows(const uint8_t* sbuf, int np, int lp_per, int nl_rel, int D,
                                            const T* q, int64_t q_rs, uint32_t rmask, int rows, double* out) {
   for (int rb = 0; rb < rows; rb += RMAX) {
     double qp[RMAX][4], qm[RMAX][4];
     load_rows<T, RMAX>(q, q_rs, rmask, rb, rows, D, qp, qm);
+    if constexpr (LPC * RMAX <= 32 && 32 % (LPC * RMAX) == 0 && 32 / (LPC * RMAX) > 1) {
+      if (lp_per == LPC) {
+        score_batch_grouped<T, RMAX, LPC>(sbuf, np, nl_rel, D, qp, qm, rb, rows, out);
+        continue;
+      }
+    }
     score_batch<T, RMAX, LPC>(sbuf, np, lp_per, nl_rel, D, qp, qm, rb, rows, out);
   }
 }
@@ -186,14 +247,20 @@ __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, i
                          int32_t* sel_count);
 
 template <typename T, int LPC>
-__global__ void __launch_bounds__(kScoreThreads, 1) select_kernel(PoolView pv, const T* __restrict__ q, int64_t q_ss,
+#ifndef SK_SEL_MINB
+#define SK_SEL_MINB 1
+#endif
+#ifndef SK_SEL_LOG_PER_SLOT
+#define SK_SEL_LOG_PER_SLOT 16
+#endif
+__global__ void __launch_bounds__(kScoreThreads, SK_SEL_MINB) select_kernel(PoolView pv, const T* __restrict__ q, int64_t q_ss,
                                                                int64_t q_rs, const uint32_t* __restrict__ row_mask,
                                                                const int32_t* __restrict__ tokens,
                                                                const uint8_t* __restrict__ invoke, int K,
                                                                double* ws_scores, uint32_t* ws_ticket,
                                                                int ws_pages, int pps, int32_t* sel_out_all,
                                                                int32_t* sel_count_all, int sel_stride,
-                                                               int smem_bytes) {
+                                                               int smem_bytes, int dbg) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar[kScoreWarps][2];
   __shared__ uint32_t is_last;
@@ -225,7 +292,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) select_kernel(PoolView pv, c
   const uint32_t row_bytes = 2 * D * 2;
   const uint32_t slot = (uint32_t)pps * LP * row_bytes;
   const int wp0 = (blockIdx.x * kScoreWarps + warp) * pps * kBatchesPerWarp;  // warp's first page
-  const int nb = max(0, min(kBatchesPerWarp, (n_pages - wp0 + pps - 1) / pps));
+  const int nb = dbg == 1 ? 0 : max(0, min(kBatchesPerWarp, (n_pages - wp0 + pps - 1) / pps));
   uint8_t* wbuf = smem + (size_t)warp * 2 * slot;
   auto issue = [&](int b) {  // lane 0: bulk copy of batch b into slot b&1
     const int p0 = wp0 + b * pps;
@@ -267,7 +334,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) select_kernel(PoolView pv, c
     if (is_last) ws_ticket[s] = 0;  // re-arm for the next invocation
   }
   __syncthreads();
-  if (!is_last) return;
+  if (!is_last || dbg == 2) return;
   topk_cta(n_pages, K, scores, reinterpret_cast<uint64_t*>(smem), smem_bytes / 8, sel_out, sel_count_all + s);
 }
 
@@ -306,6 +373,7 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t x, uint32_t* warp_tot, u
 __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, int stage_cap, int32_t* sel_out,
                          int32_t* sel_count) {
   __shared__ uint32_t hist[256];
+  __shared__ uint32_t whist[kTopkWarps * 256];
   __shared__ uint32_t warp_tot[kTopkWarps + 1];
   __shared__ uint64_t s_max[kTopkWarps], s_min[kTopkWarps];
   __shared__ uint32_t sh_bin, sh_kk, sh_done;
@@ -319,12 +387,24 @@ __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, i
   };
   // keys + the candidates' max/min (to skip the leading bytes they share)
   uint64_t kmax = 0, kmin = ~0ull;
-  for (int i = tid; i < n; i += kTopkThreads) {
-    const uint64_t k = is_pin(i, n) ? 0ull : order_key(__ldcg(scores + i));
-    if (staged) s_keys[i] = k;
-    if (k) {
-      kmax = k > kmax ? k : kmax;
-      kmin = k < kmin ? k : kmin;
+  constexpr int kU = 8;  // loads in flight per thread
+  for (int base = 0; base < n; base += kU * kTopkThreads) {
+    double sc[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = base + u * kTopkThreads + tid;
+      sc[u] = i < n ? __ldcg(scores + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = base + u * kTopkThreads + tid;
+      if (i >= n) continue;
+      const uint64_t k = is_pin(i, n) ? 0ull : order_key(sc[u]);
+      if (staged) s_keys[i] = k;
+      if (k) {
+        kmax = k > kmax ? k : kmax;
+        kmin = k < kmin ? k : kmin;
+      }
     }
   }
 #pragma unroll
@@ -360,23 +440,23 @@ __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, i
     done = false;
     shift = -8;
   }
+  // thread t owns the consecutive indices [t*kpt, t*kpt + kpt): one pass over
+  // its keys per radix digit, and page order is thread order for compaction
+  const int kpt = (n + kTopkThreads - 1) / kTopkThreads;
+  const int i0 = tid * kpt, i1 = min(n, i0 + kpt);
   for (; shift >= 0; shift -= 8) {
-    if (tid < 256) hist[tid] = 0;
+    for (int b = tid; b < kTopkWarps * 256; b += kTopkThreads) whist[b] = 0;
     __syncthreads();
-    for (int base = 0; base < n; base += kTopkThreads) {
-      const int i = base + tid;
-      bool live = false;
-      uint32_t bin = 256u + lane;  // unique dummy bin for idle lanes
-      if (i < n) {
-        const uint64_t key = key_at(i);
-        if (key && (key & mask) == prefix) {
-          live = true;
-          bin = uint32_t(key >> shift) & 255u;
-        }
-      }
-      // warp-aggregated: one shared atomic per distinct bin per warp
-      const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-      if (live && (__ffs(peers) - 1) == lane) atomicAdd(&hist[bin], uint32_t(__popc(peers)));
+    for (int i = i0; i < i1; ++i) {  // per-warp histograms: contention stays inside a warp
+      const uint64_t key = key_at(i);
+      if (key && (key & mask) == prefix) atomicAdd(&whist[warp * 256 + (uint32_t(key >> shift) & 255u)], 1u);
+    }
+    __syncthreads();
+    {
+      uint32_t h = 0;
+#pragma unroll
+      for (int w = 0; w < kTopkWarps; ++w) h += whist[w * 256 + tid];  // kTopkThreads == 256 bins
+      hist[tid] = h;
     }
     __syncthreads();
     if (warp == 0) {
@@ -417,26 +497,37 @@ __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, i
   }
   const bool all_equal_taken = done;  // every key matching the prefix is selected
   const uint32_t take_eq = sh_kk;     // else: this many keys == prefix, lowest index first
-  // ordered compaction in chunks of 1024 consecutive page indices
-  uint32_t eq_seen = 0, out_pos = 0;
-  for (int base = 0; base < n; base += kTopkThreads) {
-    const int i = base + tid;
-    const bool valid = i < n;
-    const bool pinned = valid && is_pin(i, n);
-    const uint64_t key = valid ? key_at(i) : 0ull;
-    const uint64_t km = key & mask;
-    const bool cand = valid && !pinned && key != 0;
-    const bool gt = cand && km > prefix;
-    const bool eq = cand && km == prefix;
-    uint32_t chunk_eq, chunk_take;
-    const uint32_t before = eq_seen + block_scan(eq ? 1u : 0u, warp_tot, chunk_eq);
-    const bool take = pinned || gt || (eq && (all_equal_taken || before < take_eq));
-    const uint32_t pos = out_pos + block_scan(take ? 1u : 0u, warp_tot, chunk_take);
-    if (take) sel_out[pos] = i;
-    eq_seen += chunk_eq;
-    out_pos += chunk_take;
+  // ordered compaction: rank of equal keys, then output positions, by two
+  // block-wide scans over thread (= page) order
+  uint32_t n_eq = 0;
+  for (int i = i0; i < i1; ++i) {
+    const uint64_t key = key_at(i);
+    n_eq += (key && !is_pin(i, n) && (key & mask) == prefix) ? 1u : 0u;
   }
-  if (tid == 0) *sel_count = out_pos;
+  uint32_t tot;
+  uint32_t eq_rank = block_scan(n_eq, warp_tot, tot);
+  uint32_t n_take = 0;
+  for (int i = i0; i < i1; ++i) {
+    const uint64_t key = key_at(i);
+    const bool pinned = is_pin(i, n);
+    const uint64_t km = key & mask;
+    const bool cand = !pinned && key != 0;
+    bool take = pinned || (cand && km > prefix);
+    if (cand && km == prefix) take = take || all_equal_taken || eq_rank++ < take_eq;
+    n_take += take ? 1u : 0u;
+  }
+  uint32_t out_pos = block_scan(n_take, warp_tot, tot);
+  eq_rank -= n_eq;  // replay the same decisions to write them
+  for (int i = i0; i < i1; ++i) {
+    const uint64_t key = key_at(i);
+    const bool pinned = is_pin(i, n);
+    const uint64_t km = key & mask;
+    const bool cand = !pinned && key != 0;
+    bool take = pinned || (cand && km > prefix);
+    if (cand && km == prefix) take = take || all_equal_taken || eq_rank++ < take_eq;
+    if (take) sel_out[out_pos++] = i;
+  }
+  if (tid == kTopkThreads - 1) *sel_count = out_pos;
 }
 
 template <typename T>
@@ -445,7 +536,7 @@ int select_dispatch(const PoolView& pv, int n_streams, const void* q, int64_t q_
                     int32_t* sel_out, int32_t* sel_count, int sel_stride, double* scores, uint32_t* ticket,
                     cudaStream_t st) {
   const int LP = pv.P / pv.L;
-  const int pps = LP >= 16 ? 1 : 16 / LP;  // pages per bulk copy: 16 logical pages (8 KB at D=128)
+  const int pps = LP >= SK_SEL_LOG_PER_SLOT ? 1 : SK_SEL_LOG_PER_SLOT / LP;  // pages per bulk copy
   const size_t slot = (size_t)pps * LP * 2 * pv.D * 2;
   size_t smem = 2 * kScoreWarps * slot;
   if (smem > 200 * 1024) {
@@ -455,12 +546,13 @@ int select_dispatch(const PoolView& pv, int n_streams, const void* q, int64_t q_
   const int ppc = kScoreWarps * kBatchesPerWarp * pps;  // pages per CTA
   dim3 grid((max_pages + ppc - 1) / ppc, n_streams);
   const T* qt = static_cast<const T*>(q);
+  const int dbg = getenv("SK_SEL_DEBUG") ? atoi(getenv("SK_SEL_DEBUG")) : 0;  // temporary timing switch
 #define SK_SEL(LPV)                                                                                          \
   do {                                                                                                       \
     cudaFuncSetAttribute(select_kernel<T, LPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
     select_kernel<T, LPV><<<grid, kScoreThreads, smem, st>>>(pv, qt, q_ss, q_rs, row_mask, tokens, invoke, K, \
                                                              scores, ticket, max_pages, pps, sel_out,         \
-                                                             sel_count, sel_stride, (int)smem);               \
+                                                             sel_count, sel_stride, (int)smem, dbg);          \
   } while (0)
   if (LP == 1) SK_SEL(1);
   else if (LP == 2) SK_SEL(2);
