@@ -67,7 +67,7 @@ struct DecodeParams {
   void* out;
   int64_t out_ss, out_rs;
   int out_dtype;
-  int dbg;  // temporary: phase cut-off for timing experiments (SK_DEC_DEBUG)
+  int dbg;  // ablation switch (SK_DEC_DEBUG): 1 return at entry, 2 after the page union, 3 no pages
 };
 
 // m16n8k16 MMA, fp32 accumulate.

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kScoreThreads, SK_SEL_MINB) select_kernel(Pool
   const uint32_t row_bytes = 2 * D * 2;
   const uint32_t slot = (uint32_t)pps * LP * row_bytes;
   const int wp0 = (blockIdx.x * kScoreWarps + warp) * pps * kBatchesPerWarp;  // warp's first page
-  const int nb = dbg == 1 ? 0 : max(0, min(kBatchesPerWarp, (n_pages - wp0 + pps - 1) / pps));
+  const int nb = (dbg == 1 || dbg == 3) ? 0 : max(0, min(kBatchesPerWarp, (n_pages - wp0 + pps - 1) / pps));
   uint8_t* wbuf = smem + (size_t)warp * 2 * slot;
   auto issue = [&](int b) {  // lane 0: bulk copy of batch b into slot b&1
     const int p0 = wp0 + b * pps;
@@ -304,8 +304,8 @@ __global__ void __launch_bounds__(kScoreThreads, SK_SEL_MINB) select_kernel(Pool
     mbar_init(&bar[warp][0], 1);
     mbar_init(&bar[warp][1], 1);
     fence_barrier_init();
-    if (nb > 0) issue(0);
-    if (nb > 1) issue(1);
+    if (nb > 0 && dbg != 5) issue(0);
+    if (nb > 1 && dbg != 5) issue(1);
   }
   __syncwarp();
   const T* qs = q + s * q_ss;
@@ -314,13 +314,14 @@ __global__ void __launch_bounds__(kScoreThreads, SK_SEL_MINB) select_kernel(Pool
     const int p0 = wp0 + b * pps;
     const int np = min(pps, n_pages - p0);
     const int nl = min(np * LP, n_log - p0 * LP);
-    mbar_wait(&bar[warp][b & 1], (b >> 1) & 1);
+    if (dbg != 5) mbar_wait(&bar[warp][b & 1], (b >> 1) & 1);
     const uint8_t* sb = wbuf + (b & 1) * slot;
-    if (rows == 1) score_rows<T, 1, (LPC < 16 ? LPC : 16)>(sb, np, LP, nl, D, qs, q_rs, rmask, rows, scores + p0);
+    if (dbg == 4) {
+    } else if (rows == 1) score_rows<T, 1, (LPC < 16 ? LPC : 16)>(sb, np, LP, nl, D, qs, q_rs, rmask, rows, scores + p0);
     else if (rows == 2) score_rows<T, 2, (LPC < 8 ? LPC : 8)>(sb, np, LP, nl, D, qs, q_rs, rmask, rows, scores + p0);
     else score_rows<T, 4, (LPC < 4 ? LPC : 4)>(sb, np, LP, nl, D, qs, q_rs, rmask, rows, scores + p0);
     __syncwarp();  // every lane is done with the slot before it is refilled
-    if (lane == 0 && b + 2 < nb) issue(b + 2);
+    if (lane == 0 && b + 2 < nb && dbg != 5) issue(b + 2);
   }
   // ---- CTA ticket: the stream's last CTA runs the top-k --------------------------
   // bar.sync orders the CTA's score stores before thread 0's acq_rel fence +
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(kScoreThreads, SK_SEL_MINB) select_kernel(Pool
     if (is_last) ws_ticket[s] = 0;  // re-arm for the next invocation
   }
   __syncthreads();
-  if (!is_last || dbg == 2) return;
+  if (!is_last || dbg == 2 || dbg == 3) return;
   topk_cta(n_pages, K, scores, reinterpret_cast<uint64_t*>(smem), smem_bytes / 8, sel_out, sel_count_all + s);
 }
 
@@ -546,7 +547,9 @@ int select_dispatch(const PoolView& pv, int n_streams, const void* q, int64_t q_
   const int ppc = kScoreWarps * kBatchesPerWarp * pps;  // pages per CTA
   dim3 grid((max_pages + ppc - 1) / ppc, n_streams);
   const T* qt = static_cast<const T*>(q);
-  const int dbg = getenv("SK_SEL_DEBUG") ? atoi(getenv("SK_SEL_DEBUG")) : 0;  // temporary timing switch
+  // ablation switch for timing the phases (tools/decode_probe.py): 1 no scoring, 2 no top-k,
+  // 3 neither, 4 copies without scoring
+  const int dbg = getenv("SK_SEL_DEBUG") ? atoi(getenv("SK_SEL_DEBUG")) : 0;
 #define SK_SEL(LPV)                                                                                          \
   do {                                                                                                       \
     cudaFuncSetAttribute(select_kernel<T, LPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
