@@ -37,6 +37,17 @@ def balanced_gates(n=H):
     return [0.9 - 0.001 * h if h % 4 < 2 else 0.1 + 0.001 * h for h in range(n)]
 
 
+def ncu_traffic(kernel):
+    """dram read+write bytes per launch of `kernel` from the newest committed
+    ncu --set full capture (profiles/rNN_ncu_traffic.json), else None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic.json")))
+    if not files:
+        return None
+    rec = json.load(open(files[-1]))["kernels"].get(kernel)
+    return None if rec is None else int(rec["dram_read_bytes"] + rec["dram_write_bytes"])
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -314,12 +325,14 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "inputs 1.6 GB/layer > 126 MB L2 (prefill); 256 MB L2 flush between decode steps"},
         "roofline": {"bound": "tensor", "kernel": "prefill_kernel (K4, tcgen05)", "achieved": round(achieved_tf, 1),
                      "peak": tf_peak, "unit": "TFLOP/s", "frac": round(achieved_tf / tf_peak, 4),
-                     "traffic": None, "peak_kind": peak_kind,
+                     "traffic": ncu_traffic("prefill_kernel"), "peak_kind": peak_kind,
                      "flop_per_launch": flop_layer, "launch_ms": round(k4_ms, 3),
                      "flop_def": "ledger visited 64x64 tiles x 4*64*64*D (QK^T + PV)"},
         "decode": {"us_per_step": round(dec_us, 2), "steps": n_dec, "layers": L,
                    "roofline": {"bound": "hbm", "achieved": round(dec_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                                 "frac": round(dec_gbs / hbm_peak, 4), "peak_kind": peak_kind,
+                                "traffic_decode_kernel": ncu_traffic("decode_kernel"),
+                                "traffic_select_kernel": ncu_traffic("select_kernel"),
                                 "bytes_per_step": int(dec_bytes_layer * L),
                                 "bytes_def": "per layer: KV heads x (K+2 pages x 9216 B) + stats (n_logical x 512 B) / reuse"}},
         "e2e": {"value": round(e2e_ms, 3) if e2e_ms else None, "unit": "ms", "h2d_bytes_per_step": h2d,

@@ -45,7 +45,10 @@ namespace {
 
 constexpr int kDecThreads = 256;
 constexpr int kWarps = kDecThreads / 32;
-constexpr int kCl = 8;         // CTAs per stream (cluster size, portable)
+#ifndef SK_DEC_CL
+#define SK_DEC_CL 8
+#endif
+constexpr int kCl = SK_DEC_CL;  // CTAs per stream (cluster size; 8 is portable, 16 needs opt-in)
 constexpr int kMaxRows = 8;    // group rows (query heads per KV head)
 constexpr int kMaxExtra = 64;  // sink + local pages
 constexpr int kMaxSel = 2048;  // selection entries staged in smem
@@ -420,8 +423,7 @@ template <typename T, int KIND, int D, int P>
 __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_constant__ DecodeParams prm) {
   constexpr int QR = D / 4;
   __shared__ int s_sel[kMaxSel];
-  __shared__ int s_extra[kMaxExtra];
-  __shared__ int s_nextra;
+  __shared__ int s_extra[kWarps][kMaxExtra];
   __shared__ float s_m[kWarps][kMaxRows], s_l[kWarps][kMaxRows];
   __shared__ __align__(16) float s_o[kWarps][kMaxRows][D];
   // the CTA's partial, read by cluster rank 0 through DSMEM
@@ -473,27 +475,27 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   const int nsel = rmask ? min(cnt_raw, sel_w) : 0;
   const int sink_end = min(pv.sink, n_pages), local_start = max(n_pages - pv.local, 0);
   __syncthreads();
-  // ---- the stream's page union: selection + sink/local pages it lacks ---------
-  if (warp == 0) {
-    int ne = 0;
-    if (smask) {
-      const int loc0 = max(local_start, sink_end);
-      const int ncand = sink_end + (n_pages - loc0);
-      for (int base = 0; base < ncand; base += 32) {
-        const int ci = base + lane;
-        const int p = ci < sink_end ? ci : loc0 + (ci - sink_end);
-        const bool extra = ci < ncand && !contains(s_sel, nsel, p);
-        const uint32_t bal = __ballot_sync(0xffffffffu, extra);
-        const int pos = ne + __popc(bal & ((1u << lane) - 1u));
-        if (extra && pos < kMaxExtra) s_extra[pos] = p;
-        ne += __popc(bal);
-      }
-      ne = min(ne, kMaxExtra);
+  // ---- the stream's page union: selection + sink/local pages it lacks.  Each
+  //      warp derives it itself (a ballot over <= 32 candidates against the
+  //      staged selection), so no second CTA barrier sits on the critical path.
+  int* w_extra = s_extra[warp];
+  int ne = 0;
+  if (smask) {
+    const int loc0 = max(local_start, sink_end);
+    const int ncand = sink_end + (n_pages - loc0);
+    for (int base = 0; base < ncand; base += 32) {
+      const int ci = base + lane;
+      const int p = ci < sink_end ? ci : loc0 + (ci - sink_end);
+      const bool extra = ci < ncand && !contains(s_sel, nsel, p);
+      const uint32_t bal = __ballot_sync(0xffffffffu, extra);
+      const int pos = ne + __popc(bal & ((1u << lane) - 1u));
+      if (extra && pos < kMaxExtra) w_extra[pos] = p;
+      ne += __popc(bal);
     }
-    if (lane == 0) s_nextra = ne;
+    ne = min(ne, kMaxExtra);
   }
-  __syncthreads();
-  const int U = (prm.dbg == 2 || prm.dbg == 3) ? 0 : nsel + s_nextra;
+  __syncwarp();
+  const int U = (prm.dbg == 2 || prm.dbg == 3) ? 0 : nsel + ne;
   if (prm.dbg == 2) return;
 
   // ---- this warp's pages: unit u = rank + kCl * (warp + kWarps * i) -----------
@@ -516,7 +518,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
       pg = s_sel[u];
       um = rmask | ((smask && (pg < sink_end || pg >= local_start)) ? smask : 0u);
     } else {
-      pg = s_extra[u - nsel];
+      pg = w_extra[u - nsel];
       um = smask;
     }
     const uint8_t* slot = pv.slot_ptr(s, pg);  // round trip 2 (page table)
@@ -615,6 +617,7 @@ int launch_one(const DecodeParams& prm, int n_streams, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (kCl > 8) cudaFuncSetAttribute(decode_kernel<T, KIND, D, P>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, KIND, D, P>, prm);
   if (e != cudaSuccess) {
     set_error(std::string("decode_kernel: ") + cudaGetErrorString(e));
