@@ -310,6 +310,58 @@ def run_ours(args, rank, world, local_rank):
         h2d = L * (qh.numel() + kh.numel() + vh.numel()) * 2
         d2h = L * oh.numel() * 2
 
+    # ---- cfg4: batched decode, B sequences x batch_ctx tokens, all layers -------
+    batched = None
+    if args.batch > 0:
+        from paper_2502_14866_b200.batch import BatchedLayer
+
+        del qs, ks, vs, engines, dg
+        torch.cuda.empty_cache()
+        B, bctx = args.batch, args.batch_ctx
+        blayers = [BatchedLayer(cfg, prof, B, hkv, D, device=dev, capacity_tokens=bctx + dec_steps + 8)
+                   for _ in range(L)]
+        for li, ly in enumerate(blayers):
+            g = torch.Generator(device=dev).manual_seed(5000 + 100 * li + args.seed + 17 * rank)
+            for b in range(B):
+                kb = torch.randn((bctx, hkv, D), generator=g, device=dev, dtype=torch.float16)
+                vb = torch.randn((bctx, hkv, D), generator=g, device=dev, dtype=torch.float16)
+                ly.load_context(b, kb, vb)
+            del kb, vb
+        bdg = DecodeGraph(blayers, dec_steps + 4, D, record_ledger=False)
+        bq = [(torch.randn((L, B * h, D), generator=gq, device=dev, dtype=torch.float16),
+               torch.randn((L, B * hkv, D), generator=gq, device=dev, dtype=torch.float16),
+               torch.randn((L, B * hkv, D), generator=gq, device=dev, dtype=torch.float16)) for _ in range(4)]
+        for i in range(4):
+            bdg.q.copy_(bq[i][0]); bdg.k.copy_(bq[i][1]); bdg.v.copy_(bq[i][2])  # noqa: E702
+            bdg.step()
+        bts = []
+        with Clocks(local_rank) as bclk:
+            for i in range(n_dec):
+                flush.zero_()
+                torch.cuda.synchronize()
+                bdg.q.copy_(bq[i % 4][0]); bdg.k.copy_(bq[i % 4][1]); bdg.v.copy_(bq[i % 4][2])  # noqa: E702
+                a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                bdg.step()
+                b_.record()
+                torch.cuda.synchronize()
+                bts.append(a.elapsed_time(b_))
+        b_us = statistics.mean(bts) * 1e3
+        if world > 1:
+            t = torch.tensor([b_us], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            b_us = float(t.item())
+        bn_pages = -(-(bctx + 4 + n_dec) // PAGE)
+        b_bytes = L * B * hkv * ((k_pages + 2) * slot + (bn_pages * 4 * 2 * D * 2) / REUSE)
+        b_gbs = b_bytes * world / (b_us * 1e-6) / 1e9
+        batched = {"config": f"cfg4: {B} sequences x {bctx} tokens, per-sequence page tables, {L} layers, "
+                             f"KV4, budget {BUDGET}, reuse {REUSE}", "batch": B, "ctx": bctx,
+                   "us_per_step": round(b_us, 2), "steps": n_dec, "clocks": bclk.summary(),
+                   "roofline": {"bound": "hbm", "achieved": round(b_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                                "frac": round(b_gbs / hbm_peak, 4), "peak_kind": peak_kind,
+                                "bytes_per_step": int(b_bytes * world),
+                                "bytes_def": "per layer per sequence: KV heads x (K+2 pages x 9216 B) + stats / reuse"}}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_reference_sample(ctx, L)
@@ -338,6 +390,7 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": round(e2e_ms, 3) if e2e_ms else None, "unit": "ms", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "path": "Engine.prefill(Workload(pinned host tensors)) per layer, output copied back to pinned host"},
+        "decode_batched": batched,
         "gpu_launches": L * 3 + L * (1 if world > 1 else 0),
         "clocks": clk.summary(),
     }
@@ -378,6 +431,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--batch", type=int, default=16, help="cfg4 batched decode sequences (0 = skip)")
+    ap.add_argument("--batch-ctx", type=int, default=65536)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", 0))

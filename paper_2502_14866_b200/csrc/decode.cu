@@ -8,7 +8,8 @@
 // than a microsecond of HBM time, so the kernel is built around the number
 // of dependent memory round trips, not bandwidth):
 //   * one thread-block CLUSTER of kCl CTAs per stream (= one KV head of one
-//     sequence); the stream's page union -- the selection for retrieval
+//     sequence; kCl = 8 for a single sequence, 1 when a batch of sequences
+//     already gives >= 32 streams); the stream's page union -- the selection for retrieval
 //     rows plus the sink/local window for streaming rows, each page carrying
 //     the mask of group rows that attend it -- is dealt round-robin to the
 //     cluster's warps, one whole page per warp;
@@ -45,10 +46,10 @@ namespace {
 
 constexpr int kDecThreads = 256;
 constexpr int kWarps = kDecThreads / 32;
-#ifndef SK_DEC_CL
-#define SK_DEC_CL 8
-#endif
-constexpr int kCl = SK_DEC_CL;  // CTAs per stream (cluster size; 8 is portable, 16 needs opt-in)
+constexpr int kClWide = 8;  // CTAs per stream when few streams must fill the GPU (portable cluster size)
+// With many streams (batched sequences) one CTA per stream already fills the
+// GPU, and a cluster per stream would only multiply the waves.
+constexpr int kManyStreams = 32;
 constexpr int kMaxRows = 8;    // group rows (query heads per KV head)
 constexpr int kMaxExtra = 64;  // sink + local pages
 constexpr int kMaxSel = 2048;  // selection entries staged in smem
@@ -419,7 +420,7 @@ __device__ __forceinline__ void page_attend(const uint8_t* pg, int tok_in_page, 
   }
 }
 
-template <typename T, int KIND, int D, int P>
+template <typename T, int KIND, int D, int P, int kCl>
 __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_constant__ DecodeParams prm) {
   constexpr int QR = D / 4;
   __shared__ int s_sel[kMaxSel];
@@ -511,17 +512,38 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     for (int i = 0; i < 4; ++i) st.o[ct][i] = 0.f;
   const float sl2 = prm.scale_log2;
   const float inv_levels = KIND == 0 ? 1.f : 1.f / float((1 << pv.bits) - 1);
-  for (int u = rank + kCl * warp; u < U; u += kCl * kWarps) {
-    int pg;
-    uint32_t um;
+  constexpr int RBY = KIND == 0 ? 2 * D : (KIND == 1 ? D / 2 : D);
+  constexpr int kSlotUsed = 2 * P * RBY + (KIND == 0 ? 0 : 8 * D);  // bytes of a slot the kernel reads
+  auto unit_page = [&](int u, uint32_t& um) -> int {
     if (u < nsel) {
-      pg = s_sel[u];
+      const int pg = s_sel[u];
       um = rmask | ((smask && (pg < sink_end || pg >= local_start)) ? smask : 0u);
-    } else {
-      pg = w_extra[u - nsel];
-      um = smask;
+      return pg;
     }
-    const uint8_t* slot = pv.slot_ptr(s, pg);  // round trip 2 (page table)
+    um = smask;
+    return w_extra[u - nsel];
+  };
+  // software pipeline across a warp's pages: the next page's table entry is
+  // loaded and its bytes prefetched into L2 while the current page computes
+  int u = rank + kCl * warp;
+  int pg_next = 0;
+  uint32_t um_next = 0;
+  const uint8_t* slot_next = nullptr;
+  if (u < U) {
+    pg_next = unit_page(u, um_next);
+    slot_next = pv.slot_ptr(s, pg_next);  // round trip 2 (page table)
+  }
+  for (; u < U; u += kCl * kWarps) {
+    const int pg = pg_next;
+    const uint32_t um = um_next;
+    const uint8_t* slot = slot_next;
+    const int un = u + kCl * kWarps;
+    if (un < U) {
+      pg_next = unit_page(un, um_next);
+      slot_next = pv.slot_ptr(s, pg_next);
+      for (int off = lane * 128; off < kSlotUsed; off += 32 * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(slot_next + off));
+    }
     page_attend<T, KIND, D, P>(slot, min(P, n_tok - pg * P), um & gmask, qw, sl2, inv_levels, st);
   }
 
@@ -603,28 +625,33 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   cluster.sync();  // keep every CTA's shared memory alive until all remote reads are done
 }
 
-template <typename T, int KIND, int D, int P>
-int launch_one(const DecodeParams& prm, int n_streams, cudaStream_t st) {
+template <typename T, int KIND, int D, int P, int CL>
+int launch_cl(const DecodeParams& prm, int n_streams, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kCl, n_streams, 1);
+  cfg.gridDim = dim3(CL, n_streams, 1);
   cfg.blockDim = dim3(kDecThreads, 1, 1);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCl;
+  attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (kCl > 8) cudaFuncSetAttribute(decode_kernel<T, KIND, D, P>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, KIND, D, P>, prm);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, KIND, D, P, CL>, prm);
   if (e != cudaSuccess) {
     set_error(std::string("decode_kernel: ") + cudaGetErrorString(e));
     return SK_ECUDA;
   }
   SK_CHECK_LAUNCH("decode_kernel");
   return SK_OK;
+}
+
+template <typename T, int KIND, int D, int P>
+int launch_one(const DecodeParams& prm, int n_streams, cudaStream_t st) {
+  return n_streams >= kManyStreams ? launch_cl<T, KIND, D, P, 1>(prm, n_streams, st)
+                                   : launch_cl<T, KIND, D, P, kClWide>(prm, n_streams, st);
 }
 
 template <typename T, int KIND>

@@ -28,6 +28,8 @@ class DecodeGraph:
     def __init__(self, engines: list, max_steps: int, head_dim: int, record_ledger: bool = True):
         if not engines:
             raise ValueError("need at least one engine")
+        if record_ledger and any(not hasattr(e, "_plans") for e in engines):
+            raise ValueError("per-head ledgers are recorded for single-sequence Engines only")
         e0 = engines[0]
         self.engines = engines
         self.cfg = e0.config

@@ -1,0 +1,45 @@
+"""Batched decode (BASELINE cfg4 extension): B sequences in one device pool
+per layer, decoded by one CUDA-graph step, must reproduce each sequence's
+own Engine.decode_step (selections -> identical pages -> same outputs)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2502_14866_b200 as sk
+from paper_2502_14866_b200.batch import BatchedLayer
+from paper_2502_14866_b200.decode_graph import DecodeGraph
+
+pytestmark = pytest.mark.gpu
+
+
+def test_batched_graph_matches_per_sequence_engines():
+    rng = np.random.default_rng(31)
+    B, s, h, h_kv, d, L = 3, 2048 + 21, 8, 2, 128, 2
+    gates = [0.9, 0.8, 0.1, 0.2, 0.85, 0.15, 0.12, 0.11]
+    cfg = sk.EngineConfig(quant_bits=4, budget_tokens=512, reuse_interval=3, local_blocks=4)
+    prof = sk.classify_heads(gates, 0.5, 1, 4)
+    hist = [[(rng.standard_normal((s, h_kv, d)).astype(np.float16), rng.standard_normal((s, h_kv, d)).astype(np.float16))
+             for _ in range(B)] for _ in range(L)]
+    layers = [BatchedLayer(cfg, prof, B, h_kv, d, device="cuda:0", capacity_tokens=s + 64) for _ in range(L)]
+    eng = [[sk.Engine(cfg, prof, device="cuda:0") for _ in range(B)] for _ in range(L)]
+    for li in range(L):
+        for b in range(B):
+            k, v = hist[li][b]
+            layers[li].load_context(b, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+            eng[li][b].load_context(k.astype(np.float32), v.astype(np.float32))
+    dg = DecodeGraph(layers, 16, d, record_ledger=False)
+    for t in range(7):
+        q = rng.standard_normal((L, B, h, d)).astype(np.float16)
+        kn = rng.standard_normal((L, B, h_kv, d)).astype(np.float16)
+        vn = rng.standard_normal((L, B, h_kv, d)).astype(np.float16)
+        dg.q.copy_(torch.from_numpy(q.reshape(L, B * h, d)))
+        dg.k.copy_(torch.from_numpy(kn.reshape(L, B * h_kv, d)))
+        dg.v.copy_(torch.from_numpy(vn.reshape(L, B * h_kv, d)))
+        out = dg.step().float().cpu().numpy().reshape(L, B, h, d)
+        for li in range(L):
+            for b in range(B):
+                res = eng[li][b].decode_step(q[li, b].astype(np.float32), kn[li, b].astype(np.float32),
+                                             vn[li, b].astype(np.float32))
+                np.testing.assert_allclose(out[li, b], res.output, atol=2e-3, rtol=0, err_msg=f"step {t} layer {li} seq {b}")
+    assert all(p.tokens_host == [s + 7] * (B * h_kv) for p in (ly.pool for ly in layers))
