@@ -110,9 +110,22 @@ __device__ __forceinline__ float2 unpack2(uint32_t w) {
 }
 
 // nibble word -> fp16x2 register `slot` (exact integers 0..15)
+// (slot is a compile-time constant after unrolling).  Even slots take the
+// low nibble of each 16-bit half: LOP3 into the 1024 + n fp16 pattern, then
+// subtract 1024.  Odd slots take the high nibble in place -- 1024 + 16 n --
+// and one HFMA2 (x/16 - 64) recovers n, so a word costs 1 shift (shared by
+// slots 2 and 3), 4 LOP3 and 4 half2 ops.  Every value is exact in fp16.
 __device__ __forceinline__ uint32_t nib2h(uint32_t w, int slot) {
-  uint32_t x = ((w >> (4 * slot)) & 0x000F000Fu) | 0x64006400u;
-  __half2 h = __hsub2(*reinterpret_cast<__half2*>(&x), __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400)));
+  const uint32_t x = slot >= 2 ? (w >> 8) : w;
+  uint32_t y;
+  if (slot & 1) {
+    y = (x & 0x00F000F0u) | 0x64006400u;
+    __half2 h = __hfma2(*reinterpret_cast<__half2*>(&y), __half2half2(__ushort_as_half(0x2C00)),   // 1/16
+                        __half2half2(__ushort_as_half(0xD400)));                                     // -64
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  y = (x & 0x000F000Fu) | 0x64006400u;
+  __half2 h = __hsub2(*reinterpret_cast<__half2*>(&y), __half2half2(__ushort_as_half(0x6400)));   // -1024
   return *reinterpret_cast<uint32_t*>(&h);
 }
 // byte pair (r2 = 0: bytes 0,1; r2 = 1: bytes 2,3) -> fp16x2 exact integers 0..255
