@@ -8,8 +8,8 @@
 // than a microsecond of HBM time, so the kernel is built around the number
 // of dependent memory round trips, not bandwidth):
 //   * one thread-block CLUSTER of kCl CTAs per stream (= one KV head of one
-//     sequence; kCl = 8 for a single sequence, 1 when a batch of sequences
-//     already gives >= 32 streams); the stream's page union -- the selection for retrieval
+//     sequence; kCl = 8 for a single sequence, down to 1 as batched
+//     sequences add streams -- cluster_for); the stream's page union -- the selection for retrieval
 //     rows plus the sink/local window for streaming rows, each page carrying
 //     the mask of group rows that attend it -- is dealt round-robin to the
 //     cluster's warps, one whole page per warp;
@@ -46,10 +46,16 @@ namespace {
 
 constexpr int kDecThreads = 256;
 constexpr int kWarps = kDecThreads / 32;
-constexpr int kClWide = 8;  // CTAs per stream when few streams must fill the GPU (portable cluster size)
-// With many streams (batched sequences) one CTA per stream already fills the
-// GPU, and a cluster per stream would only multiply the waves.
-constexpr int kManyStreams = 32;
+// CTAs per stream: a cluster of up to 8 (the portable maximum) when few
+// streams must fill the 148 SMs; fewer as the stream count grows, down to one
+// CTA per stream once the streams alone fill the GPU (a bigger cluster would
+// only multiply the waves: one CTA per SM at 255 registers).
+inline int cluster_for(int n_streams) {
+  if (n_streams <= 18) return 8;
+  if (n_streams <= 37) return 4;
+  if (n_streams <= 74) return 2;
+  return 1;
+}
 constexpr int kMaxRows = 8;    // group rows (query heads per KV head)
 constexpr int kMaxExtra = 64;  // sink + local pages
 constexpr int kMaxSel = 2048;  // selection entries staged in smem
@@ -608,8 +614,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   // ---- cluster merge: CTA `rank` finishes channels [rank*D/kCl, +D/kCl) of
   //      every row from the kCl partials (DSMEM) + the new token ----------------
   constexpr int CPC = D / kCl;  // channels per CTA
-  if (tid < G * CPC) {
-    const int rr = tid / CPC, c = rank * CPC + tid % CPC;
+  for (int i = tid; i < G * CPC; i += kDecThreads) {
+    const int rr = i / CPC, c = rank * CPC + i % CPC;
     float pm[kCl], pl[kCl], po[kCl];
 #pragma unroll
     for (int cr = 0; cr < kCl; ++cr) {  // independent remote loads, issued together
@@ -663,8 +669,12 @@ int launch_cl(const DecodeParams& prm, int n_streams, cudaStream_t st) {
 
 template <typename T, int KIND, int D, int P>
 int launch_one(const DecodeParams& prm, int n_streams, cudaStream_t st) {
-  return n_streams >= kManyStreams ? launch_cl<T, KIND, D, P, 1>(prm, n_streams, st)
-                                   : launch_cl<T, KIND, D, P, kClWide>(prm, n_streams, st);
+  switch (cluster_for(n_streams)) {
+    case 8: return launch_cl<T, KIND, D, P, 8>(prm, n_streams, st);
+    case 4: return launch_cl<T, KIND, D, P, 4>(prm, n_streams, st);
+    case 2: return launch_cl<T, KIND, D, P, 2>(prm, n_streams, st);
+    default: return launch_cl<T, KIND, D, P, 1>(prm, n_streams, st);
+  }
 }
 
 template <typename T, int KIND>

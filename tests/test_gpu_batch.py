@@ -43,3 +43,36 @@ def test_batched_graph_matches_per_sequence_engines():
                                              vn[li, b].astype(np.float32))
                 np.testing.assert_allclose(out[li, b], res.output, atol=2e-3, rtol=0, err_msg=f"step {t} layer {li} seq {b}")
     assert all(p.tokens_host == [s + 7] * (B * h_kv) for p in (ly.pool for ly in layers))
+
+
+@pytest.mark.parametrize("batch,h,h_kv", [(40, 8, 1), (12, 32, 8), (5, 8, 2)])
+def test_batched_eager_matches_engines_all_cluster_sizes(batch, h, h_kv):
+    """40 / 96 / 10 streams exercise the 1-, 2- and 8-CTA decode layouts
+    (cluster_for in decode.cu): each sequence's output must match its own
+    Engine.  Covers every output row and channel of the cluster merge."""
+    rng = np.random.default_rng(batch)
+    s, d = 1200 + batch, 128
+    gates = rng.uniform(0, 1, h).tolist()
+    cfg = sk.EngineConfig(quant_bits=4, budget_tokens=256, reuse_interval=2, local_blocks=2)
+    prof = sk.classify_heads(gates, 0.5, 1, 2)
+    layer = BatchedLayer(cfg, prof, batch, h_kv, d, device="cuda:0", capacity_tokens=s + 32)
+    engs = []
+    for b in range(batch):
+        k = rng.standard_normal((s, h_kv, d)).astype(np.float16)
+        v = rng.standard_normal((s, h_kv, d)).astype(np.float16)
+        layer.load_context(b, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+        e = sk.Engine(cfg, prof, device="cuda:0")
+        e.load_context(k.astype(np.float32), v.astype(np.float32))
+        engs.append(e)
+    dg = DecodeGraph([layer], 8, d, record_ledger=False)
+    for t in range(3):
+        q = rng.standard_normal((batch, h, d)).astype(np.float16)
+        kn = rng.standard_normal((batch, h_kv, d)).astype(np.float16)
+        vn = rng.standard_normal((batch, h_kv, d)).astype(np.float16)
+        dg.q.copy_(torch.from_numpy(q.reshape(1, batch * h, d)))
+        dg.k.copy_(torch.from_numpy(kn.reshape(1, batch * h_kv, d)))
+        dg.v.copy_(torch.from_numpy(vn.reshape(1, batch * h_kv, d)))
+        out = dg.step().float().cpu().numpy().reshape(batch, h, d)
+        for b in range(batch):
+            res = engs[b].decode_step(q[b].astype(np.float32), kn[b].astype(np.float32), vn[b].astype(np.float32))
+            np.testing.assert_allclose(out[b], res.output, atol=2e-3, rtol=0, err_msg=f"step {t} seq {b}")

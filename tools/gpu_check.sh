@@ -1,4 +1,4 @@
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_b.csv python tools/profile_batched.py > /dev/null 2>&1
-python tools/launches.py gpurun_out/launches_b.csv | grep -v "at::"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:select_kernel -c 1 -o gpurun_out/ncu_b_select python tools/profile_batched.py > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:decode_kernel -c 1 -o gpurun_out/ncu_b_decode python tools/profile_batched.py > /dev/null 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 300 python tools/decode_probe.py 2>&1 | grep -E "fuse=0"
+timeout 1200 python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --decode-steps 16 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('prefill', d['value'], 'decode', d['decode']['us_per_step'], 'batched', d['decode_batched']['us_per_step'], d['decode_batched']['roofline']['frac'])"
+SK_SWEEP_OUT=gpurun_out/sweep_r01b.jsonl timeout 1800 python tools/sweep.py 2>&1 | cut -c 1-60,200-400 | tail -12
