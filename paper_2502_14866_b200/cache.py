@@ -200,6 +200,51 @@ class DevicePool:
         for s in range(first_stream, first_stream + n):
             self.tokens_host[s] += m
 
+    # -- snapshot restore ---------------------------------------------------------
+    def restore_pages(self, s: int, pages: list) -> None:
+        """Write reference-shaped PhysicalPages (codes, scale/zero, stats) into
+        stream s: the inverse of snapshot_pages.  Values must be exact in the
+        pool dtype (they are when the snapshot came from a pool of that
+        dtype).  The stream's token count becomes the end of its last page."""
+        if not pages:
+            return
+        n_tok = max(p.page_id * self.P + p.token_count for p in pages)
+        self.reserve(n_tok)
+        np_dt = np.float16 if self.dtype == torch.float16 else None
+        if np_dt is None:
+            raise ValueError("snapshot restore supports fp16 pools")
+        levels = (1 << self.bits) - 1 if self.bits else 1
+        lp = self.P // self.L
+        D, Dp = self.D, self.Dp
+        slots, raws = [], []
+        stats = self.stats[s].view(-1, 2, Dp)
+        for pg in pages:
+            t = pg.token_count
+            pad = lambda a: np.pad(np.asarray(a, np.float64), (0, Dp - D))  # noqa: E731
+            if self.bits:
+                kc = np.pad(np.asarray(pg.k_codes[:t], np.uint8), ((0, 0), (0, Dp - D)))
+                vc = np.pad(np.asarray(pg.v_codes[:t], np.uint8), ((0, 0), (0, Dp - D)))
+                bounds = []
+                for scale, zero, codes in ((pg.k_scale, pg.k_zero, kc), (pg.v_scale, pg.v_zero, vc)):
+                    lo = pad(zero)
+                    const = (pad(scale) == 1.0) & (codes.max(axis=0) == 0)  # hi == lo -> scale forced to 1
+                    hi = np.where(const, lo, lo + pad(scale) * levels)
+                    bounds += [lo.astype(np_dt), hi.astype(np_dt)]
+                raw = layout.encode_slot(kc, vc, *bounds, Dp, self.P, self.bits, np_dt, self.slot_bytes)
+            else:
+                kc = np.pad(np.asarray(pg.k_codes[:t], np.float64), ((0, 0), (0, Dp - D))).astype(np_dt)
+                vc = np.pad(np.asarray(pg.v_codes[:t], np.float64), ((0, 0), (0, Dp - D))).astype(np_dt)
+                raw = layout.encode_slot(kc, vc, None, None, None, None, Dp, self.P, 0, np_dt, self.slot_bytes)
+            slots.append(int(self.page_table_host[s, pg.page_id]))
+            raws.append(raw)
+            for jl, st in enumerate(pg.stats):
+                row = np.stack([pad(st.k_min), pad(st.k_max)]).astype(np_dt)
+                stats[pg.page_id * lp + jl].copy_(torch.from_numpy(row))
+        arena = self.arena.view(-1, self.slot_bytes)
+        arena[torch.as_tensor(slots, device=self.device)] = torch.from_numpy(np.stack(raws)).to(self.device)
+        self.tokens_host[s] = n_tok
+        self.tokens[s] = n_tok
+
     # -- host views -------------------------------------------------------------
     def page_count(self, s: int) -> int:
         t = self.tokens_host[s]
@@ -440,6 +485,38 @@ class TwoWayCache:
             for kv in sorted(pool):
                 for page in pool[kv].live_pages():
                     fp.write(json.dumps(_page_record(pool_name, page)) + "\n")
+
+
+def _load_jsonl(cls, fp: IO[str], *, dtype: torch.dtype = _device.DEFAULT_DTYPE, device=None) -> "TwoWayCache":
+    """cache.py:347-368: rebuild a cache from a dump_jsonl snapshot.  Pages go
+    back into device pools; a head whose last page is partial refuses further
+    appends (its raw staging is gone, cache.py:199-203)."""
+    header = json.loads(fp.readline())
+    recs = [json.loads(line) for line in fp if line.strip()]
+    dense = sorted({r["kv_head"] for r in recs if r["pool"] == "dense"})
+    streaming = sorted({r["kv_head"] for r in recs if r["pool"] == "streaming"})
+    P = header["physical_page"]
+    cap = max([r["page_id"] * P + r["token_count"] for r in recs] or [1])
+    cache = cls(P, header["logical_page"], header["bits"], dense, streaming, dtype=dtype, device=device,
+                capacity_tokens=cap)
+    if not recs:
+        return cache
+    cache.ensure_pool(len(recs[0]["k_scale"]))
+    pool = cache.pool
+    for kv in cache.heads:
+        mine = [r for r in recs if r["kv_head"] == kv]
+        pages = [PhysicalPage(r["page_id"], kv, P, r["token_count"], np.asarray(r["k_codes"]),
+                              np.asarray(r["v_codes"]), np.asarray(r["k_scale"]), np.asarray(r["k_zero"]),
+                              np.asarray(r["v_scale"]), np.asarray(r["v_zero"]),
+                              [PageStats(np.asarray(st["k_min"]), np.asarray(st["k_max"]), st["covered_tokens"])
+                               for st in r["stats"]]) for r in mine]
+        pool.restore_pages(cache.stream_of[kv], pages)
+        hp = cache.pool_of(kv)
+        hp._restored_partial = bool(pages) and max(pages, key=lambda p: p.page_id).token_count < P
+    return cache
+
+
+TwoWayCache.load_jsonl = classmethod(_load_jsonl)
 
 
 def _page_record(pool_name: str, page: PhysicalPage) -> dict:

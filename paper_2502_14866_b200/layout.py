@@ -96,3 +96,36 @@ def decode_slot(raw: np.ndarray, head_dim: int, page: int, bits: int, np_dtype):
     bnd = raw[2 * P * rb:2 * P * rb + 8 * D].view(np_dtype).reshape(4, D)
     kpos, vpos = bound_maps(D)
     return (kc.astype(np.uint8), vc.astype(np.uint8), bnd[0][kpos], bnd[1][kpos], bnd[2][vpos], bnd[3][vpos])
+
+
+def encode_slot(kc, vc, klo, khi, vlo, vhi, head_dim: int, page: int, bits: int, np_dtype, slot_bytes: int):
+    """Inverse of decode_slot: pack one page (codes [t, D] for t <= P tokens,
+    bounds [D] in natural channel order) into the device slot layout."""
+    D, P = head_dim, page
+    rb = code_row_bytes(D, bits)
+    raw = np.zeros(slot_bytes, np.uint8)
+    t = kc.shape[0]
+    k_idx, v_idx, k_sh, v_sh = maps(D, P, bits)
+    if bits == 0:
+        kreg = np.zeros(P * D, np_dtype)
+        vreg = np.zeros(P * D, np_dtype)
+        kreg[k_idx[:t]] = kc
+        vreg[v_idx[:t]] = vc
+        raw[:P * rb] = kreg.view(np.uint8)
+        raw[P * rb:2 * P * rb] = vreg.view(np.uint8)
+        return raw
+    kreg = np.zeros(P * rb, np.uint8)
+    vreg = np.zeros(P * rb, np.uint8)
+    if bits <= 4:
+        np.bitwise_or.at(kreg, k_idx[:t].ravel(), (kc.astype(np.uint8) << k_sh[:t]).ravel().astype(np.uint8))
+        np.bitwise_or.at(vreg, v_idx[:t].ravel(), (vc.astype(np.uint8) << v_sh[:t]).ravel().astype(np.uint8))
+    else:
+        kreg[k_idx[:t]] = kc
+        vreg[v_idx[:t]] = vc
+    raw[:P * rb] = kreg
+    raw[P * rb:2 * P * rb] = vreg
+    kpos, vpos = bound_maps(D)
+    bnd = np.zeros((4, D), np_dtype)
+    bnd[0][kpos], bnd[1][kpos], bnd[2][vpos], bnd[3][vpos] = klo, khi, vlo, vhi
+    raw[2 * P * rb:2 * P * rb + 8 * D] = bnd.view(np.uint8).ravel()
+    return raw
