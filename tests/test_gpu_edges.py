@@ -163,3 +163,50 @@ def test_kv_head_shards_recombine_bitwise():
         np.testing.assert_array_equal(np.concatenate([p.output for p in parts], axis=0), rf.output)
         assert [tuple(tb.positions) for p in parts for tb in p.index_tables] == \
             [tuple(tb.positions) for tb in rf.index_tables]
+
+
+@pytest.mark.parametrize("page,logical,bits", [(32, 16, 4), (128, 32, 4), (128, 16, 8), (32, 8, None)])
+def test_other_page_geometries_against_oracle(page, logical, bits):
+    """Physical pages of 32 / 128 tokens (the K4 plan falls back to explicit
+    per-row masks for 64-row query tiles over non-64 key tiles), logical pages
+    of 8-32 tokens: prefill outputs and ledgers, then decode index tables and
+    outputs against the oracle."""
+    rng = np.random.default_rng(page * 7 + logical)
+    n = s = 520
+    h, h_kv, d = 8, 2, 128
+    gates = gates_for(h, rng)
+    q, k, v = fp16_vals(rng, n, h, d), fp16_vals(rng, s, h_kv, d), fp16_vals(rng, s, h_kv, d)
+    kw = dict(physical_page=page, logical_page=logical, quant_bits=bits, budget_tokens=4 * page, reuse_interval=2,
+              local_blocks=2)
+    eng = sk.Engine(sk.EngineConfig(**kw), sk.classify_heads(gates, 0.5, 1, 2), device="cuda:0")
+    ref = O.OracleEngine(O.Config(**kw), O.assign_roles(gates, 0.5, 1, 2))
+    close(eng.prefill(sk.Workload(q, k, v)), ref.prefill(q, k, v))
+    for t in range(4):
+        qn, kn, vn = fp16_vals(rng, h, d), fp16_vals(rng, h_kv, d), fp16_vals(rng, h_kv, d)
+        res = eng.decode_step(qn, kn, vn)
+        rr = ref.decode_step(qn, kn, vn)
+        assert [tuple(tb.positions) for tb in res.index_tables] == rr.tables, f"step {t}"
+        close(res.output, rr.output)
+    assert eng.ledger.tiles == ref.tally.tiles
+
+
+def test_decode_bf16_pool():
+    rng = np.random.default_rng(77)
+    s, h, h_kv, d = 1500, 8, 2, 128
+    gates = gates_for(h, rng)
+    cfg = sk.EngineConfig(quant_bits=4, budget_tokens=512, reuse_interval=2, local_blocks=2)
+    kt = torch.from_numpy(fp16_vals(rng, s, h_kv, d)).to(torch.bfloat16)
+    vt = torch.from_numpy(fp16_vals(rng, s, h_kv, d)).to(torch.bfloat16)
+    eng = sk.Engine(cfg, sk.classify_heads(gates, 0.5, 1, 2), device="cuda:0", dtype=torch.bfloat16)
+    eng.load_context(kt.cuda(), vt.cuda())
+    ref = O.OracleEngine(O.Config(quant_bits=4, budget_tokens=512, reuse_interval=2, local_blocks=2),
+                         O.assign_roles(gates, 0.5, 1, 2))
+    ref.load_context(kt.float().numpy(), vt.float().numpy())
+    for t in range(4):
+        qn = torch.from_numpy(fp16_vals(rng, h, d)).to(torch.bfloat16)
+        kn = torch.from_numpy(fp16_vals(rng, h_kv, d)).to(torch.bfloat16)
+        vn = torch.from_numpy(fp16_vals(rng, h_kv, d)).to(torch.bfloat16)
+        res = eng.decode_step(qn.cuda(), kn.cuda(), vn.cuda())
+        rr = ref.decode_step(qn.float().numpy(), kn.float().numpy(), vn.float().numpy())
+        assert [tuple(tb.positions) for tb in res.index_tables] == rr.tables, f"step {t}"
+        close(res.output.float().cpu().numpy(), rr.output, atol=3e-2)

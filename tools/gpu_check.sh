@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_snapshot.py -x -q 2>&1 | tail -15
+timeout 900 python -m pytest tests/test_gpu_edges.py -q 2>&1 | tail -25
