@@ -23,9 +23,12 @@
 //     (codes -> exact fp16 integers with one LOP3 + one HSUB2 per two);
 //     group rows sit in the MMA's M dimension, so GQA rows share each load;
 //   * one online-softmax state per (warp, row); warps merge in shared
-//     memory; after one cluster barrier every CTA finishes D/kCl output
-//     channels from the kCl partials (distributed shared memory) plus the
-//     new token's raw K/V.  No global workspace, atomics or grid fences.
+//     memory; every CTA then pushes its partial for each D/kCl-channel
+//     slice into the slice owner's shared-memory inbox (DSMEM stores + one
+//     release-arrive on the owner's mbarrier), and each owner finishes its
+//     slice plus the new token's raw K/V.  No global workspace, atomics or
+//     grid fences, and no blocking cluster barrier (the one split
+//     arrive/wait only orders the inbox initialisation).
 // Round trips on the critical path: {tokens, selection, q} -> page table ->
 // page data -> cluster barrier.
 #include <cooperative_groups.h>
@@ -77,7 +80,7 @@ struct DecodeParams {
   void* out;
   int64_t out_ss, out_rs;
   int out_dtype;
-  int dbg;  // ablation switch (SK_DEC_DEBUG): 1 return at entry, 2 after the page union, 3 no pages
+  int dbg;  // ablation switch (SK_DEC_DEBUG=3: skip the pages, keep every barrier and the merge)
 };
 
 // m16n8k16 MMA, fp32 accumulate.
@@ -447,11 +450,22 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   __shared__ float s_m[kWarps][kMaxRows], s_l[kWarps][kMaxRows];
   __shared__ __align__(16) float s_o[kWarps][kMaxRows][D];
   // the CTA's partial, read by cluster rank 0 through DSMEM
-  __shared__ float c_m[kMaxRows], c_l[kMaxRows];
-  __shared__ __align__(16) float c_o[kMaxRows][D];
-  __shared__ float s_fac[kWarps][kMaxRows], s_self[kMaxRows];
+  // inbox of this CTA's output slice: every cluster CTA pushes its partial
+  // (m, l, O[:, slice]) here through DSMEM, then arrives on inbox_bar
+  constexpr int CPC = D / kCl;  // channels finished per CTA
+  __shared__ float in_m[kCl][kMaxRows], in_l[kCl][kMaxRows];
+  __shared__ __align__(16) float in_o[kCl][kMaxRows][CPC];
+  __shared__ uint64_t inbox_bar;
+  __shared__ float s_fac[kWarps][kMaxRows], s_self[kMaxRows], s_self_m[kMaxRows], s_self_l[kMaxRows];
 
   cg::cluster_group cluster = cg::this_cluster();
+  if (threadIdx.x == 0) {
+    mbar_init(&inbox_bar, kCl);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // split cluster barrier: arrive now, wait right before the first remote
+  // access, so every inbox barrier is initialised without a blocking sync
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   const PoolView& pv = prm.pv;
   const int s = blockIdx.y;
   const int rank = blockIdx.x;  // == cluster rank (the cluster spans grid.x)
@@ -459,7 +473,6 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   const int r = lane >> 2, g = r, j = lane & 3;
   const int G = prm.G;
 
-  if (prm.dbg == 1) return;
   // ---- round trip 1: header, selection, q (all independent) -----------------
   const int n_tok = prm.tokens[s];
   const uint32_t rm_raw = prm.row_mask[s];
@@ -515,8 +528,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     ne = min(ne, kMaxExtra);
   }
   __syncwarp();
-  const int U = (prm.dbg == 2 || prm.dbg == 3) ? 0 : nsel + ne;
-  if (prm.dbg == 2) return;
+  const int U = prm.dbg == 3 ? 0 : nsel + ne;
 
   // ---- this warp's pages: unit u = rank + kCl * (warp + kWarps * i) -----------
   RowState<D> st;
@@ -598,42 +610,58 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
       s_fac[w][tid] = f;
       L = fmaf(f, s_l[w][tid], L);
     }
-    c_m[tid] = M;
-    c_l[tid] = L;
+    s_self_m[tid] = M;
+    s_self_l[tid] = L;
   }
   __syncthreads();
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every inbox is initialised
+  // ---- push this CTA's partial to the owners of each channel slice ------------
+  if (tid < kCl * G) {
+    const int r = tid / G, rr = tid % G;
+    *cluster.map_shared_rank(&in_m[rank][rr], r) = s_self_m[rr];
+    *cluster.map_shared_rank(&in_l[rank][rr], r) = s_self_l[rr];
+  }
   for (int i = tid; i < G * D; i += kDecThreads) {
     const int rr = i / D, c = i % D;
     float O = 0.f;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) O = fmaf(s_fac[w][rr], s_o[w][rr][c], O);
-    c_o[rr][c] = O;
+    *cluster.map_shared_rank(&in_o[rank][rr][c % CPC], c / CPC) = O;
   }
-  cluster.sync();  // every CTA's partial is visible cluster-wide
+  __syncthreads();
+  if (tid < kCl) {  // one release-arrive per owner CTA
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(&inbox_bar)), "r"(tid));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  }
 
-  // ---- cluster merge: CTA `rank` finishes channels [rank*D/kCl, +D/kCl) of
-  //      every row from the kCl partials (DSMEM) + the new token ----------------
-  constexpr int CPC = D / kCl;  // channels per CTA
+  // ---- finish channels [rank*CPC, +CPC) of every row from the inbox + the new
+  //      token (no remote reads, so no closing cluster barrier is needed) ------
+  {
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile(
+          "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], 0;\n\t"
+          "selp.b32 %0, 1, 0, P;\n\t}\n"
+          : "=r"(ok)
+          : "r"(smem_u32(&inbox_bar))
+          : "memory");
+  }
   for (int i = tid; i < G * CPC; i += kDecThreads) {
-    const int rr = i / CPC, c = rank * CPC + i % CPC;
-    float pm[kCl], pl[kCl], po[kCl];
-#pragma unroll
-    for (int cr = 0; cr < kCl; ++cr) {  // independent remote loads, issued together
-      pm[cr] = *cluster.map_shared_rank(&c_m[rr], cr);
-      pl[cr] = *cluster.map_shared_rank(&c_l[rr], cr);
-      po[cr] = *cluster.map_shared_rank(&c_o[rr][c], cr);
-    }
+    const int rr = i / CPC, cc = i % CPC, c = rank * CPC + cc;
     const float s_new = s_self[rr];
     float M = s_new;
 #pragma unroll
-    for (int cr = 0; cr < kCl; ++cr) M = fmaxf(M, pm[cr]);
+    for (int cr = 0; cr < kCl; ++cr) M = fmaxf(M, in_m[cr][rr]);
     const float fs = exp2f(s_new - M);
     float L = fs, O = fs * DT<T>::to_f(reinterpret_cast<const T*>(prm.v_new)[s * prm.new_ss + c]);
 #pragma unroll
     for (int cr = 0; cr < kCl; ++cr) {
-      const float f = pm[cr] == -INFINITY ? 0.f : exp2f(pm[cr] - M);
-      L = fmaf(f, pl[cr], L);
-      O = fmaf(f, po[cr], O);
+      const float pm = in_m[cr][rr];
+      const float f = pm == -INFINITY ? 0.f : exp2f(pm - M);
+      L = fmaf(f, in_l[cr][rr], L);
+      O = fmaf(f, in_o[cr][rr][cc], O);
     }
     O /= L;
     const int64_t oi = s * prm.out_ss + (int64_t)rr * prm.out_rs + c;
@@ -641,7 +669,6 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     else if (prm.out_dtype == SK_F16) reinterpret_cast<__half*>(prm.out)[oi] = __float2half_rn(O);
     else reinterpret_cast<__nv_bfloat16*>(prm.out)[oi] = __float2bfloat16_rn(O);
   }
-  cluster.sync();  // keep every CTA's shared memory alive until all remote reads are done
 }
 
 template <typename T, int KIND, int D, int P, int CL>
