@@ -261,6 +261,7 @@ def run_ours(args, rank, world, local_rank):
         dec_once(i)
     dec_ts = []
     n_dec = (dec_steps // REUSE) * REUSE
+    dec_gather = torch.empty((world,) + tuple(dg.out.shape), dtype=dg.out.dtype, device=dev) if world > 1 else None
     for i in range(n_dec):
         flush.zero_()  # L2 flush between timed steps
         torch.cuda.synchronize()
@@ -268,9 +269,13 @@ def run_ours(args, rank, world, local_rank):
         dg.q.copy_(qn)
         dg.k.copy_(kn)
         dg.v.copy_(vn)
+        if world > 1:
+            dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        dg.step()
+        out_l = dg.step()
+        if world > 1:  # head outputs of every layer gathered over NVLink (one collective per step)
+            dist.all_gather_into_tensor(dec_gather, out_l)
         b.record()
         torch.cuda.synchronize()
         dec_ts.append(a.elapsed_time(b))
@@ -286,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
     # bytes one decode step must read per layer: union of pages per KV head
     # (selection + 2 extra local pages) + stats of every logical page / reuse
     dec_bytes_layer = hkv * ((k_pages + 2) * slot + (n_pages * 4 * 2 * D * 2) / REUSE)
-    dec_gbs = dec_bytes_layer * L / (dec_us * 1e-6) / 1e9
+    dec_gbs = dec_bytes_layer * L * world / (dec_us * 1e-6) / 1e9  # whole job: every rank's KV heads
 
     # ---- e2e through the public API with host (pinned) buffers ----------------
     e2e_ms = None
@@ -307,8 +312,8 @@ def run_ours(args, rank, world, local_rank):
 
         timed(e2e_step, 1)
         e2e_ms = statistics.mean(timed(e2e_step, 1))
-        h2d = L * (qh.numel() + kh.numel() + vh.numel()) * 2
-        d2h = L * oh.numel() * 2
+        h2d = L * (qh.numel() + kh.numel() + vh.numel()) * 2 * world  # whole job: every rank's heads
+        d2h = L * oh.numel() * 2 * world
 
     # ---- cfg4: batched decode, B sequences x batch_ctx tokens, all layers -------
     batched = None
@@ -335,14 +340,19 @@ def run_ours(args, rank, world, local_rank):
             bdg.q.copy_(bq[i][0]); bdg.k.copy_(bq[i][1]); bdg.v.copy_(bq[i][2])  # noqa: E702
             bdg.step()
         bts = []
+        b_gather = torch.empty((world,) + tuple(bdg.out.shape), dtype=bdg.out.dtype, device=dev) if world > 1 else None
         with Clocks(local_rank) as bclk:
             for i in range(n_dec):
                 flush.zero_()
                 torch.cuda.synchronize()
                 bdg.q.copy_(bq[i % 4][0]); bdg.k.copy_(bq[i % 4][1]); bdg.v.copy_(bq[i % 4][2])  # noqa: E702
+                if world > 1:
+                    dist.barrier()
                 a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
-                bdg.step()
+                bout = bdg.step()
+                if world > 1:
+                    dist.all_gather_into_tensor(b_gather, bout)
                 b_.record()
                 torch.cuda.synchronize()
                 bts.append(a.elapsed_time(b_))
@@ -385,7 +395,7 @@ def run_ours(args, rank, world, local_rank):
                                 "frac": round(dec_gbs / hbm_peak, 4), "peak_kind": peak_kind,
                                 "traffic_decode_kernel": ncu_traffic("decode_kernel"),
                                 "traffic_select_kernel": ncu_traffic("select_kernel"),
-                                "bytes_per_step": int(dec_bytes_layer * L),
+                                "bytes_per_step": int(dec_bytes_layer * L * world),
                                 "bytes_def": "per layer: KV heads x (K+2 pages x 9216 B) + stats (n_logical x 512 B) / reuse"}},
         "e2e": {"value": round(e2e_ms, 3) if e2e_ms else None, "unit": "ms", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
