@@ -185,46 +185,76 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     constexpr uint32_t idesc_o = make_idesc_f16(128, D, kBF16, false, true);
     mbar_wait(&sm.q_full, 0);
     tc_fence_after();
-    auto issue_pv = [&](int jj) {  // O_t += P_t,jj V_jj for both tiles
+    auto issue_s = [&](int t, int jj) {  // S_t,jj = Q_t K_jj^T into TMEM buffer jj&1
       const int st = jj % kNS;
+      if (elect_one()) {
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        mbar_wait(&sm.p_full[t][jj & 1], (jj >> 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            uint64_t a = make_sdesc_sw128(smem_u32(sm.p[t][jj & 1]) + kk * 32, 16, 1024);
-            uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][1][0]) + kk * 2048, 64 * 128, 1024);
-            mma_f16_ss(tmem + kOCol + t * 128, a, b, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
-          }
-          mma_commit(&sm.p_empty[t][jj & 1]);
-          mma_commit(&sm.o_done[t]);
-          if (t == 1) mma_commit(&sm.kv_empty[st]);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          uint64_t a = make_sdesc_sw128(smem_u32(sm.q[t][kk / 4]) + (kk % 4) * 32, 16, 1024);
+          uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][0][kk / 4]) + (kk % 4) * 32, 16, 1024);
+          mma_f16_ss(tmem + t * 128 + (jj & 1) * 64, a, b, idesc_s, kk > 0);
         }
-        __syncwarp();
+        mma_commit(&sm.s_full[t][jj & 1]);
       }
+      __syncwarp();
     };
-    for (int j = 0; j < n_blocks; ++j) {
-      const int st = j % kNS;
-      mbar_wait(&sm.kv_full[st], (j / kNS) & 1);
+    auto issue_pv = [&](int t, int jj) {  // O_t += P_t,jj V_jj
+      const int st = jj % kNS;
+      mbar_wait(&sm.p_full[t][jj & 1], (jj >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            uint64_t a = make_sdesc_sw128(smem_u32(sm.q[t][kk / 4]) + (kk % 4) * 32, 16, 1024);
-            uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][0][kk / 4]) + (kk % 4) * 32, 16, 1024);
-            mma_f16_ss(tmem + t * 128 + (j & 1) * 64, a, b, idesc_s, kk > 0);
-          }
-          mma_commit(&sm.s_full[t][j & 1]);
+        for (int kk = 0; kk < 4; ++kk) {
+          uint64_t a = make_sdesc_sw128(smem_u32(sm.p[t][jj & 1]) + kk * 32, 16, 1024);
+          uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][1][0]) + kk * 2048, 64 * 128, 1024);
+          mma_f16_ss(tmem + kOCol + t * 128, a, b, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
         }
+        mma_commit(&sm.p_empty[t][jj & 1]);
+        mma_commit(&sm.o_done[t]);
+        if (t == 1) mma_commit(&sm.kv_empty[st]);
       }
       __syncwarp();
-      if (j > 0) issue_pv(j - 1);
+    };
+    auto wait_kv = [&](int jj) {
+      mbar_wait(&sm.kv_full[jj % kNS], (jj / kNS) & 1);
+      tc_fence_after();
+    };
+    // S_t,j reuses the TMEM buffer of S_t,j-2, whose softmax finished before
+    // PV_t,j-2 could be issued -- and every order below issues PV_t,j-2 first.
+#ifndef SK_PF_ORDER
+#define SK_PF_ORDER 0
+#endif
+    if (SK_PF_ORDER == 0) {  // S_0,j S_1,j | PV_0,j-1 PV_1,j-1
+      for (int j = 0; j < n_blocks; ++j) {
+        wait_kv(j);
+        issue_s(0, j);
+        issue_s(1, j);
+        if (j > 0) {
+          issue_pv(0, j - 1);
+          issue_pv(1, j - 1);
+        }
+      }
+      if (n_blocks > 0) {
+        issue_pv(0, n_blocks - 1);
+        issue_pv(1, n_blocks - 1);
+      }
+    } else {  // S_0,j+1 | PV_0,j | S_1,j+1 | PV_1,j (tile softmaxes staggered)
+      if (n_blocks > 0) {
+        wait_kv(0);
+        issue_s(0, 0);
+        issue_s(1, 0);
+      }
+      for (int j = 0; j < n_blocks; ++j) {
+        const bool more = j + 1 < n_blocks;
+        if (more) {
+          wait_kv(j + 1);
+          issue_s(0, j + 1);
+        }
+        issue_pv(0, j);
+        if (more) issue_s(1, j + 1);
+        issue_pv(1, j);
+      }
     }
-    if (n_blocks > 0) issue_pv(n_blocks - 1);
   } else {
     // ------------------------------ softmax -----------------------------------
     const int t = (warp - 2) >> 2;   // tile of this warpgroup
