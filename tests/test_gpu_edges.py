@@ -210,3 +210,27 @@ def test_decode_bf16_pool():
         rr = ref.decode_step(qn.float().numpy(), kn.float().numpy(), vn.float().numpy())
         assert [tuple(tb.positions) for tb in res.index_tables] == rr.tables, f"step {t}"
         close(res.output.float().cpu().numpy(), rr.output, atol=3e-2)
+
+
+@pytest.mark.parametrize("n,pinned", [(1000, True), (300, False), (2048, True)])
+def test_prefill_host_torch_equals_device_path(n, pinned):
+    """Host torch inputs (pinned or pageable) give exactly the device-input
+    path's output and ledger, and a non-finite host input raises."""
+    rng = np.random.default_rng(n)
+    h, h_kv, d = 8, 2, 128
+    gates = gates_for(h, rng)
+    prof = sk.classify_heads(gates, 0.5, 1, 2)
+    q, k, v = (torch.from_numpy(fp16_vals(rng, *sh)).half() for sh in ((n, h, d), (n, h_kv, d), (n, h_kv, d)))
+    if pinned:
+        q, k, v = q.pin_memory(), k.pin_memory(), v.pin_memory()
+    e_host = sk.Engine(sk.EngineConfig(), prof, device="cuda:0")
+    e_dev = sk.Engine(sk.EngineConfig(), prof, device="cuda:0")
+    out_h = e_host.prefill(sk.Workload(q, k, v))
+    out_d = e_dev.prefill(sk.Workload(q.cuda(), k.cuda(), v.cuda()))
+    torch.testing.assert_close(out_h, out_d, rtol=0, atol=0)
+    assert e_host.ledger.tiles == e_dev.ledger.tiles
+    assert e_host.cache.num_tokens == n
+    q_bad = q.clone()
+    q_bad[n // 3, 1, 5] = float("inf")
+    with pytest.raises(ValueError, match="non-finite"):
+        e_host.prefill(sk.Workload(q_bad, k, v))
