@@ -36,7 +36,11 @@
 namespace sk {
 namespace {
 
-constexpr int kNS = 3;             // K/V pipeline stages
+#ifndef SK_TMEM_P
+#define SK_TMEM_P 1
+#endif
+constexpr bool kTmemP = SK_TMEM_P;   // P stored over its S columns in TMEM (A operand of PV)
+constexpr int kNS = kTmemP ? 5 : 3;  // K/V pipeline stages (the smem P tiles make room for two more)
 constexpr int kPfThreads = 320;    // 10 warps
 constexpr int kItemRows = 256;     // two 128-row tiles
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
@@ -47,7 +51,7 @@ struct PfSmem {
   static constexpr int NC = D / 64;  // 128-byte column chunks
   alignas(1024) uint8_t q[2][NC][128 * 128];
   alignas(1024) uint8_t kv[kNS][2][NC][64 * 128];
-  alignas(1024) uint8_t p[2][2][128 * 128];
+  alignas(kTmemP ? 16 : 1024) uint8_t p[kTmemP ? 1 : 2][kTmemP ? 1 : 2][kTmemP ? 16 : 128 * 128];
   uint64_t q_full;
   uint64_t kv_full[kNS];
   uint64_t kv_empty[kNS];
@@ -115,6 +119,27 @@ __device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
   uint64_t d;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
+}
+
+// A operand in TMEM (P), B in shared memory (V): D[tmem] (+)= A[tmem] * B
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
 }
 
 template <typename T, int D>
@@ -205,9 +230,14 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          uint64_t a = make_sdesc_sw128(smem_u32(sm.p[t][jj & 1]) + kk * 32, 16, 1024);
           uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][1][0]) + kk * 2048, 64 * 128, 1024);
-          mma_f16_ss(tmem + kOCol + t * 128, a, b, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
+          if (kTmemP) {
+            mma_f16_ts(tmem + kOCol + t * 128, tmem + t * 128 + (jj & 1) * 64 + kk * 8, b, idesc_o,
+                       (jj > 0 || kk > 0) ? 1u : 0u);
+          } else {
+            uint64_t a = make_sdesc_sw128(smem_u32(sm.p[kTmemP ? 0 : t][jj & 1]) + kk * 32, 16, 1024);
+            mma_f16_ss(tmem + kOCol + t * 128, a, b, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
+          }
         }
         mma_commit(&sm.p_empty[t][jj & 1]);
         mma_commit(&sm.o_done[t]);
@@ -348,14 +378,21 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         const float2 a = f2_unpack(f2_add(f2_add(rs[0], rs[1]), f2_add(rs[2], rs[3])));
         l_run += a.x + a.y;
       }
-      if (j >= 2) mbar_wait(&sm.p_empty[t][j & 1], ((j >> 1) - 1) & 1);
-      uint8_t* prow = sm.p[t][j & 1] + row * 128;
+      if (kTmemP) {
+        // P over the first 32 columns of this S buffer: S_t,j+2 (the next
+        // writer) is issued after PV_t,j, and tcgen05 MMAs run in order
+        tmem_st_x32(trow + s_col + (j & 1) * 64, pk);
+        tmem_wait_st();
+      } else {
+        if (j >= 2) mbar_wait(&sm.p_empty[t][j & 1], ((j >> 1) - 1) & 1);
+        uint8_t* prow = sm.p[kTmemP ? 0 : t][j & 1] + row * 128;
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        uint4 v = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-        *reinterpret_cast<uint4*>(prow + ((ch ^ (row & 7)) << 4)) = v;
+        for (int ch = 0; ch < 8; ++ch) {
+          uint4 v = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+          *reinterpret_cast<uint4*>(prow + ((ch ^ (row & 7)) << 4)) = v;
+        }
+        fence_proxy_async_smem();
       }
-      fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.p_full[t][j & 1]);
