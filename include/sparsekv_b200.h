@@ -102,6 +102,20 @@ int sk_append_pages(const sk_pool* pool, int32_t n_streams, const void* k_src, c
                     int32_t max_pages_touched, void* stream);
 
 /*
+ * K1b -- pool gather (chunked prefill).  Dequantises the resident pages of
+ * streams [0, n_streams) (first n_tokens tokens, every stream holds that
+ * many) into a token-major history: element (s, t, c) of K / V at
+ * k_out / v_out + t*out_token_stride + s*out_stream_stride + c, in
+ * pool->dtype, value code*scale + lo (PhysicalPage.dequantize,
+ * cache.py:54-56 / :97-102, cast to the attention dtype as engine.py:250-262
+ * does); raw pools (bits 0) are copied.  Evicted pages of streaming streams
+ * are not written.  No reference entry point: the reference has no
+ * continued prefill; this is the device half of Engine.prefill_chunk.
+ */
+int sk_gather_pages(const sk_pool* pool, int32_t n_streams, int32_t n_tokens, void* k_out, void* v_out,
+                    int64_t out_stream_stride, int64_t out_token_stride, void* stream);
+
+/*
  * K2 -- hierarchical page selection (Eq. 2).  Replaces
  * score_pages / select_pages / pinned_pages (selector.py:39-108) and the
  * call site engine.py:237-255.  For every stream with invoke[s] != 0 and a

@@ -569,6 +569,48 @@ class OracleEngine:
             self.pools.head(kv).append(k[:, kv], v[:, kv])
         return out
 
+    def prefill_chunk(self, q, k, v) -> np.ndarray:
+        """Continued prefill (an extension: the reference has no such entry
+        point; it composes the reference's own pieces).  The chunk's queries
+        sit at positions S0..S0+n-1 and attend, under the static schedules of
+        an (n, S0+n) workload (engine.py:152-165), a history made of the
+        cached pages dequantised and cast to the q dtype exactly as the
+        decode path reads them (engine.py:250-262, cache.py:97-102) followed
+        by the chunk's raw K/V; the chunk is then appended (cache.py:189-261).
+        A schedule that reaches an evicted page raises, like the reference's
+        page lookup would."""
+        if self.pools is None or self.pools.num_tokens == 0:
+            return self.prefill(q, k, v)
+        c = self.cfg
+        dt = q.dtype
+        n, h_kv = q.shape[0], k.shape[1]
+        s0 = self.pools.num_tokens
+        s = s0 + n
+        kf = np.zeros((s, h_kv, q.shape[2]), dtype=dt)
+        vf = np.zeros_like(kf)
+        resident = {}
+        for kv in range(h_kv):
+            head = self.pools.head(kv)
+            resident[kv] = set(head.pages)
+            for i, pg in head.pages.items():
+                kk, vv = pg.kv()
+                kf[i * c.physical_page:i * c.physical_page + pg.tokens, kv] = kk.astype(dt)
+                vf[i * c.physical_page:i * c.physical_page + pg.tokens, kv] = vv.astype(dt)
+        kf[s0:] = k.astype(dt)
+        vf[s0:] = v.astype(dt)
+        sched = self.schedules(n, s)
+        g = self.grp
+        for (h, qt), tiles in sched.items():
+            miss = [t for t in tiles if t * c.physical_page < s0 and t not in resident[h // g]]
+            if miss:
+                raise ValueError(f"head {h}, query tile {qt} needs evicted pages {miss}")
+        out, delta = tiled_attention(q, kf, vf, sched, c.tile_q_prefill, c.physical_page, PREFILL)
+        for (st, h), (vis, tot) in delta.tiles.items():
+            self.tally.add(st, h, vis, tot)
+        for kv in range(h_kv):
+            self.pools.head(kv).append(k[:, kv], v[:, kv])
+        return out
+
     def load_context(self, k, v) -> None:
         """engine.py:175-204 -- cache only, no attention."""
         self.grp = len(self.roles) // k.shape[1]

@@ -200,6 +200,25 @@ class DevicePool:
         for s in range(first_stream, first_stream + n):
             self.tokens_host[s] += m
 
+    # -- gather (K1b) ------------------------------------------------------------------
+    def gather(self, extra_tokens: int = 0):
+        """Dequantised history of every stream as device k/v [S0 + extra, Hkv, Dp]
+        in the pool dtype (rows >= S0 left for the caller; evicted pages of
+        streaming streams unwritten).  One K1b launch."""
+        counts = set(self.tokens_host)
+        if len(counts) != 1:
+            raise ValueError(f"pools out of sync: token counts {sorted(counts)}")
+        n0 = counts.pop()
+        shape = (n0 + extra_tokens, self.n_streams, self.Dp)
+        k = torch.empty(shape, dtype=self.dtype, device=self.device)
+        v = torch.empty(shape, dtype=self.dtype, device=self.device)
+        if n0:
+            pool = self.abi()
+            rc = _lib.load().sk_gather_pages(C.byref(pool), self.n_streams, n0, k.data_ptr(), v.data_ptr(), self.Dp,
+                                             self.n_streams * self.Dp, _device.stream_ptr(self.device))
+            _lib.check(rc)
+        return k, v
+
     # -- snapshot restore ---------------------------------------------------------
     def restore_pages(self, s: int, pages: list) -> None:
         """Write reference-shaped PhysicalPages (codes, scale/zero, stats) into

@@ -274,6 +274,56 @@ class Engine:
         self.cache.append_all(k, v)
         return out
 
+    def prefill_chunk(self, w: Workload):
+        """Continued (chunked) prefill -- an extension, the reference has no such
+        entry point.  ``w.q`` [n, H, D] are the chunk's queries at positions
+        S0..S0+n-1 and ``w.k``/``w.v`` [n, Hkv, D] its own keys/values; the
+        chunk attends the cached history (dequantised exactly as the decode
+        path reads it, engine.py:250-262) plus its own raw K/V under the static
+        prefill schedules of an (n, S0+n) workload (engine.py:152-165), then is
+        appended to the cache.  On an empty engine this is ``prefill``."""
+        if self.cache is None or self.cache.pool is None or self.cache.num_tokens == 0:
+            return self.prefill(w)
+        if len(self.profiles) != w.num_heads:
+            raise ValueError(f"{len(self.profiles)} profiles for {w.num_heads} heads")
+        pool = self.cache.pool
+        if w.head_dim != self.cache._user_dim or w.k.shape[1] != pool.n_streams:
+            raise ValueError("chunk shapes do not match the cached history")
+        dp = pool.Dp
+        q = _device.to_device(w.q, self._dtype, self.device, dp)
+        k = _device.to_device(w.k, self._dtype, self.device, dp)
+        v = _device.to_device(w.v, self._dtype, self.device, dp)
+        check_finite_device(w, q, k, v)
+        out = self.prefill_chunk_device(q, k, v, w.head_dim)
+        np_dt = None if _device.is_torch(w.q) else np.asarray(w.q).dtype
+        return _device.to_output(out[..., :w.head_dim], w.q, np_dt)
+
+    def prefill_chunk_device(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, head_dim: int) -> torch.Tensor:
+        """Device fast path of prefill_chunk: q [n,H,Dp], k/v [n,Hkv,Dp] padded, pool dtype."""
+        if self.cache is None or self.cache.pool is None or self.cache.num_tokens == 0:
+            return self.prefill_device(q, k, v, head_dim)
+        cfg = self.config
+        pool = self.cache.pool
+        n, h, dp = q.shape
+        if h != len(self.profiles) or h != self._group_size * pool.n_streams or tuple(k.shape) != (n, pool.n_streams, dp):
+            raise ValueError("chunk shapes do not match the cached history")
+        for p in self.profiles:  # streaming heads may only reach pages their ring keeps
+            if p.role != RETRIEVAL and (p.sink_blocks > cfg.sink_blocks or p.local_blocks > cfg.local_blocks):
+                raise ValueError(f"head {p.head}: window ({p.sink_blocks}, {p.local_blocks}) exceeds the "
+                                 f"streaming pool's ({cfg.sink_blocks}, {cfg.local_blocks}); evicted pages "
+                                 "cannot be attended")
+        s0 = self.cache.num_tokens
+        kh, vh = pool.gather(extra_tokens=n)
+        kh[s0:] = k
+        vh[s0:] = v
+        plan = self._plan(n, s0 + n)
+        out = run_prefill(q, kh, vh, plan, 1.0 / math.sqrt(head_dim))
+        for hh in range(h):
+            self.ledger.record_tiles(PREFILL, hh, int(plan.visited[hh]), int(plan.total[hh]))
+        del kh, vh
+        self.cache.append_all(k, v)
+        return out
+
     def load_context(self, k_history, v_history) -> None:
         """engine.py:175-204: K1 bulk append, no attention."""
         shape_k, shape_v = tuple(np.shape(k_history)), tuple(np.shape(v_history))
