@@ -169,6 +169,18 @@ class DevicePool:
                 mp *= 2
             self._alloc(mp)
 
+    def matches(self, kinds, head_dim: int, page: int, logical: int, bits, sink: int, local: int, dtype) -> bool:
+        """Same streams and layout (a pool that can be recycled for a fresh cache)."""
+        return (list(kinds) == self.kinds and head_dim == self.D and (page, logical) == (self.P, self.L)
+                and (0 if bits is None else int(bits)) == self.bits and (sink, local) == (self.sink, self.local)
+                and dtype == self.dtype)
+
+    def reset(self) -> None:
+        """Empty every stream (device-side; pages past the token counts are
+        never read, and the first append rebuilds page 0 from scratch)."""
+        self.tokens.zero_()
+        self.tokens_host = [0] * self.n_streams
+
     # -- ABI view -------------------------------------------------------------
     def abi(self, first_stream: int = 0) -> _lib.SkPool:
         s = first_stream
@@ -457,13 +469,27 @@ class TwoWayCache:
 
     def ensure_pool(self, head_dim: int) -> DevicePool:
         if self.pool is None:
-            kinds = [_lib.SK_KIND_DENSE if kv in self._dense else _lib.SK_KIND_STREAMING for kv in self.heads]
+            kinds = self.pool_kinds()
             self.pool = DevicePool(kinds, head_dim, self.physical_page, self.logical_page, self.quant_bits,
                                    self.sink_blocks, self.local_blocks, self._dtype, self._device, self._capacity)
             for kv in self.heads:
                 hp = self.pool_of(kv)
                 hp._pool, hp._stream = self.pool, self.stream_of[kv]
         return self.pool
+
+    def pool_kinds(self) -> list:
+        return [_lib.SK_KIND_DENSE if kv in self._dense else _lib.SK_KIND_STREAMING for kv in self.heads]
+
+    def adopt_pool(self, pool: DevicePool) -> DevicePool:
+        """Back this cache with an existing (emptied) device pool."""
+        if not pool.matches(self.pool_kinds(), pool.D, self.physical_page, self.logical_page, self.quant_bits,
+                            self.sink_blocks, self.local_blocks, self._dtype):
+            raise ValueError("pool geometry does not match this cache")
+        self.pool = pool
+        for kv in self.heads:
+            hp = self.pool_of(kv)
+            hp._pool, hp._stream = pool, self.stream_of[kv]
+        return pool
 
     def pool_of(self, kv_head: int) -> HeadPages:
         if kv_head in self.dense_pool:

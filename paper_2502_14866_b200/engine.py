@@ -196,12 +196,22 @@ class Engine:
     def _new_cache(self, num_kv_heads: int, head_dim: int, tokens: int) -> None:
         cfg = self.config
         dense = self._dense_kv_heads(num_kv_heads)
+        old = self.cache.pool if self.cache is not None else None
         self.cache = TwoWayCache(cfg.physical_page, cfg.logical_page, cfg.quant_bits, dense,
                                  set(range(num_kv_heads)) - dense, cfg.sink_blocks, cfg.local_blocks,
                                  dtype=self._dtype, device=self.device,
                                  capacity_tokens=max(self._capacity, tokens + 1))
-        self.cache.ensure_pool(head_dim)
-        g = self._group_size
+        # A fresh cache (engine.py:146-150) recycles the previous device pool when
+        # the geometry matches: emptied by a device-side reset, so a re-prefill
+        # issues no host->device copies on the compute stream (they would queue
+        # behind bulk uploads on the copy engine, see pipeline.py).
+        if old is not None and old.matches(self.cache.pool_kinds(), head_dim, cfg.physical_page, cfg.logical_page,
+                                           cfg.quant_bits, cfg.sink_blocks, cfg.local_blocks, self._dtype):
+            old.reset()
+            old.reserve(tokens + 1)
+            self.cache.adopt_pool(old)
+        else:
+            self.cache.ensure_pool(head_dim)
         masks = []
         for kv in range(num_kv_heads):
             mk = 0
@@ -209,11 +219,11 @@ class Engine:
                 if self.profiles[h].role == RETRIEVAL:
                     mk |= 1 << r
             masks.append(mk)
+        if getattr(self, "_row_mask_host", None) != masks:
+            self._row_mask = _device.h2d(np.array(masks, np.int32), self.device)
         self._row_mask_host = masks
-        self._row_mask = _device.h2d(np.array(masks, np.int32), self.device)
         self._sel = None
         self.selection_states = {}
-        del g
 
     def _plan(self, n: int, s: int):
         cfg = self.config
