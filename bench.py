@@ -397,7 +397,7 @@ def run_ours(args, rank, world, local_rank):
                                 "bytes_def": "per layer: KV heads x (K+2 pages x 9216 B) + stats (n_logical x 512 B) / reuse"}},
         "e2e": {"value": round(e2e_ms, 3) if e2e_ms else None, "unit": "ms", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "path": "Engine.prefill(Workload(pinned host tensors)) per layer, output copied back to pinned host"},
+                "path": "sk.prefill_layers(engines, pinned host q/k/v per layer, pinned host outputs): per-layer Engine.prefill_device with the H2D of layer l+1 and the D2H of layer l-1 overlapping layer l"},
         "decode_batched": batched,
         "gpu_launches": L * 3 + L * (1 if world > 1 else 0),
         "clocks": clk.summary(),
