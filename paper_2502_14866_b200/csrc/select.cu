@@ -245,6 +245,12 @@ __device__ __forceinline__ void score_rows(const uint8_t* sbuf, int np, int lp_p
 
 __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, int stage_cap, int32_t* sel_out,
                          int32_t* sel_count);
+constexpr int kRegTopkKeys = 16;                               // keys per thread held in registers
+constexpr int kRegTopkMax = kRegTopkKeys * kTopkThreads;       // n <= 4096 pages (256k tokens at P=64)
+constexpr int kRegTopkBits = 11;                               // radix digit: 2048 bins
+constexpr int kRegTopkSmem = 2 * (1 << kRegTopkBits) * 4;      // two histograms
+__device__ void topk_cta_reg(int n, int K, const double* scores, uint32_t* hist2, int32_t* sel_out,
+                             int32_t* sel_count);
 
 template <typename T, int LPC>
 #ifndef SK_SEL_MINB
@@ -336,7 +342,10 @@ __global__ void __launch_bounds__(kScoreThreads, SK_SEL_MINB) select_kernel(Pool
   }
   __syncthreads();
   if (!is_last || dbg == 2 || dbg == 3) return;
-  topk_cta(n_pages, K, scores, reinterpret_cast<uint64_t*>(smem), smem_bytes / 8, sel_out, sel_count_all + s);
+  if (n_pages <= kRegTopkMax && smem_bytes >= kRegTopkSmem && dbg != 7)
+    topk_cta_reg(n_pages, K, scores, reinterpret_cast<uint32_t*>(smem), sel_out, sel_count_all + s);
+  else
+    topk_cta(n_pages, K, scores, reinterpret_cast<uint64_t*>(smem), smem_bytes / 8, sel_out, sel_count_all + s);
 }
 
 // Block-wide exclusive scan of one value per thread (kTopkThreads threads)
@@ -529,6 +538,140 @@ __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, i
     if (take) sel_out[out_pos++] = i;
   }
   if (tid == kTopkThreads - 1) *sel_count = out_pos;
+}
+
+// Top-k of one stream, keys in registers (n <= kRegTopkMax).  Same result
+// as topk_cta -- pins, then the best K-|pins| others by (score desc, index
+// asc), ascending -- with far fewer block barriers: one shared 2048-bin
+// histogram per 11-bit radix pass (random scores rarely collide, so no
+// per-warp copies), double-buffered so zeroing the next one needs no extra
+// barrier, the boundary bin found with one block scan (3 barriers per pass),
+// and one packed scan (strict | equal counts) for the ordered compaction.
+__device__ void topk_cta_reg(int n, int K, const double* scores, uint32_t* hist2, int32_t* sel_out,
+                             int32_t* sel_count) {
+  constexpr int NB = 1 << kRegTopkBits;
+  constexpr int BPT = NB / kTopkThreads;  // bins per thread (8)
+  __shared__ uint32_t wtot[kTopkWarps + 1];
+  __shared__ uint64_t s_max[kTopkWarps], s_min[kTopkWarps];
+  __shared__ uint32_t sh_bin, sh_kk, sh_done;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int pin[3];
+  const int npins = pins_of(n, pin);
+  const int kpt = (n + kTopkThreads - 1) / kTopkThreads;
+  const int i0 = tid * kpt;
+  uint64_t key[kRegTopkKeys];
+  uint64_t kmax = 0, kmin = ~0ull;
+#pragma unroll
+  for (int j = 0; j < kRegTopkKeys; ++j) {
+    const int i = i0 + j;
+    key[j] = 0;
+    if (j < kpt && i < n && !is_pin(i, n)) key[j] = order_key(__ldcg(scores + i));
+    if (key[j]) {
+      kmax = key[j] > kmax ? key[j] : kmax;
+      kmin = key[j] < kmin ? key[j] : kmin;
+    }
+  }
+  for (int b = tid; b < NB; b += kTopkThreads) hist2[b] = 0;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const uint64_t a = __shfl_xor_sync(0xffffffffu, kmax, off), c = __shfl_xor_sync(0xffffffffu, kmin, off);
+    kmax = a > kmax ? a : kmax;
+    kmin = c < kmin ? c : kmin;
+  }
+  if (lane == 0) {
+    s_max[warp] = kmax;
+    s_min[warp] = kmin;
+  }
+  __syncthreads();
+  kmax = 0;
+  kmin = ~0ull;
+#pragma unroll
+  for (int w = 0; w < kTopkWarps; ++w) {
+    kmax = s_max[w] > kmax ? s_max[w] : kmax;
+    kmin = s_min[w] < kmin ? s_min[w] : kmin;
+  }
+  uint32_t kk = K - npins;  // keys still to take at/below the current prefix
+  // bits below `hi` are unresolved; the candidates agree on every bit above
+  int hi = kmax == kmin ? 0 : 64 - __clzll(kmax ^ kmin);
+  uint64_t mask = hi >= 64 ? 0ull : (~0ull << hi);
+  uint64_t prefix = kmax & mask;
+  int cur = 0;
+  while (hi > 0) {
+    const int w = hi < kRegTopkBits ? hi : kRegTopkBits;
+    const int shift = hi - w;
+    const uint32_t dm = (1u << w) - 1u;
+    uint32_t* h = hist2 + cur * NB;
+#pragma unroll
+    for (int j = 0; j < kRegTopkKeys; ++j)
+      if (key[j] && (key[j] & mask) == prefix) atomicAdd(&h[uint32_t(key[j] >> shift) & dm], 1u);
+    uint32_t* hn = hist2 + (cur ^ 1) * NB;
+    for (int b = tid; b < NB; b += kTopkThreads) hn[b] = 0;
+    __syncthreads();  // A: histogram complete
+    // thread t owns bins NB-1-BPT*t .. NB-BPT*(t+1), scanned from the top
+    uint32_t loc[BPT], sum = 0;
+#pragma unroll
+    for (int e = 0; e < BPT; ++e) {
+      loc[e] = h[NB - 1 - BPT * tid - e];
+      sum += loc[e];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += o;
+    }
+    if (lane == 31) wtot[warp] = incl;
+    __syncthreads();  // B: warp totals
+    uint32_t excl = incl - sum;
+#pragma unroll
+    for (int w2 = 0; w2 < kTopkWarps; ++w2) excl += w2 < warp ? wtot[w2] : 0u;
+    if (excl < kk && kk <= excl + sum) {
+      uint32_t cum = excl;
+#pragma unroll
+      for (int e = 0; e < BPT; ++e) {
+        if (cum + loc[e] >= kk && cum < kk) {
+          sh_bin = NB - 1 - BPT * tid - e;
+          sh_kk = kk - cum;
+          sh_done = loc[e] == kk - cum ? 1u : 0u;
+        }
+        cum += loc[e];
+      }
+    }
+    __syncthreads();  // C: boundary bin published
+    const uint32_t bin = sh_bin;
+    kk = sh_kk;
+    const bool done = sh_done;
+    prefix |= (uint64_t)bin << shift;
+    mask |= (uint64_t)dm << shift;
+    hi = shift;
+    cur ^= 1;
+    if (done) break;  // every key of the boundary bin is taken
+  }
+  // ordered compaction: pins and keys above the prefix are taken; of the keys
+  // equal to it, the kk lowest indices.  One scan of packed (taken | equal << 16).
+  uint32_t n_take = 0, n_eq = 0;
+#pragma unroll
+  for (int j = 0; j < kRegTopkKeys; ++j) {
+    const int i = i0 + j;
+    if (j >= kpt || i >= n) continue;
+    const uint64_t km = key[j] & mask;
+    if (is_pin(i, n) || (key[j] && km > prefix)) ++n_take;
+    else if (key[j] && km == prefix) ++n_eq;
+  }
+  uint32_t tot;
+  const uint32_t ex = block_scan(n_take | (n_eq << 16), wtot, tot);
+  uint32_t eq_rank = ex >> 16;
+  uint32_t pos = (ex & 0xFFFFu) + (eq_rank < kk ? eq_rank : kk);
+#pragma unroll
+  for (int j = 0; j < kRegTopkKeys; ++j) {
+    const int i = i0 + j;
+    if (j >= kpt || i >= n) continue;
+    const uint64_t km = key[j] & mask;
+    bool take = is_pin(i, n) || (key[j] && km > prefix);
+    if (!take && key[j] && km == prefix) take = eq_rank++ < kk;
+    if (take) sel_out[pos++] = i;
+  }
+  if (tid == kTopkThreads - 1) *sel_count = (tot & 0xFFFFu) + ((tot >> 16) < kk ? (tot >> 16) : kk);
 }
 
 template <typename T>

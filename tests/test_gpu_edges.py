@@ -234,3 +234,30 @@ def test_prefill_host_torch_equals_device_path(n, pinned):
     q_bad[n // 3, 1, 5] = float("inf")
     with pytest.raises(ValueError, match="non-finite"):
         e_host.prefill(sk.Workload(q_bad, k, v))
+
+
+@pytest.mark.parametrize("n", [5, 37, 300, 2049, 4096, 4097, 5000])
+@pytest.mark.parametrize("ties", [False, True])
+def test_topk_paths_against_oracle(n, ties):
+    """K2's top-k -- the register path (n <= 4096 pages) and the staged
+    fallback (n > 4096) -- against the oracle's (score desc, index asc)
+    selection, on random and on heavily tied page scores."""
+    from paper_2502_14866_b200.cache import PageStats, PhysicalPage
+
+    rng = np.random.default_rng(n + 7 * ties)
+    d = 16
+    if ties:  # few distinct boxes -> many equal scores
+        lo = rng.integers(-2, 1, (n, d)).astype(np.float64) * 0.5
+        hi = lo + rng.integers(0, 2, (n, d)) * 0.5
+    else:
+        a, b = fp16_vals(rng, n, d).astype(np.float64), fp16_vals(rng, n, d).astype(np.float64)
+        lo, hi = np.minimum(a, b), np.maximum(a, b)
+    q = fp16_vals(rng, 2, d).astype(np.float64)
+    z = np.zeros(d)
+    ours_pages = [PhysicalPage(i, 0, 64, 64, None, None, z, z, z, z, [PageStats(lo[i], hi[i], 64)]) for i in range(n)]
+    ref_pages = [O.Page(i, 64, None, None, None, None, None, None, [(lo[i], hi[i], 64)]) for i in range(n)]
+    for k in sorted({4, 7, 64, max(4, n // 3), n - 1}):
+        if k >= n:
+            continue
+        got = sk.select_pages(q, ours_pages, k * 64, 64)
+        assert got == O.top_pages(q, ref_pages, k * 64, 64), (n, k, ties)
