@@ -19,7 +19,8 @@ lib = _lib.load()
 
 
 def make(gates):
-    cfg = sk.EngineConfig(quant_bits=4, budget_tokens=4096, reuse_interval=4, local_blocks=4)
+    cfg = sk.EngineConfig(quant_bits=4, budget_tokens=int(os.environ.get("SK_BUDGET", 4096)), reuse_interval=4,
+                          local_blocks=4)
     prof = sk.classify_heads(gates, 0.5 if len(set(gates)) > 1 else 0.0, 1, 4)
     e = sk.Engine(cfg, prof, device="cuda:0", capacity_tokens=ctx + 4096)
     g = torch.Generator(device="cuda").manual_seed(0)
