@@ -22,6 +22,9 @@ for _ in range(L):
     k = torch.randn((N, HKV, D), generator=g, device="cuda", dtype=torch.float16)
     e.load_context(k, k)
     engines.append(e)
+if os.environ.get("SK_PROBE_NO_APPEND"):  # ablation: drop the side-stream K1 from the graph
+    from paper_2502_14866_b200 import _lib
+    _lib.load().sk_append_pages = lambda *a: 0
 dg = DecodeGraph(engines, 40, D, record_ledger=False)
 dg.q.normal_(generator=g)
 dg.k.normal_(generator=g)
