@@ -236,10 +236,8 @@ def gen_needles_device(kind: str, trials: int, num_history: int, head_dim: int, 
     keys[..., :head_dim] = torch.randn((num_history, trials, head_dim), generator=gen, device=dev).to(dtype)
     values[..., :head_dim] = torch.randn((num_history, trials, head_dim), generator=gen, device=dev).to(dtype)
     probes[..., :head_dim] = torch.randn((trials, group, head_dim), generator=gen, device=dev).to(dtype)
-    free = _free_pages(num_history, physical_page)
     spec = WorkloadSpec(kind, num_history, 1, 1, 1, head_dim, margin, cluster_span, physical_page, logical_page)
     positions = np.array([_needle_positions(spec, rng) for _ in range(trials)], np.int64)
-    del free
     page = physical_page if kind == NEEDLE else logical_page
     scores = _box_scores_device(keys, probes, page)  # [T, nb]
     excl = torch.zeros_like(scores, dtype=torch.bool)
