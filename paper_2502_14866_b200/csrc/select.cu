@@ -245,10 +245,10 @@ __device__ __forceinline__ void score_rows(const uint8_t* sbuf, int np, int lp_p
 
 __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, int stage_cap, int32_t* sel_out,
                          int32_t* sel_count);
-constexpr int kRegTopkKeys = 16;                               // keys per thread held in registers
-constexpr int kRegTopkMax = kRegTopkKeys * kTopkThreads;       // n <= 4096 pages (256k tokens at P=64)
+constexpr int kRegTopkMax = 24 * kTopkThreads;                 // n <= 6144 pages (384k tokens at P=64)
 constexpr int kRegTopkBits = 11;                               // radix digit: 2048 bins
 constexpr int kRegTopkSmem = 2 * (1 << kRegTopkBits) * 4;      // two histograms
+template <int KPT>
 __device__ void topk_cta_reg(int n, int K, const double* scores, uint32_t* hist2, int32_t* sel_out,
                              int32_t* sel_count);
 
@@ -342,8 +342,10 @@ __global__ void __launch_bounds__(kScoreThreads, SK_SEL_MINB) select_kernel(Pool
   }
   __syncthreads();
   if (!is_last || dbg == 2 || dbg == 3) return;
-  if (n_pages <= kRegTopkMax && smem_bytes >= kRegTopkSmem && dbg != 7)
-    topk_cta_reg(n_pages, K, scores, reinterpret_cast<uint32_t*>(smem), sel_out, sel_count_all + s);
+  if (n_pages <= 16 * kTopkThreads && smem_bytes >= kRegTopkSmem && dbg != 7)  // keys per thread: as few as fit
+    topk_cta_reg<16>(n_pages, K, scores, reinterpret_cast<uint32_t*>(smem), sel_out, sel_count_all + s);
+  else if (n_pages <= kRegTopkMax && smem_bytes >= kRegTopkSmem && dbg != 7)
+    topk_cta_reg<24>(n_pages, K, scores, reinterpret_cast<uint32_t*>(smem), sel_out, sel_count_all + s);
   else
     topk_cta(n_pages, K, scores, reinterpret_cast<uint64_t*>(smem), smem_bytes / 8, sel_out, sel_count_all + s);
 }
@@ -547,6 +549,7 @@ __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, i
 // per-warp copies), double-buffered so zeroing the next one needs no extra
 // barrier, the boundary bin found with one block scan (3 barriers per pass),
 // and one packed scan (strict | equal counts) for the ordered compaction.
+template <int KPT>
 __device__ void topk_cta_reg(int n, int K, const double* scores, uint32_t* hist2, int32_t* sel_out,
                              int32_t* sel_count) {
   constexpr int NB = 1 << kRegTopkBits;
@@ -559,10 +562,10 @@ __device__ void topk_cta_reg(int n, int K, const double* scores, uint32_t* hist2
   const int npins = pins_of(n, pin);
   const int kpt = (n + kTopkThreads - 1) / kTopkThreads;
   const int i0 = tid * kpt;
-  uint64_t key[kRegTopkKeys];
+  uint64_t key[KPT];
   uint64_t kmax = 0, kmin = ~0ull;
 #pragma unroll
-  for (int j = 0; j < kRegTopkKeys; ++j) {
+  for (int j = 0; j < KPT; ++j) {
     const int i = i0 + j;
     key[j] = 0;
     if (j < kpt && i < n && !is_pin(i, n)) key[j] = order_key(__ldcg(scores + i));
@@ -602,7 +605,7 @@ __device__ void topk_cta_reg(int n, int K, const double* scores, uint32_t* hist2
     const uint32_t dm = (1u << w) - 1u;
     uint32_t* h = hist2 + cur * NB;
 #pragma unroll
-    for (int j = 0; j < kRegTopkKeys; ++j)
+    for (int j = 0; j < KPT; ++j)
       if (key[j] && (key[j] & mask) == prefix) atomicAdd(&h[uint32_t(key[j] >> shift) & dm], 1u);
     uint32_t* hn = hist2 + (cur ^ 1) * NB;
     for (int b = tid; b < NB; b += kTopkThreads) hn[b] = 0;
@@ -651,7 +654,7 @@ __device__ void topk_cta_reg(int n, int K, const double* scores, uint32_t* hist2
   // equal to it, the kk lowest indices.  One scan of packed (taken | equal << 16).
   uint32_t n_take = 0, n_eq = 0;
 #pragma unroll
-  for (int j = 0; j < kRegTopkKeys; ++j) {
+  for (int j = 0; j < KPT; ++j) {
     const int i = i0 + j;
     if (j >= kpt || i >= n) continue;
     const uint64_t km = key[j] & mask;
@@ -663,7 +666,7 @@ __device__ void topk_cta_reg(int n, int K, const double* scores, uint32_t* hist2
   uint32_t eq_rank = ex >> 16;
   uint32_t pos = (ex & 0xFFFFu) + (eq_rank < kk ? eq_rank : kk);
 #pragma unroll
-  for (int j = 0; j < kRegTopkKeys; ++j) {
+  for (int j = 0; j < KPT; ++j) {
     const int i = i0 + j;
     if (j >= kpt || i >= n) continue;
     const uint64_t km = key[j] & mask;

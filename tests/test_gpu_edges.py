@@ -236,11 +236,11 @@ def test_prefill_host_torch_equals_device_path(n, pinned):
         e_host.prefill(sk.Workload(q_bad, k, v))
 
 
-@pytest.mark.parametrize("n", [5, 37, 300, 2049, 4096, 4097, 5000])
+@pytest.mark.parametrize("n", [5, 37, 300, 2049, 4096, 4097, 6144, 6145, 7000])
 @pytest.mark.parametrize("ties", [False, True])
 def test_topk_paths_against_oracle(n, ties):
-    """K2's top-k -- the register path (n <= 4096 pages) and the staged
-    fallback (n > 4096) -- against the oracle's (score desc, index asc)
+    """K2's top-k -- the register path (n <= 6144 pages) and the staged
+    fallback (n > 6144) -- against the oracle's (score desc, index asc)
     selection, on random and on heavily tied page scores."""
     from paper_2502_14866_b200.cache import PageStats, PhysicalPage
 
