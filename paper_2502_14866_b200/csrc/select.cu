@@ -96,10 +96,16 @@ __device__ __forceinline__ void to_f64x4(uint2 w, double* o) {
   o[3] = b.y;
 }
 
-// q+ / q- (fp64) of retrieval rows [rbase, rbase + RMAX) for this lane's channels
+// Retrieval rows [rbase, rbase + RMAX) for this lane's channels.  Up to two
+// rows use the sign-select form max(q*kmax, q*kmin) = q * (q > 0 ? kmax :
+// kmin): qa = q (fp64) and per 32-bit word of stats a mask picking k_max
+// where q > 0, so each (row, channel) costs one conversion and one DFMA.
+// Four rows share the converted k_min/k_max instead: qa = q+, qb = q-.
+// Either way the fp64 sum sees exactly the same non-zero terms in the same
+// order (sum over channels of q+*kmax + q-*kmin), so scores are identical.
 template <typename T, int RMAX>
 __device__ __forceinline__ void load_rows(const T* q, int64_t q_rs, uint32_t rmask, int rbase, int rows, int D,
-                                          double (&qp)[RMAX][4], double (&qm)[RMAX][4]) {
+                                          double (&qd)[RMAX][4], double (&qb)[RMAX][4], uint32_t (&qsel)[RMAX][2]) {
   const int lane = threadIdx.x & 31, cpl = D / 32;
   uint32_t mbits = rmask;
   for (int r = 0; r < rbase; ++r) mbits &= mbits - 1;
@@ -109,12 +115,52 @@ __device__ __forceinline__ void load_rows(const T* q, int64_t q_rs, uint32_t rma
     const bool ok = rbase + r < rows && g >= 0;
     if (ok) mbits &= mbits - 1;
     const T* qr = q + (int64_t)(ok ? g : 0) * q_rs + lane * cpl;
+    qsel[r][0] = qsel[r][1] = 0u;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const double x = (ok && c < cpl) ? (double)DT<T>::to_f(qr[c]) : 0.0;
-      qp[r][c] = x > 0.0 ? x : 0.0;
-      qm[r][c] = x < 0.0 ? x : 0.0;
+      if constexpr (RMAX <= 2) {
+        qd[r][c] = x;
+        if (x > 0.0) qsel[r][c >> 1] |= (c & 1) ? 0xFFFF0000u : 0x0000FFFFu;
+      } else {
+        qd[r][c] = x > 0.0 ? x : 0.0;
+        qb[r][c] = x < 0.0 ? x : 0.0;
+      }
     }
+  }
+}
+
+template <typename T, int RMAX>
+__device__ __forceinline__ void row_scores(uint2 wmin, uint2 wmax, const double (&qd)[RMAX][4],
+                                           const double (&qb)[RMAX][4], const uint32_t (&qsel)[RMAX][2],
+                                           double* acc_out) {
+  if constexpr (RMAX > 2) {
+    double kmin[4], kmax[4];
+    to_f64x4<T>(wmin, kmin);
+    to_f64x4<T>(wmax, kmax);
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        acc = fma(qd[r][c], kmax[c], acc);
+        acc = fma(qb[r][c], kmin[c], acc);
+      }
+      acc_out[r] = acc;
+    }
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    uint2 w;
+    w.x = (wmax.x & qsel[r][0]) | (wmin.x & ~qsel[r][0]);
+    w.y = (wmax.y & qsel[r][1]) | (wmin.y & ~qsel[r][1]);
+    double k[4];
+    to_f64x4<T>(w, k);
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc = fma(qd[r][c], k[c], acc);
+    acc_out[r] = acc;
   }
 }
 
@@ -124,7 +170,7 @@ __device__ __forceinline__ void load_rows(const T* q, int64_t q_rs, uint32_t rma
 // butterfly pass (RMAX * LPC <= 16).
 template <typename T, int RMAX, int LPC>
 __device__ __forceinline__ void score_batch(const uint8_t* sbuf, int np, int lp_per, int nl_rel, int D,
-                                            const double (&qp)[RMAX][4], const double (&qm)[RMAX][4], int rbase,
+                                            const double (&qd)[RMAX][4], const double (&qb)[RMAX][4], const uint32_t (&qsel)[RMAX][2], int rbase,
                                             int rows, double* out) {
   constexpr int NV = RMAX * LPC;
   const int lane = threadIdx.x & 31;
@@ -146,19 +192,10 @@ __device__ __forceinline__ void score_batch(const uint8_t* sbuf, int np, int lp_
           wmin = make_uint2(*reinterpret_cast<const uint32_t*>(st + lane * 2), 0u);
           wmax = make_uint2(*reinterpret_cast<const uint32_t*>(st + D + lane * 2), 0u);
         }
-        double kmin[4], kmax[4];
-        to_f64x4<T>(wmin, kmin);
-        to_f64x4<T>(wmax, kmax);
+        double acc[RMAX];
+        row_scores<T, RMAX>(wmin, wmax, qd, qb, qsel, acc);
 #pragma unroll
-        for (int r = 0; r < RMAX; ++r) {
-          double acc = 0.0;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            acc = fma(qp[r][c], kmax[c], acc);
-            acc = fma(qm[r][c], kmin[c], acc);
-          }
-          v[r * LPC + jj] = acc;
-        }
+        for (int r = 0; r < RMAX; ++r) v[r * LPC + jj] = acc[r];
       }
       Butterfly<NV, 16>::run(v, lane);
       const int idx = lane >> (6 - __ffs(NV));  // value index owned by this lane
@@ -179,8 +216,9 @@ __device__ __forceinline__ void score_batch(const uint8_t* sbuf, int np, int lp_
 // is paid once per PG pages instead of once per page.
 template <typename T, int RMAX, int LP>
 __device__ __forceinline__ void score_batch_grouped(const uint8_t* sbuf, int np, int nl_rel, int D,
-                                                    const double (&qp)[RMAX][4], const double (&qm)[RMAX][4],
-                                                    int rbase, int rows, double* out) {
+                                                    const double (&qd)[RMAX][4], const double (&qb)[RMAX][4],
+                                                    const uint32_t (&qsel)[RMAX][2], int rbase, int rows,
+                                                    double* out) {
   constexpr int PG = 32 / (RMAX * LP);
   constexpr int NV = 32;
   const int lane = threadIdx.x & 31;
@@ -202,19 +240,10 @@ __device__ __forceinline__ void score_batch_grouped(const uint8_t* sbuf, int np,
           wmin = make_uint2(*reinterpret_cast<const uint32_t*>(st + lane * 2), 0u);
           wmax = make_uint2(*reinterpret_cast<const uint32_t*>(st + D + lane * 2), 0u);
         }
-        double kmin[4], kmax[4];
-        to_f64x4<T>(wmin, kmin);
-        to_f64x4<T>(wmax, kmax);
+        double acc[RMAX];
+        row_scores<T, RMAX>(wmin, wmax, qd, qb, qsel, acc);
 #pragma unroll
-        for (int r = 0; r < RMAX; ++r) {
-          double acc = 0.0;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            acc = fma(qp[r][c], kmax[c], acc);
-            acc = fma(qm[r][c], kmin[c], acc);
-          }
-          v[(pg * RMAX + r) * LP + lp] = acc;
-        }
+        for (int r = 0; r < RMAX; ++r) v[(pg * RMAX + r) * LP + lp] = acc[r];
       }
     }
     Butterfly<NV, 16>::run(v, lane);  // lane l now holds value l
@@ -231,15 +260,16 @@ template <typename T, int RMAX, int LPC>
 __device__ __forceinline__ void score_rows(const uint8_t* sbuf, int np, int lp_per, int nl_rel, int D,
                                            const T* q, int64_t q_rs, uint32_t rmask, int rows, double* out) {
   for (int rb = 0; rb < rows; rb += RMAX) {
-    double qp[RMAX][4], qm[RMAX][4];
-    load_rows<T, RMAX>(q, q_rs, rmask, rb, rows, D, qp, qm);
+    double qd[RMAX][4], qb[RMAX][4];
+    uint32_t qsel[RMAX][2];
+    load_rows<T, RMAX>(q, q_rs, rmask, rb, rows, D, qd, qb, qsel);
     if constexpr (LPC * RMAX <= 32 && 32 % (LPC * RMAX) == 0 && 32 / (LPC * RMAX) > 1) {
       if (lp_per == LPC) {
-        score_batch_grouped<T, RMAX, LPC>(sbuf, np, nl_rel, D, qp, qm, rb, rows, out);
+        score_batch_grouped<T, RMAX, LPC>(sbuf, np, nl_rel, D, qd, qb, qsel, rb, rows, out);
         continue;
       }
     }
-    score_batch<T, RMAX, LPC>(sbuf, np, lp_per, nl_rel, D, qp, qm, rb, rows, out);
+    score_batch<T, RMAX, LPC>(sbuf, np, lp_per, nl_rel, D, qd, qb, qsel, rb, rows, out);
   }
 }
 
