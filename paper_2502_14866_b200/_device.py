@@ -77,3 +77,9 @@ def to_output(t: torch.Tensor, like, np_dtype=None):
         return t
     out = t.float().cpu().numpy()
     return out.astype(np_dtype) if np_dtype is not None else out
+
+
+def all_finite(t: torch.Tensor) -> torch.Tensor:
+    """Device bool scalar: no NaN/inf in t.  One read of t (max-norm; NaN and
+    inf propagate through it), no full-size temporaries."""
+    return torch.isfinite(torch.linalg.vector_norm(t, float("inf")))

@@ -321,7 +321,7 @@ def check_finite_device(w: Workload, q, k, v) -> None:
     evaluated on their device copies."""
     if _device.is_torch(w.q) and not w.q.is_cuda:
         for name, t in (("q", q), ("k", k), ("v", v)):
-            if not bool(torch.isfinite(t).all()):
+            if not bool(_device.all_finite(t)):
                 raise ValueError(f"non-finite values in {name}")
 
 

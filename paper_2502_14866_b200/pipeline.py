@@ -70,7 +70,7 @@ def prefill_layers(engines: Sequence, inputs: Sequence, outputs: Sequence) -> No
         b = layer % 2
         comp.wait_event(ev_in[b])
         q, k, v = bufs[b]
-        bad[layer] = ~(torch.isfinite(q).all() & torch.isfinite(k).all() & torch.isfinite(v).all())
+        bad[layer] = ~(_device.all_finite(q) & _device.all_finite(k) & _device.all_finite(v))
         out = engines[layer].prefill_device(q, k, v, d)
         ev_used[b].record(comp)
         with torch.cuda.stream(s_out):
