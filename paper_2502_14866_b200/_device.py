@@ -82,4 +82,6 @@ def to_output(t: torch.Tensor, like, np_dtype=None):
 def all_finite(t: torch.Tensor) -> torch.Tensor:
     """Device bool scalar: no NaN/inf in t.  One read of t (max-norm; NaN and
     inf propagate through it), no full-size temporaries."""
+    if not t.is_floating_point():
+        return torch.ones((), dtype=torch.bool, device=t.device)
     return torch.isfinite(torch.linalg.vector_norm(t, float("inf")))

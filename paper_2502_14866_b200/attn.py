@@ -51,7 +51,7 @@ class Workload:
         for name, t in (("q", q), ("k", k), ("v", v)):
             if _device.is_torch(t) and not t.is_cuda:
                 continue  # host torch tensors are checked on the device after upload (Engine / blockwise)
-            finite = bool(torch.isfinite(t).all()) if _device.is_torch(t) else bool(np.isfinite(t).all())
+            finite = bool(_device.all_finite(t)) if _device.is_torch(t) else bool(np.isfinite(t).all())
             if not finite:
                 raise ValueError(f"non-finite values in {name}")
         self.q, self.k, self.v = q, k, v

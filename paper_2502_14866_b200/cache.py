@@ -414,7 +414,7 @@ class HeadPages:
             raise ValueError("keys/values must both be [m, dim]")
         if np.shape(keys)[0] < 1:
             raise ValueError("append requires at least one token")
-        fin = (lambda t: bool(torch.isfinite(t).all())) if _device.is_torch(keys) else (lambda t: bool(np.isfinite(t).all()))
+        fin = (lambda t: bool(_device.all_finite(t))) if _device.is_torch(keys) else (lambda t: bool(np.isfinite(t).all()))
         if not (fin(keys) and fin(values)):
             raise ValueError("non-finite keys or values")
         if getattr(self, "_restored_partial", False):
