@@ -46,3 +46,36 @@ def test_pipelined_rejects_non_finite():
     with pytest.raises(ValueError, match="non-finite"):
         sk.prefill_layers([sk.Engine(cfg, prof, device="cuda:0")] * 2, [(q, k, k), (q, k, v)],
                           [torch.empty_like(q), torch.empty_like(q)])
+
+
+def test_reprefill_recycles_pool_like_a_fresh_engine():
+    """A second (and third) prefill on the same Engine recycles its device
+    pool (DevicePool.reset): outputs, pages and the following decode step
+    must equal a fresh engine's -- shorter and longer contexts included."""
+    rng = np.random.default_rng(5)
+    h, hkv, d = 8, 2, 128
+    gates = [0.9, 0.1, 0.8, 0.2, 0.85, 0.15, 0.7, 0.3]
+    cfg = sk.EngineConfig(local_blocks=2, budget_tokens=256)
+    prof = sk.classify_heads(gates, 0.5, 1, 2)
+    reused = sk.Engine(cfg, prof, device="cuda:0")
+    for n in (900, 333, 2100):
+        q = rng.standard_normal((n, h, d)).astype(np.float16).astype(np.float32)
+        k = rng.standard_normal((n, hkv, d)).astype(np.float16).astype(np.float32)
+        v = rng.standard_normal((n, hkv, d)).astype(np.float16).astype(np.float32)
+        fresh = sk.Engine(cfg, prof, device="cuda:0")
+        a = reused.prefill(sk.Workload(q, k, v))
+        b = fresh.prefill(sk.Workload(q, k, v))
+        np.testing.assert_array_equal(a, b)
+        for kv in range(hkv):
+            pa, pb = reused.cache.pool_of(kv).live_pages(), fresh.cache.pool_of(kv).live_pages()
+            assert [p.page_id for p in pa] == [p.page_id for p in pb]
+            for x, y in zip(pa, pb):
+                np.testing.assert_array_equal(x.k_codes, y.k_codes)
+                np.testing.assert_array_equal(x.v_codes, y.v_codes)
+                assert len(x.stats) == len(y.stats)
+        qn = rng.standard_normal((h, d)).astype(np.float32)
+        kn = rng.standard_normal((hkv, d)).astype(np.float32)
+        vn = rng.standard_normal((hkv, d)).astype(np.float32)
+        ra, rb = reused.decode_step(qn, kn, vn), fresh.decode_step(qn, kn, vn)
+        assert [t.positions for t in ra.index_tables] == [t.positions for t in rb.index_tables]
+        np.testing.assert_array_equal(ra.output, rb.output)
