@@ -133,7 +133,12 @@ int sk_gather_pages(const sk_pool* pool, int32_t n_streams, int32_t n_tokens, vo
  *   sel_count: device [n_streams].
  *   max_pages_hint: >= ceil(max tokens / P), sizes the grid.
  */
+/* Workspace bytes: [u32 ticket per stream, padded to 256 B | f64 page score
+ * per (stream, page < max_pages)].  Zero it once; the kernel re-arms its
+ * tickets, so one buffer serves every launch with a max_pages_hint it fits.
+ * The scores of the last launch start at sk_select_scores_offset(n). */
 int64_t sk_select_workspace(int32_t n_streams, int32_t max_pages);
+int64_t sk_select_scores_offset(int32_t n_streams);
 int sk_select_pages(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
                     int64_t q_stream_stride, int64_t q_row_stride, const uint32_t* row_mask,
                     const int32_t* tokens, const uint8_t* invoke, int32_t budget_pages, int32_t max_pages_hint,
@@ -145,21 +150,25 @@ int sk_select_pages(const sk_pool* pool, int32_t n_streams, int32_t group_rows, 
  * per-head page loop of Engine.decode_step (engine.py:257-281) with
  * PhysicalPage.dequantize (cache.py:97-102) and merge_block
  * (attn.py:191-229).  Per stream, group row r attends: the stream's
- * selection (retrieval rows) or the sink+local window of the current page
- * count (streaming rows), then the raw new token in-register.  Pages are
- * dequantised on the fly; splits are merged with log-sum-exp.  If
- * fuse_append != 0 the last CTA of each stream then appends k_new/v_new
- * (K1 semantics, one token) and increments tokens[s].
+ * selection (retrieval rows, bit r of row_mask[s] set) or the sink+local
+ * window of the current page count (streaming rows, streaming_schedule at
+ * qt = page_count - 1, heads.py:107-125), then the raw new token
+ * in-register.  Pages are dequantised on the fly; the CTAs of a stream
+ * merge their partials with log-sum-exp.
+ *   row_window: device [n_streams][group_rows] u32 = sink_blocks | local_blocks << 16
+ *               of each streaming row (its HeadProfile), or NULL for the pool's window.
+ *               A streaming-pool stream only holds the pool's window: the caller must
+ *               not ask for more (the reference raises "evicted" there).
+ *   append_new: != 0 appends k_new/v_new (K1, one token) right behind the attention on
+ *               the same stream (a second launch) and increments tokens[s].
  *   out: element (s, r, c) at out + s*out_stream_stride + r*out_row_stride + c, type out_dtype.
  */
-int64_t sk_decode_workspace(int32_t n_streams, int32_t group_rows, int32_t head_dim, int32_t max_splits);
 int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
                    int64_t q_stream_stride, int64_t q_row_stride, const void* k_new, const void* v_new,
-                   int64_t new_stream_stride, const uint32_t* row_mask, const int32_t* sel,
-                   const int32_t* sel_count, int32_t sel_stride, int32_t* tokens, float softmax_scale,
-                   void* out, int64_t out_stream_stride, int64_t out_row_stride, int32_t out_dtype,
-                   int32_t pages_per_split, int32_t max_splits, int32_t fuse_append, void* workspace,
-                   int64_t workspace_bytes, void* stream);
+                   int64_t new_stream_stride, const uint32_t* row_mask, const uint32_t* row_window,
+                   const int32_t* sel, const int32_t* sel_count, int32_t sel_stride, int32_t* tokens,
+                   float softmax_scale, void* out, int64_t out_stream_stride, int64_t out_row_stride,
+                   int32_t out_dtype, int32_t append_new, void* stream);
 
 /*
  * K4 -- block-sparse causal prefill attention on tcgen05 tensor cores.

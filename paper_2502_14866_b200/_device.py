@@ -49,13 +49,68 @@ def is_torch(x) -> bool:
     return isinstance(x, torch.Tensor)
 
 
+_ALLOW_ROUNDING = False
+
+
+def allow_input_rounding(flag: bool = True) -> None:
+    """Opt in to rounding wider inputs (fp32/fp64) to the device dtype.
+
+    The reference computes in its input dtype (attn.py:28-30).  The B200 path
+    stores pages, statistics and queries in fp16/bf16, so its page stats,
+    codes and selections equal the reference's only for inputs the device
+    dtype represents exactly; by default any other input is refused with a
+    ValueError instead of being rounded silently."""
+    global _ALLOW_ROUNDING
+    _ALLOW_ROUNDING = bool(flag)
+
+
+class rounding_allowed:
+    """Context manager: allow_input_rounding(True) inside, the previous
+    policy restored on exit (for harness code that only counts tiles)."""
+
+    def __enter__(self):
+        self._prev = _ALLOW_ROUNDING
+        allow_input_rounding(True)
+        return self
+
+    def __exit__(self, *exc):
+        allow_input_rounding(self._prev)
+        return False
+
+
+def _check_exact(src: torch.Tensor, dst: torch.Tensor) -> None:
+    """src (wide, on the device) == dst (device dtype) element for element;
+    NaN passes here so the callers' finiteness checks keep their messages."""
+    back = dst.to(src.dtype)
+    bad = ~((back == src) | torch.isnan(src))
+    if bool(bad.any()):
+        i = int(bad.flatten().nonzero()[0])
+        raise ValueError(f"input value {src.flatten()[i].item()!r} is not exactly representable in {dst.dtype} "
+                         f"(the device dtype); cast the inputs to {dst.dtype} first, or call "
+                         f"paper_2502_14866_b200.allow_input_rounding(True) to accept rounded page stats")
+
+
 def to_device(x, dtype: torch.dtype, device: torch.device, pad_to: int | None = None) -> torch.Tensor:
-    """numpy / torch -> contiguous device tensor of `dtype`, last dim zero-padded."""
+    """numpy / torch -> contiguous device tensor of `dtype`, last dim zero-padded.
+    Wider floating inputs must be exact in `dtype` (see allow_input_rounding)."""
     t = x if is_torch(x) else torch.from_numpy(np.ascontiguousarray(x))
-    t = t.to(device=device, dtype=dtype, non_blocking=True)
+    if t.dtype != dtype and t.is_floating_point() and not _ALLOW_ROUNDING:
+        wide = t.to(device=device, non_blocking=True)
+        t = wide.to(dtype)
+        _check_exact(wide, t)
+    else:
+        t = t.to(device=device, dtype=dtype, non_blocking=True)
     if pad_to is not None and t.shape[-1] != pad_to:
         t = torch.nn.functional.pad(t, (0, pad_to - t.shape[-1]))
     return t.contiguous()
+
+
+def exact_cast(t: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:
+    """t.to(dtype), refusing values `dtype` cannot hold exactly (unless rounding is allowed)."""
+    out = t.to(dtype)
+    if t.dtype != dtype and t.is_floating_point() and not _ALLOW_ROUNDING:
+        _check_exact(t, out)
+    return out
 
 
 def h2d(a, device: torch.device, dtype=None) -> torch.Tensor:

@@ -20,8 +20,8 @@ LIB_PATH = os.environ.get("SK_LIB_PATH") or os.path.join(os.path.dirname(os.path
 
 # every symbol include/sparsekv_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ("sk_version", "sk_last_error", "sk_device_supported", "sk_slot_bytes", "sk_append_pages",
-           "sk_gather_pages", "sk_select_workspace", "sk_select_pages",
-           "sk_decode_workspace", "sk_decode_attn", "sk_prefill_attn")
+           "sk_gather_pages", "sk_select_workspace", "sk_select_scores_offset", "sk_select_pages",
+           "sk_decode_attn", "sk_prefill_attn")
 
 
 class SkPool(C.Structure):
@@ -49,14 +49,14 @@ _SIGS = {
     "sk_gather_pages": (C.c_int, [C.POINTER(SkPool), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
                                   C.c_int64, C.c_void_p]),
     "sk_select_workspace": (C.c_int64, [C.c_int32, C.c_int32]),
+    "sk_select_scores_offset": (C.c_int64, [C.c_int32]),
     "sk_select_pages": (C.c_int, [C.POINTER(SkPool), C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_int64,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                   C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]),
-    "sk_decode_workspace": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "sk_decode_attn": (C.c_int, [C.POINTER(SkPool), C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_int64,
                                  C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
-                                 C.c_int32, C.c_void_p, C.c_float, C.c_void_p, C.c_int64, C.c_int64, C.c_int32,
-                                 C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]),
+                                 C.c_void_p, C.c_int32, C.c_void_p, C.c_float, C.c_void_p, C.c_int64, C.c_int64,
+                                 C.c_int32, C.c_int32, C.c_void_p]),
     "sk_prefill_attn": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                   C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_void_p, C.c_int32,
                                   C.c_void_p, C.c_void_p, C.c_void_p]),

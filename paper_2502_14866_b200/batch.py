@@ -16,6 +16,7 @@ parity test checks every sequence against its own `Engine`.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import _device, _lib
@@ -58,10 +59,20 @@ class BatchedLayer:
                                config.sink_blocks, config.local_blocks, dtype, self.device, capacity_tokens)
         self._row_mask_host = masks * batch
         self._row_mask = _device.h2d(torch.tensor(self._row_mask_host, dtype=torch.int32).numpy(), self.device)
+        pool_win = config.sink_blocks | (config.local_blocks << 16)
+        wins = [pool_win if p.role == RETRIEVAL else (p.sink_blocks | (p.local_blocks << 16)) for p in profiles]
+        if any(kinds[kv] == _lib.SK_KIND_STREAMING and any(w != pool_win for w in wins[kv * g:(kv + 1) * g])
+               for kv in range(num_kv_heads)):
+            raise KeyError("a streaming head's window differs from the streaming pool's (evicted pages)")
+        self._row_window = None if all(w == pool_win for w in wins) else \
+            _device.h2d(np.array(wins * batch, np.uint32), self.device)
         self.cache = _StreamsView(self.pool, [s for s, k in enumerate(kinds) if k == _lib.SK_KIND_DENSE])
         self.selection_states: dict = {}
         self.ledger = CostLedger()
         self.decode_steps = 0
+
+    def row_window_ptr(self):
+        return None if self._row_window is None else self._row_window.data_ptr()
 
     def load_context(self, seq: int, k: torch.Tensor, v: torch.Tensor) -> None:
         """K1 bulk append of one sequence's history (device [S, Hkv, Dp], pool dtype)."""

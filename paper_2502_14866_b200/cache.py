@@ -91,6 +91,15 @@ def _np_view(raw_u8: np.ndarray, dtype: torch.dtype) -> np.ndarray:
     return (u16.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
 
 
+def _np_exact(a: np.ndarray, np_dt) -> np.ndarray:
+    """a.astype(np_dt), refusing values the pool dtype cannot hold exactly
+    (a snapshot restores bit-exact pages or nothing; see allow_input_rounding)."""
+    out = np.asarray(a).astype(np_dt)
+    if not _device._ALLOW_ROUNDING and not np.array_equal(out.astype(np.float64), np.asarray(a, np.float64)):
+        raise ValueError(f"snapshot values are not exactly representable in {np.dtype(np_dt).name} (the pool dtype)")
+    return out
+
+
 class DevicePool:
     """All streams of one attention layer: arena + page tables + stats + staging.
 
@@ -215,15 +224,19 @@ class DevicePool:
     # -- gather (K1b) ------------------------------------------------------------------
     def gather(self, extra_tokens: int = 0):
         """Dequantised history of every stream as device k/v [S0 + extra, Hkv, Dp]
-        in the pool dtype (rows >= S0 left for the caller; evicted pages of
-        streaming streams unwritten).  One K1b launch."""
+        in the pool dtype (rows >= S0 left for the caller).  Rows of pages a
+        streaming stream has evicted are zero: K4 may load them inside a
+        key block whose other page is attended (P < 64), and a masked
+        column still meets its V row in the P.V product, where recycled
+        NaN bits would poison the output.  One K1b launch."""
         counts = set(self.tokens_host)
         if len(counts) != 1:
             raise ValueError(f"pools out of sync: token counts {sorted(counts)}")
         n0 = counts.pop()
         shape = (n0 + extra_tokens, self.n_streams, self.Dp)
-        k = torch.empty(shape, dtype=self.dtype, device=self.device)
-        v = torch.empty(shape, dtype=self.dtype, device=self.device)
+        alloc = torch.zeros if any(kd != _lib.SK_KIND_DENSE for kd in self.kinds) else torch.empty
+        k = alloc(shape, dtype=self.dtype, device=self.device)
+        v = alloc(shape, dtype=self.dtype, device=self.device)
         if n0:
             pool = self.abi()
             rc = _lib.load().sk_gather_pages(C.byref(pool), self.n_streams, n0, k.data_ptr(), v.data_ptr(), self.Dp,
@@ -260,16 +273,16 @@ class DevicePool:
                     lo = pad(zero)
                     const = (pad(scale) == 1.0) & (codes.max(axis=0) == 0)  # hi == lo -> scale forced to 1
                     hi = np.where(const, lo, lo + pad(scale) * levels)
-                    bounds += [lo.astype(np_dt), hi.astype(np_dt)]
+                    bounds += [_np_exact(lo, np_dt), _np_exact(hi, np_dt)]
                 raw = layout.encode_slot(kc, vc, *bounds, Dp, self.P, self.bits, np_dt, self.slot_bytes)
             else:
-                kc = np.pad(np.asarray(pg.k_codes[:t], np.float64), ((0, 0), (0, Dp - D))).astype(np_dt)
-                vc = np.pad(np.asarray(pg.v_codes[:t], np.float64), ((0, 0), (0, Dp - D))).astype(np_dt)
+                kc = _np_exact(np.pad(np.asarray(pg.k_codes[:t], np.float64), ((0, 0), (0, Dp - D))), np_dt)
+                vc = _np_exact(np.pad(np.asarray(pg.v_codes[:t], np.float64), ((0, 0), (0, Dp - D))), np_dt)
                 raw = layout.encode_slot(kc, vc, None, None, None, None, Dp, self.P, 0, np_dt, self.slot_bytes)
             slots.append(int(self.page_table_host[s, pg.page_id]))
             raws.append(raw)
             for jl, st in enumerate(pg.stats):
-                row = np.stack([pad(st.k_min), pad(st.k_max)]).astype(np_dt)
+                row = _np_exact(np.stack([pad(st.k_min), pad(st.k_max)]), np_dt)
                 stats[pg.page_id * lp + jl].copy_(torch.from_numpy(row))
         arena = self.arena.view(-1, self.slot_bytes)
         arena[torch.as_tensor(slots, device=self.device)] = torch.from_numpy(np.stack(raws)).to(self.device)
@@ -337,31 +350,69 @@ class DevicePool:
 
 
 class PageTable:
-    """cache.py:109-140 view: live page indices of one stream."""
+    """cache.py:109-140 -- token-order live pages with position -> (page_id,
+    slot) lookup.
 
-    def __init__(self, head: "HeadPages"):
-        self._head = head
-        self.page_size = head.page_size
+    ``PageTable(page_size)`` is the reference's stand-alone table (register /
+    evict / lookup over a dict).  A ``HeadPages`` owns a *view* table instead
+    (``PageTable(head)``): its live pages and token count are read from the
+    device stream, whose int32 page table (DevicePool.page_table) is what the
+    kernels use; register/evict on a view raise, since residency is decided
+    by K1's ring eviction (cache.py:253-261)."""
+
+    def __init__(self, page_size_or_head):
+        if isinstance(page_size_or_head, HeadPages):
+            self._head = page_size_or_head
+            self.page_size = self._head.page_size
+            self._live = None
+        else:
+            self._head = None
+            self.page_size = int(page_size_or_head)
+            self._live: dict = {}  # global page index -> page_id
+            self._num_tokens = 0
 
     @property
     def num_tokens(self) -> int:
-        return self._head.num_tokens
+        return self._head.num_tokens if self._head is not None else self._num_tokens
+
+    @num_tokens.setter
+    def num_tokens(self, n: int) -> None:
+        if self._head is not None:
+            raise AttributeError("a device-backed page table counts tokens from its stream")
+        self._num_tokens = int(n)
+
+    def register(self, page_index: int, page_id: int) -> None:
+        if self._head is not None:
+            raise TypeError("device-backed page tables are written by K1 appends, not register()")
+        self._live[page_index] = page_id
+
+    def evict(self, page_index: int) -> None:
+        if self._head is not None:
+            raise TypeError("device-backed page tables evict through K1's streaming ring, not evict()")
+        del self._live[page_index]
 
     @property
     def live_indices(self) -> list:
-        return self._head._live()
+        return self._head._live() if self._head is not None else sorted(self._live)
 
     @property
     def page_ids(self) -> list:
-        return self._head._live()
+        # device pages are identified by their global page index (page_id == index)
+        if self._head is not None:
+            return self._head._live()
+        return [self._live[i] for i in sorted(self._live)]
 
     def lookup(self, position: int):
         if not 0 <= position < self.num_tokens:
             raise IndexError(f"position {position} outside [0, {self.num_tokens})")
         index = position // self.page_size
-        if index not in set(self._head._live()):
+        if self._head is not None:
+            if index not in set(self._head._live()):
+                raise KeyError(f"position {position} falls in an evicted page")
+            return index, position % self.page_size
+        if index not in self._live:
             raise KeyError(f"position {position} falls in an evicted page")
-        return index, position % self.page_size
+        return self._live[index], position % self.page_size
 
 
 class HeadPages:

@@ -36,7 +36,29 @@ __device__ void append_page(const PoolView& pv, int s, int p, int n0, int n1, co
   const int D = pv.D, P = pv.P;
   const bool streaming = pv.kind[s] == SK_KIND_STREAMING;
   const int count = (n1 + P - 1) / P;
-  if (streaming && p >= pv.sink && p < count - pv.local) return;  // evicted by the end of this append
+  constexpr int vec = 8;  // 16-byte vectors
+  // The staging page holds the raw tokens of the stream's open page.  The
+  // CTA of the first touched page (p_open) is the only one that reads it;
+  // when the append ends in a different, partial page, that same CTA (not
+  // the last page's) writes the new tail into staging once its own read is
+  // done -- so no two CTAs of one launch touch staging unordered.
+  const int p_open = n0 / P, p_last = (n1 - 1) / P;
+  const bool tail_by_open = p == p_open && p_last != p_open && (n1 % P) != 0;
+  auto write_tail_from_src = [&]() {
+    T* wk = reinterpret_cast<T*>(pv.staging_ptr(s, 0));
+    T* wv = reinterpret_cast<T*>(pv.staging_ptr(s, 1));
+    const int tail0 = p_last * P;  // > n0: every tail token is new
+    for (int i = threadIdx.x; i < (n1 - tail0) * (D / vec); i += blockDim.x) {
+      const int tl = i / (D / vec), c = (i % (D / vec)) * vec;
+      const int64_t off = (int64_t)(tail0 + tl - n0) * src_ts + c;
+      *reinterpret_cast<uint4*>(wk + tl * D + c) = *reinterpret_cast<const uint4*>(src_k + off);
+      *reinterpret_cast<uint4*>(wv + tl * D + c) = *reinterpret_cast<const uint4*>(src_v + off);
+    }
+  };
+  if (streaming && p >= pv.sink && p < count - pv.local) {  // evicted by the end of this append
+    if (tail_by_open) write_tail_from_src();
+    return;
+  }
 
   const int t0 = p * P;
   const int t1 = min(t0 + P, n1);
@@ -50,7 +72,6 @@ __device__ void append_page(const PoolView& pv, int s, int p, int n0, int n1, co
   // 1. raw page -> smem (staging for positions < n0, new tokens otherwise)
   const T* stg_k = reinterpret_cast<const T*>(pv.staging_ptr(s, 0));
   const T* stg_v = reinterpret_cast<const T*>(pv.staging_ptr(s, 1));
-  constexpr int vec = 8;  // 16-byte vectors
   for (int i = threadIdx.x; i < ntok * (D / vec); i += blockDim.x) {
     int tl = i / (D / vec), c = (i % (D / vec)) * vec;
     int t = t0 + tl;
@@ -67,6 +88,7 @@ __device__ void append_page(const PoolView& pv, int s, int p, int n0, int n1, co
     *reinterpret_cast<uint4*>(rv + tl * D + c) = vv;
   }
   __syncthreads();
+  if (tail_by_open) write_tail_from_src();  // staging reads of this CTA are complete
 
   uint8_t* slot = pv.slot_ptr(s, p);
   uint8_t* kc = pv.k_codes(slot);
@@ -195,8 +217,9 @@ __device__ void append_page(const PoolView& pv, int s, int p, int n0, int n1, co
       st[D + c] = DT<T>::from_f(hi);
     }
   }
-  // 5. a partial page at the end keeps its raw tokens in staging
-  if (t1 == n1 && (n1 % P) != 0) {
+  // 5. a partial page at the end keeps its raw tokens in staging (written
+  //    here only when it is also the open page; otherwise by p_open's CTA)
+  if (t1 == n1 && (n1 % P) != 0 && p == p_open) {
     T* wk = reinterpret_cast<T*>(pv.staging_ptr(s, 0));
     T* wv = reinterpret_cast<T*>(pv.staging_ptr(s, 1));
     int first = max(n0, t0) - t0;

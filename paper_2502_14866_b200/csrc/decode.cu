@@ -72,6 +72,7 @@ struct DecodeParams {
   const void* v_new;
   int64_t new_ss;
   const uint32_t* row_mask;
+  const uint32_t* row_window;  // [stream][row] sink | local << 16 (pages), or NULL = the pool's window
   const int32_t* sel;
   const int32_t* sel_count;
   int sel_stride;
@@ -80,8 +81,15 @@ struct DecodeParams {
   void* out;
   int64_t out_ss, out_rs;
   int out_dtype;
-  int dbg;  // ablation switch (SK_DEC_DEBUG=3: skip the pages, keep every barrier and the merge)
 };
+
+// Ablation build (tools/decode_probe.py, never the shipped library):
+// -DSK_DEC_ABLATE_PAGES skips the page work, keeping every barrier and the merge.
+#ifdef SK_DEC_ABLATE_PAGES
+constexpr bool kAblatePages = true;
+#else
+constexpr bool kAblatePages = false;
+#endif
 
 // m16n8k16 MMA, fp32 accumulate.
 template <typename MT>
@@ -476,6 +484,9 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   // ---- round trip 1: header, selection, q (all independent) -----------------
   const int n_tok = prm.tokens[s];
   const uint32_t rm_raw = prm.row_mask[s];
+  // per-row streaming windows (HeadProfile.sink_blocks / local_blocks, engine.py:264-267)
+  uint32_t win = (uint32_t)pv.sink | ((uint32_t)pv.local << 16);
+  if (prm.row_window != nullptr && lane < G) win = __ldg(prm.row_window + (int64_t)s * G + lane);
   const int cnt_raw = prm.sel_count[s];
   const int32_t* sel = prm.sel + (int64_t)s * prm.sel_stride;
   const int sel_w = min(prm.sel_stride, kMaxSel);
@@ -506,7 +517,22 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   const uint32_t rmask = rm_raw & gmask;
   const uint32_t smask = gmask & ~rmask;
   const int nsel = rmask ? min(cnt_raw, sel_w) : 0;
-  const int sink_end = min(pv.sink, n_pages), local_start = max(n_pages - pv.local, 0);
+  // lane r (< G) holds row r's window; the union over streaming rows is
+  // [0, max sink) u [n - max local, n), and each page carries the mask of the
+  // streaming rows whose own window contains it
+  const bool srow = lane < G && ((smask >> lane) & 1u);
+  const int my_sink = srow ? min((int)(win & 0xFFFFu), n_pages) : 0;
+  const int my_loc = srow ? max(n_pages - (int)(win >> 16), 0) : n_pages;
+  int sink_end = my_sink, local_start = my_loc;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    sink_end = max(sink_end, __shfl_xor_sync(0xffffffffu, sink_end, off));
+    local_start = min(local_start, __shfl_xor_sync(0xffffffffu, local_start, off));
+  }
+  // streaming rows attending page pg (warp-uniform pg)
+  auto win_rows = [&](int pg) -> uint32_t {
+    return __ballot_sync(0xffffffffu, srow && (pg < my_sink || pg >= my_loc));
+  };
   __syncthreads();
   // ---- the stream's page union: selection + sink/local pages it lacks.  Each
   //      warp derives it itself (a ballot over <= 32 candidates against the
@@ -528,7 +554,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     ne = min(ne, kMaxExtra);
   }
   __syncwarp();
-  const int U = prm.dbg == 3 ? 0 : nsel + ne;
+  const int U = kAblatePages ? 0 : nsel + ne;
 
   // ---- this warp's pages: unit u = rank + kCl * (warp + kWarps * i) -----------
   RowState<D> st;
@@ -546,13 +572,9 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   constexpr int RBY = KIND == 0 ? 2 * D : (KIND == 1 ? D / 2 : D);
   constexpr int kSlotUsed = 2 * P * RBY + (KIND == 0 ? 0 : 8 * D);  // bytes of a slot the kernel reads
   auto unit_page = [&](int u, uint32_t& um) -> int {
-    if (u < nsel) {
-      const int pg = s_sel[u];
-      um = rmask | ((smask && (pg < sink_end || pg >= local_start)) ? smask : 0u);
-      return pg;
-    }
-    um = smask;
-    return w_extra[u - nsel];
+    const int pg = u < nsel ? s_sel[u] : w_extra[u - nsel];
+    um = (u < nsel ? rmask : 0u) | (smask ? win_rows(pg) : 0u);
+    return pg;
   };
   // software pipeline across a warp's pages: the next page's table entry is
   // loaded and its bytes prefetched into L2 while the current page computes
@@ -722,29 +744,17 @@ int launch_kind(const DecodeParams& prm, int n_streams, cudaStream_t st) {
 }  // namespace
 }  // namespace sk
 
-extern "C" int64_t sk_decode_workspace(int32_t n_streams, int32_t group_rows, int32_t head_dim, int32_t max_splits) {
-  (void)n_streams;
-  (void)group_rows;
-  (void)head_dim;
-  (void)max_splits;
-  return 256;  // the cluster merge needs no global workspace
-}
-
 extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
                               int64_t q_stream_stride, int64_t q_row_stride, const void* k_new, const void* v_new,
-                              int64_t new_stream_stride, const uint32_t* row_mask, const int32_t* sel,
-                              const int32_t* sel_count, int32_t sel_stride, int32_t* tokens, float softmax_scale,
-                              void* out, int64_t out_stream_stride, int64_t out_row_stride, int32_t out_dtype,
-                              int32_t pages_per_split, int32_t max_splits, int32_t fuse_append, void* workspace,
-                              int64_t workspace_bytes, void* stream) {
+                              int64_t new_stream_stride, const uint32_t* row_mask, const uint32_t* row_window,
+                              const int32_t* sel, const int32_t* sel_count, int32_t sel_stride, int32_t* tokens,
+                              float softmax_scale, void* out, int64_t out_stream_stride, int64_t out_row_stride,
+                              int32_t out_dtype, int32_t append_new, void* stream) {
   using namespace sk;
   int rc = check_pool(pool);
   if (rc) return rc;
-  (void)workspace;
-  (void)workspace_bytes;
   SK_CHECK_ARG(n_streams >= 1 && n_streams <= 65535, "decode: stream count must be in [1, 65535]");
   SK_CHECK_ARG(group_rows >= 1 && group_rows <= kMaxRows, "decode: group size must be in [1, 8]");
-  SK_CHECK_ARG(pages_per_split >= 1 && max_splits >= 1, "decode: bad split geometry");
   SK_CHECK_ARG(sel_stride >= 1 && sel_stride <= kMaxSel, "decode: selection width must be in [1, 2048]");
   SK_CHECK_ARG(pool->sink + pool->local <= kMaxExtra, "decode: sink + local window too large");
   SK_CHECK_ARG(out_dtype == SK_F16 || out_dtype == SK_BF16 || out_dtype == SK_F32, "decode: bad out dtype");
@@ -762,6 +772,7 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   prm.v_new = v_new;
   prm.new_ss = new_stream_stride;
   prm.row_mask = row_mask;
+  prm.row_window = row_window;
   prm.sel = sel;
   prm.sel_count = sel_count;
   prm.sel_stride = sel_stride;
@@ -771,7 +782,6 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   prm.out_ss = out_stream_stride;
   prm.out_rs = out_row_stride;
   prm.out_dtype = out_dtype;
-  prm.dbg = getenv("SK_DEC_DEBUG") ? atoi(getenv("SK_DEC_DEBUG")) : 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int kind = pool->bits == 0 ? 0 : (pool->bits <= 4 ? 1 : 2);
   int rc2;
@@ -783,7 +793,7 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
                     : (kind == 1 ? launch_kind<__nv_bfloat16, 1>(prm, n_streams, st)
                                  : launch_kind<__nv_bfloat16, 2>(prm, n_streams, st));
   }
-  if (rc2 != SK_OK || !fuse_append) return rc2;
+  if (rc2 != SK_OK || !append_new) return rc2;
   // the new token is appended by K1's one-token kernel right behind the
   // attention (stream order: every read of its page has completed)
   return append_launch(pool, n_streams, k_new, v_new, new_stream_stride, 0, tokens, 1, 1, st);

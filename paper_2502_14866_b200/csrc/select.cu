@@ -723,9 +723,12 @@ int select_dispatch(const PoolView& pv, int n_streams, const void* q, int64_t q_
   const int ppc = kScoreWarps * kBatchesPerWarp * pps;  // pages per CTA
   dim3 grid((max_pages + ppc - 1) / ppc, n_streams);
   const T* qt = static_cast<const T*>(q);
-  // ablation switch for timing the phases (tools/decode_probe.py): 1 no scoring, 2 no top-k,
-  // 3 neither, 4 copies without scoring
-  const int dbg = getenv("SK_SEL_DEBUG") ? atoi(getenv("SK_SEL_DEBUG")) : 0;
+  // ablation builds for timing the phases (tools/decode_probe.py; never the shipped library):
+  // -DSK_SEL_ABLATE=1 no scoring, 2 no top-k, 3 neither, 4 copies without scoring
+#ifndef SK_SEL_ABLATE
+#define SK_SEL_ABLATE 0
+#endif
+  const int dbg = SK_SEL_ABLATE;
 #define SK_SEL(LPV)                                                                                          \
   do {                                                                                                       \
     cudaFuncSetAttribute(select_kernel<T, LPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
@@ -747,8 +750,10 @@ int select_dispatch(const PoolView& pv, int n_streams, const void* q, int64_t q_
 }  // namespace
 }  // namespace sk
 
+extern "C" int64_t sk_select_scores_offset(int32_t n_streams) { return ((int64_t)n_streams * 4 + 255) / 256 * 256; }
+
 extern "C" int64_t sk_select_workspace(int32_t n_streams, int32_t max_pages) {
-  return (int64_t)n_streams * max_pages * 8 + (int64_t)n_streams * 4 + 256;  // scores + tickets
+  return sk_select_scores_offset(n_streams) + (int64_t)n_streams * max_pages * 8;  // tickets + scores
 }
 
 extern "C" int sk_select_pages(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
@@ -769,8 +774,10 @@ extern "C" int sk_select_pages(const sk_pool* pool, int32_t n_streams, int32_t g
   SK_CHECK_ARG(q && row_mask && tokens && sel_out && sel_count && workspace, "select: NULL pointer");
   SK_CHECK_ARG(reinterpret_cast<uintptr_t>(pool->stats) % 16 == 0, "select: stats must be 16-byte aligned");
   PoolView pv = make_view(*pool);
-  double* scores = static_cast<double*>(workspace);
-  uint32_t* ticket = reinterpret_cast<uint32_t*>(scores + (int64_t)n_streams * max_pages_hint);
+  // workspace = [tickets: n_streams x u32, padded to 256 B][scores: n_streams x max_pages_hint f64]; the
+  // tickets sit at a fixed offset so one zeroed buffer serves any max_pages_hint it is large enough for
+  uint32_t* ticket = static_cast<uint32_t*>(workspace);
+  double* scores = reinterpret_cast<double*>(static_cast<uint8_t*>(workspace) + sk_select_scores_offset(n_streams));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (pool->dtype == SK_F16)
     return select_dispatch<__half>(pv, n_streams, q, q_stream_stride, q_row_stride, row_mask, tokens, invoke,

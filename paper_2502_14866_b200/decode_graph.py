@@ -37,18 +37,26 @@ class DecodeGraph:
         self.head_dim = head_dim
         self.record_ledger = record_ledger
         pools = [e.cache.pool for e in engines]
-        tok = pools[0].tokens_host[0]
+        # streams may hold different token counts (a ragged batch: per-sequence
+        # page tables); every layer must hold the same counts stream by stream
+        start = list(pools[0].tokens_host)
         for p in pools:
-            if set(p.tokens_host) != {tok}:
-                raise ValueError("all layers must hold the same token count")
+            if list(p.tokens_host) != start:
+                raise ValueError("all layers must hold the same token counts, stream by stream")
+        tok = max(start)
+        for p in pools:
             p.reserve(tok + max_steps + 1)
         self.pools = pools
+        for e in engines:  # a streaming pool never holds more than its own window
+            if getattr(e, "_row_window", None) is not None and hasattr(e, "_check_windows"):
+                e._check_windows(-(-(tok + max_steps) // e.config.physical_page))
         self.g = e0._group_size
         self.h_kv = pools[0].n_streams
         self.h = self.h_kv * self.g
         self.dp = pools[0].Dp
         self.dtype = pools[0].dtype
         self.start_tokens = tok
+        self.start_per_stream = start
         self.steps_done = 0
         self.max_steps = max_steps
         cfg = self.cfg
@@ -63,11 +71,6 @@ class DecodeGraph:
         width = max(4, self.k_pages)
         self.sel = [torch.zeros((self.h_kv, width), dtype=torch.int32, device=self.dev) for _ in engines]
         self.cnt = [torch.zeros(self.h_kv, dtype=torch.int32, device=self.dev) for _ in engines]
-        units = max(selection_size(self.max_pages_hint, self.k_pages), 1) + cfg.sink_blocks + cfg.local_blocks
-        self.pps = max(1, 128 // cfg.physical_page)  # 8 warps x 16-token tiles per CTA
-        self.max_splits = -(-units // self.pps)
-        need = _lib.load().sk_decode_workspace(self.h_kv, self.g, self.dp, self.max_splits)
-        self.dec_ws = [torch.zeros(need, dtype=torch.uint8, device=self.dev) for _ in engines]
         self.sel_ws = [torch.zeros(_lib.load().sk_select_workspace(self.h_kv, self.max_pages_hint),
                                    dtype=torch.uint8, device=self.dev) for _ in engines]
         self.graphs = {}
@@ -89,13 +92,12 @@ class DecodeGraph:
                                      self.max_pages_hint, self.sel[li].data_ptr(), self.cnt[li].data_ptr(),
                                      self.sel[li].shape[1], ws.data_ptr(), ws.numel(), stream)
             _lib.check(rc)
-        ws = self.dec_ws[li]
         rc = lib.sk_decode_attn(C.byref(abi), self.h_kv, self.g, self.q[li].data_ptr(), self.g * self.dp, self.dp,
                                 self.k[li].data_ptr(), self.v[li].data_ptr(), self.dp, e._row_mask.data_ptr(),
-                                self.sel[li].data_ptr(), self.cnt[li].data_ptr(), self.sel[li].shape[1],
-                                pool.tokens.data_ptr(), C.c_float(1.0 / math.sqrt(self.head_dim)),
-                                self.out[li].data_ptr(), self.g * self.dp, self.dp, _device.sk_dtype(self.dtype),
-                                self.pps, self.max_splits, 0, ws.data_ptr(), ws.numel(), stream)
+                                e.row_window_ptr(), self.sel[li].data_ptr(), self.cnt[li].data_ptr(),
+                                self.sel[li].shape[1], pool.tokens.data_ptr(),
+                                C.c_float(1.0 / math.sqrt(self.head_dim)), self.out[li].data_ptr(),
+                                self.g * self.dp, self.dp, _device.sk_dtype(self.dtype), 0, stream)
         _lib.check(rc)
         # K1 one-token append on a side stream: overlaps the next layer's attention
         side.wait_stream(main)
@@ -139,12 +141,13 @@ class DecodeGraph:
         self.graphs[select].replay()
         n_tok = self.start_tokens + self.steps_done
         n_pages = -(-n_tok // cfg.physical_page)
+        pages_of = [-(-(t + self.steps_done) // cfg.physical_page) for t in self.start_per_stream]
         for e, pool in zip(self.engines, self.pools):
             if select:
                 from .selector import SelectionState
-                size = selection_size(n_pages, self.k_pages)
                 for kv in e.cache.dense_pool:
                     if e._row_mask_host[kv]:
+                        size = selection_size(pages_of[kv], self.k_pages)
                         e.selection_states[kv] = SelectionState(_Sized(size), step, cfg.reuse_interval,
                                                                 cfg.budget_tokens)
                         e.ledger.record_selector(kv)

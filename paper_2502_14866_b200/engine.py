@@ -176,7 +176,6 @@ class Engine:
         self._group_size: int | None = None
         self._dtype, self._device_arg, self._capacity = dtype, device, capacity_tokens
         self._plans: dict = {}
-        self._dec_ws = None
         self._sel = None
 
     # -- helpers ----------------------------------------------------------------
@@ -222,8 +221,38 @@ class Engine:
         if getattr(self, "_row_mask_host", None) != masks:
             self._row_mask = _device.h2d(np.array(masks, np.int32), self.device)
         self._row_mask_host = masks
+        # per-row streaming windows for K3, only when a profile differs from the pool's
+        wins = [[self._window_of(h) for h in self._group_heads(kv)] for kv in range(num_kv_heads)]
+        pool_win = cfg.sink_blocks | (cfg.local_blocks << 16)
+        if all(w == pool_win for row in wins for w in row):
+            self._row_window = None
+        else:
+            self._row_window = _device.h2d(np.array(wins, np.uint32), self.device)
         self._sel = None
         self.selection_states = {}
+
+    def _window_of(self, h: int) -> int:
+        """sink | local << 16 of streaming head h (retrieval rows: the pool's)."""
+        p, cfg = self.profiles[h], self.config
+        if p.role == RETRIEVAL:
+            return cfg.sink_blocks | (cfg.local_blocks << 16)
+        return p.sink_blocks | (p.local_blocks << 16)
+
+    def _check_windows(self, n_pages: int) -> None:
+        """A streaming-pool KV head keeps only the pool's sink + local pages
+        (cache.py:253-261); a profile asking for more reads an evicted page,
+        which the reference refuses (page_at -> KeyError)."""
+        cfg, g = self.config, self._group_size
+        for kv in self.cache.streaming_pool:
+            for h in self._group_heads(kv):
+                p = self.profiles[h]
+                want = {t for a, b in lambda_segments(n_pages, p.sink_blocks, p.local_blocks, n_pages - 1)
+                        for t in range(a, b)}
+                live = set(self.cache.pool.live_indices(self.cache.stream_of[kv]))
+                missing = sorted(want - live)
+                if missing:
+                    raise KeyError(f"page index {missing[0]} is not resident: head {h}'s window "
+                                   f"({p.sink_blocks}, {p.local_blocks}) reaches evicted pages of KV head {kv}")
 
     def _plan(self, n: int, s: int):
         cfg = self.config
@@ -351,12 +380,6 @@ class Engine:
         self.cache.append_all(k, v)
 
     # -- decode -------------------------------------------------------------------
-    def _decode_workspace(self, n_streams: int, max_splits: int, dp: int) -> torch.Tensor:
-        need = _lib.load().sk_decode_workspace(n_streams, self._group_size, dp, max_splits)
-        if self._dec_ws is None or self._dec_ws.numel() < need:
-            self._dec_ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
-        return self._dec_ws
-
     def decode_step(self, q_new, k_new, v_new) -> DecodeResult:
         """engine.py:208-286."""
         if self.cache is None or self.cache.pool is None or self.cache.num_tokens == 0:
@@ -374,6 +397,10 @@ class Engine:
         out = self.decode_device(q, kn, vn, d)
         np_dt = None if _device.is_torch(q_new) else np.asarray(q_new).dtype
         return DecodeResult(_device.to_output(out[:, :d], q_new, np_dt), self._last_tables, self._last_invoked)
+
+    def row_window_ptr(self):
+        w = getattr(self, "_row_window", None)
+        return None if w is None else w.data_ptr()
 
     def decode_device(self, q: torch.Tensor, kn: torch.Tensor, vn: torch.Tensor, head_dim: int) -> torch.Tensor:
         """Device fast path: q [H,Dp], kn/vn [Hkv,Dp] in the pool dtype."""
@@ -421,18 +448,15 @@ class Engine:
         pool.reserve(n_tok + 1)
         sel, cnt = self._sel if self._sel is not None else (
             torch.zeros((h_kv, 4), dtype=torch.int32, device=dev), torch.zeros(h_kv, dtype=torch.int32, device=dev))
-        units = max(selection_size(n_pages, k_pages), 1) + cfg.sink_blocks + cfg.local_blocks
-        pps = max(1, 128 // cfg.physical_page)  # 8 warps x 16-token tiles per CTA
-        max_splits = -(-units // pps)
-        ws = self._decode_workspace(h_kv, max_splits, pool.Dp)
+        if self._row_window is not None:
+            self._check_windows(n_pages)
         out = torch.empty((h_kv * g, pool.Dp), dtype=self._dtype, device=dev)
         abi = pool.abi()
         rc = _lib.load().sk_decode_attn(
             C.byref(abi), h_kv, g, q.data_ptr(), g * pool.Dp, pool.Dp, kn.data_ptr(), vn.data_ptr(), pool.Dp,
-            self._row_mask.data_ptr(), sel.data_ptr(), cnt.data_ptr(), sel.shape[1], pool.tokens.data_ptr(),
-            C.c_float(1.0 / math.sqrt(head_dim)), out.data_ptr(), g * pool.Dp, pool.Dp,
-            _device.sk_dtype(self._dtype), pps, max_splits, 1, ws.data_ptr(), ws.numel(),
-            _device.stream_ptr(dev))
+            self._row_mask.data_ptr(), self.row_window_ptr(), sel.data_ptr(), cnt.data_ptr(), sel.shape[1],
+            pool.tokens.data_ptr(), C.c_float(1.0 / math.sqrt(head_dim)), out.data_ptr(), g * pool.Dp, pool.Dp,
+            _device.sk_dtype(self._dtype), 1, _device.stream_ptr(dev))
         _lib.check(rc)
         for s in range(h_kv):
             pool.tokens_host[s] += 1

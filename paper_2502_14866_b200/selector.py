@@ -49,19 +49,34 @@ def selection_size(num_pages: int, budget_pages: int) -> int:
 
 
 class _Workspace:
-    """Per-device select workspace; its tickets must start at zero."""
+    """Per-(device, stream count) select workspace, grown geometrically.  Its
+    tickets sit at a fixed offset (sk_select_workspace) and start at zero;
+    the kernel re-arms them, so a larger page count only ever reallocates
+    when it outgrows the buffer."""
 
     _by_dev: dict = {}
 
     @classmethod
     def get(cls, device, n_streams: int, max_pages: int) -> torch.Tensor:
-        need = _lib.load().sk_select_workspace(n_streams, max_pages)
-        key = (str(device), n_streams, max_pages)
+        lib = _lib.load()
+        need = lib.sk_select_workspace(n_streams, max_pages)
+        key = (str(device), n_streams)
         ws = cls._by_dev.get(key)
         if ws is None or ws.numel() < need:
-            ws = torch.zeros(need, dtype=torch.uint8, device=device)
+            pages = max_pages if ws is None else max(max_pages, 2 * cls._pages(ws, n_streams))
+            ws = torch.zeros(lib.sk_select_workspace(n_streams, pages), dtype=torch.uint8, device=device)
             cls._by_dev[key] = ws
         return ws
+
+    @staticmethod
+    def _pages(ws: torch.Tensor, n_streams: int) -> int:
+        return (ws.numel() - _lib.load().sk_select_scores_offset(n_streams)) // (8 * n_streams)
+
+    @staticmethod
+    def scores(ws: torch.Tensor, n_streams: int, max_pages: int) -> torch.Tensor:
+        """f64 [n_streams, max_pages] page scores of the last launch on ws."""
+        off = _lib.load().sk_select_scores_offset(n_streams)
+        return ws[off:off + 8 * n_streams * max_pages].view(torch.float64).view(n_streams, max_pages)
 
 
 def select_streams(pool: DevicePool, q: torch.Tensor, q_stream_stride: int, q_row_stride: int, group_rows: int,
@@ -98,7 +113,7 @@ def _pool_for_pages(pages: Sequence[PhysicalPage], page_size: int, device) -> De
             s = p.stats[min(j, len(p.stats) - 1)]
             host[i * lp + j, 0, :dim] = s.k_min
             host[i * lp + j, 1, :dim] = s.k_max
-    pool.stats[0, :host.shape[0]] = torch.from_numpy(host).to(device=pool.device, dtype=pool.dtype)
+    pool.stats[0, :host.shape[0]] = _device.exact_cast(torch.from_numpy(host).to(pool.device), pool.dtype)
     pool.tokens_host[0] = len(pages) * page_size
     pool.tokens.fill_(len(pages) * page_size)
     return pool
@@ -156,7 +171,36 @@ def score_pages(q_group, pages: Sequence[PhysicalPage], *, device=None) -> np.nd
     padded = pages + [pages[0]] * max(0, 5 - n)  # K2 scores only when |pins| < K < n
     out, cnt, ws = _run_select(q_group, padded, 4, pages[0].capacity, device)
     torch.cuda.current_stream().synchronize()
-    return ws[:8 * len(padded)].view(torch.float64)[:n].cpu().numpy().copy()
+    return _Workspace.scores(ws, 1, len(padded))[0, :n].cpu().numpy().copy()
+
+
+def exact_top_k_pages(q_group, keys, budget_tokens: int, page_size: int, *, device=None) -> list:
+    """selector.py:160-189 -- brute-force oracle: pages ranked by their best
+    exact token score (fp64 q.k of every stored key, max over the group rows
+    and the page), with the selector's pins and tie rule.  Runs on the device
+    (fp64 matmul); used to measure selection recall, not on the decode path."""
+    if budget_tokens < page_size:
+        raise ValueError(f"budget {budget_tokens} is below one page ({page_size} tokens)")
+    dev = _device.device_of(device)
+    as_t = lambda x: (x.detach() if _device.is_torch(x) else torch.from_numpy(np.asarray(x, np.float64)))  # noqa: E731
+    q = as_t(q_group).to(dev, torch.float64)
+    if q.ndim == 1:
+        q = q[None, :]
+    k = as_t(keys).to(dev, torch.float64)
+    num_pages = -(-k.shape[0] // page_size)
+    kp = -(-budget_tokens // page_size)
+    if kp >= num_pages:
+        return list(range(num_pages))
+    tok = (q @ k.T).amax(0)
+    pad = num_pages * page_size - k.shape[0]
+    if pad:
+        tok = torch.cat([tok, tok.new_full((pad,), -float("inf"))])
+    page_scores = tok.view(num_pages, page_size).amax(1).cpu().numpy()
+    pins = pinned_pages(num_pages)
+    free = max(kp - len(pins), 0)
+    cand = [i for i in range(num_pages) if i not in set(pins)]
+    cand.sort(key=lambda i: (-page_scores[i], i))
+    return sorted(set(pins) | set(cand[:free]))
 
 
 @dataclass

@@ -41,7 +41,9 @@ def test_pure_host_entry_points(lib):
     assert L.sk_slot_bytes(128, 64, 4, 0) == 9216          # KV4 page: 8 KB codes + 1 KB bounds
     assert L.sk_slot_bytes(128, 64, 0, 0) == 32768         # fp16 page
     assert L.sk_select_workspace(8, 2048) >= 8 * 2048 * 8
-    assert L.sk_decode_workspace(8, 4, 128, 18) > 0
+    off = L.sk_select_scores_offset(8)
+    assert off >= 8 * 4 and off % 256 == 0                 # tickets first, scores 256-B aligned after them
+    assert L.sk_select_workspace(8, 2048) == off + 8 * 2048 * 8
 
 
 def test_sass_contains_tcgen05_and_tma(lib):

@@ -116,12 +116,13 @@ def test_decode_shapes_against_oracle(case):
     assert eng.ledger.tiles == ref.tally.tiles
 
 
-def test_decode_128k_selection_and_outputs():
-    """BASELINE cfg2 geometry for one layer (32/8/128, 128k tokens, budget
-    4096, reuse 4, KV4, balanced gates): 5 decode steps (two selection
-    steps) -- every index table bit-exact, outputs within tolerance."""
+@pytest.mark.parametrize("s,steps", [(131072, 5), (262144, 5)])
+def test_decode_128k_selection_and_outputs(s, steps):
+    """BASELINE cfg2 / cfg3 geometry for one layer (32/8/128, 128k and 256k
+    tokens, budget 4096, reuse 4, KV4, balanced gates): 5 decode steps (two
+    selection steps) -- every index table bit-exact, outputs within tolerance."""
     rng = np.random.default_rng(128)
-    s, h, h_kv, d = 131072, 32, 8, 128
+    h, h_kv, d = 32, 8, 128
     gates = [0.9 - 0.001 * i if i % 4 < 2 else 0.1 + 0.001 * i for i in range(h)]
     k, v = fp16_vals(rng, s, h_kv, d), fp16_vals(rng, s, h_kv, d)
     cfg = sk.EngineConfig(quant_bits=4, budget_tokens=4096, reuse_interval=4, local_blocks=4)
@@ -130,7 +131,8 @@ def test_decode_128k_selection_and_outputs():
     ref = O.OracleEngine(O.Config(quant_bits=4, budget_tokens=4096, reuse_interval=4, local_blocks=4),
                          O.assign_roles(gates, 0.5, 1, 4))
     ref.load_context(k, v)
-    for t in range(5):
+    del k, v
+    for t in range(steps):
         qn, kn, vn = fp16_vals(rng, h, d), fp16_vals(rng, h_kv, d), fp16_vals(rng, h_kv, d)
         res = eng.decode_step(qn, kn, vn)
         rr = ref.decode_step(qn, kn, vn)
@@ -261,3 +263,22 @@ def test_topk_paths_against_oracle(n, ties):
             continue
         got = sk.select_pages(q, ours_pages, k * 64, 64)
         assert got == O.top_pages(q, ref_pages, k * 64, 64), (n, k, ties)
+
+
+def test_inexact_wide_inputs_are_refused_not_rounded():
+    """fp32/fp64 values the device dtype cannot hold would give page stats and
+    selections that silently differ from the reference's; the boundary refuses
+    them unless rounding is explicitly allowed."""
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((64, 16))  # fp64, not fp16-exact
+    head = sk.cache.HeadPages(0, 64, 16, 4, True)
+    with pytest.raises(ValueError, match="not exactly representable"):
+        head.append(x, x)
+    with pytest.raises(ValueError, match="not exactly representable"):
+        sk.quantize_page(x, 4)
+    with sk._device.rounding_allowed():
+        codes, _, _ = sk.quantize_page(x, 4)
+    assert codes.max() <= 15
+    x16 = x.astype(np.float16).astype(np.float64)  # exact in fp16: accepted as is
+    head.append(x16, x16)
+    assert head.num_tokens == 64

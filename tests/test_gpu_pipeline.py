@@ -73,9 +73,9 @@ def test_reprefill_recycles_pool_like_a_fresh_engine():
                 np.testing.assert_array_equal(x.k_codes, y.k_codes)
                 np.testing.assert_array_equal(x.v_codes, y.v_codes)
                 assert len(x.stats) == len(y.stats)
-        qn = rng.standard_normal((h, d)).astype(np.float32)
-        kn = rng.standard_normal((hkv, d)).astype(np.float32)
-        vn = rng.standard_normal((hkv, d)).astype(np.float32)
+        qn = rng.standard_normal((h, d)).astype(np.float16).astype(np.float32)
+        kn = rng.standard_normal((hkv, d)).astype(np.float16).astype(np.float32)
+        vn = rng.standard_normal((hkv, d)).astype(np.float16).astype(np.float32)
         ra, rb = reused.decode_step(qn, kn, vn), fresh.decode_step(qn, kn, vn)
         assert [t.positions for t in ra.index_tables] == [t.positions for t in rb.index_tables]
         np.testing.assert_array_equal(ra.output, rb.output)

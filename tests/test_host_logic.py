@@ -103,3 +103,45 @@ def test_block_iterator_semantics():
         sk.BlockIterator(((5, 7), (6, 9)))
     with pytest.raises(ValueError):
         sk.BlockIterator(((3, 3),))
+
+
+def test_load_gates_reads_per_layer_arrays(tmp_path):
+    """heads.py:128-136: one layer of a JSON array of per-layer gate arrays."""
+    import json
+
+    import paper_2502_14866_b200 as sk
+    path = tmp_path / "gates.json"
+    path.write_text(json.dumps([[0.9, 0.1, 0.3], [0.5, 0.4, 1], [0, 0.25, 0.75]]))
+    assert sk.load_gates(path) == [0.9, 0.1, 0.3]
+    assert sk.load_gates(str(path), 1) == [0.5, 0.4, 1.0]
+    assert all(isinstance(g, float) for g in sk.load_gates(path, 2))
+    with pytest.raises(ValueError, match="outside"):
+        sk.load_gates(path, 3)
+    with pytest.raises(ValueError, match="outside"):
+        sk.load_gates(path, -1)
+    bad = tmp_path / "bad.json"
+    for doc in ([], {"layers": []}):
+        bad.write_text(json.dumps(doc))
+        with pytest.raises(ValueError, match="non-empty JSON array"):
+            sk.load_gates(bad)
+    # the profiles of a loaded layer, like the reference's per-layer oracle (SURVEY 8b)
+    prof = sk.classify_heads(sk.load_gates(path, 2), 0.5, 1, 4)
+    assert [p.role for p in prof] == [sk.STREAMING, sk.RETRIEVAL, sk.RETRIEVAL]
+
+
+def test_page_table_standalone_api():
+    """cache.py:109-140: PageTable(page_size) with register / evict / lookup."""
+    import paper_2502_14866_b200 as sk
+    t = sk.PageTable(64)
+    t.register(0, 10)
+    t.register(2, 12)
+    t.register(1, 11)
+    t.num_tokens = 150
+    assert t.live_indices == [0, 1, 2] and t.page_ids == [10, 11, 12]
+    assert t.lookup(0) == (10, 0) and t.lookup(130) == (12, 2)
+    t.evict(1)
+    with pytest.raises(KeyError, match="evicted"):
+        t.lookup(64)
+    with pytest.raises(IndexError, match="outside"):
+        t.lookup(150)
+    assert t.page_ids == [10, 12]

@@ -77,18 +77,14 @@ for name, gates in [("balanced", [0.9 - 0.001 * h if h % 4 < 2 else 0.1 + 0.001 
         _lib.check(rc)
 
     print(name, "select us", round(time_it(sel_call), 2))
-    for pps in (2,):
-        for fuse in (0, 1):
-            units = 64 + 5
-            ms = -(-units // pps)
-            wsd = torch.zeros(lib.sk_decode_workspace(HKV, g, D, ms), dtype=torch.uint8, device="cuda")
-            out = torch.empty((H, D), dtype=torch.float16, device="cuda")
+    for fuse in (0, 1):
+        out = torch.empty((H, D), dtype=torch.float16, device="cuda")
 
-            def dec_call():
-                rc = lib.sk_decode_attn(C.byref(abi), HKV, g, q.data_ptr(), g * D, D, kn.data_ptr(), kn.data_ptr(), D,
-                                        e._row_mask.data_ptr(), sel.data_ptr(), cnt.data_ptr(), kp,
-                                        pool.tokens.data_ptr(), C.c_float(1 / math.sqrt(D)), out.data_ptr(), g * D, D,
-                                        _lib.SK_F16, pps, ms, fuse, wsd.data_ptr(), wsd.numel(), torch.cuda.current_stream().cuda_stream)
-                _lib.check(rc)
+        def dec_call():
+            rc = lib.sk_decode_attn(C.byref(abi), HKV, g, q.data_ptr(), g * D, D, kn.data_ptr(), kn.data_ptr(), D,
+                                    e._row_mask.data_ptr(), None, sel.data_ptr(), cnt.data_ptr(), kp,
+                                    pool.tokens.data_ptr(), C.c_float(1 / math.sqrt(D)), out.data_ptr(), g * D, D,
+                                    _lib.SK_F16, fuse, torch.cuda.current_stream().cuda_stream)
+            _lib.check(rc)
 
-            print(name, f"decode pps={pps} splits={ms} fuse={fuse} us", round(time_it(dec_call), 2))
+        print(name, f"decode append={fuse} us", round(time_it(dec_call), 2))
