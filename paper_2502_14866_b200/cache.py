@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import json
+import weakref
 from dataclasses import dataclass, field
 from typing import IO, Iterable
 
@@ -74,6 +75,23 @@ class PhysicalPage:
 
 def dequantize_page(page: PhysicalPage):
     return page.dequantize()
+
+
+# PhysicalPage snapshot -> (DevicePool, stream) it was read from, kept OUTSIDE
+# the record so page.__dict__ holds exactly the reference's fields (callers
+# rebuild pages with PhysicalPage(**page.__dict__), test_selector.py:62).
+_ORIGIN: dict = {}
+
+
+def _set_origin(page: PhysicalPage, pool, stream: int) -> None:
+    key = id(page)
+    _ORIGIN[key] = (pool, stream)
+    weakref.finalize(page, _ORIGIN.pop, key, None)
+
+
+def page_origin(page):
+    """(DevicePool, stream) a snapshot page came from, or None."""
+    return _ORIGIN.get(id(page))
 
 
 # ---------------------------------------------------------------------------
@@ -272,8 +290,14 @@ class DevicePool:
                 for scale, zero, codes in ((pg.k_scale, pg.k_zero, kc), (pg.v_scale, pg.v_zero, vc)):
                     lo = pad(zero)
                     const = (pad(scale) == 1.0) & (codes.max(axis=0) == 0)  # hi == lo -> scale forced to 1
-                    hi = np.where(const, lo, lo + pad(scale) * levels)
-                    bounds += [_np_exact(lo, np_dt), _np_exact(hi, np_dt)]
+                    hi = np.where(const, lo, lo + pad(scale) * levels).astype(np_dt)  # nearest: undoes the /levels
+                    lo16 = _np_exact(lo, np_dt)
+                    # the restored bounds must reproduce the snapshot's scale exactly (cache.py:44-46)
+                    sc = (hi.astype(np.float64) - lo16.astype(np.float64)) / levels
+                    sc = np.where(sc > 0, sc, 1.0)
+                    if not _device._ALLOW_ROUNDING and not np.array_equal(sc[:D], np.asarray(scale, np.float64)):
+                        raise ValueError("snapshot scales are not reproducible from bounds in the pool dtype")
+                    bounds += [lo16, hi]
                 raw = layout.encode_slot(kc, vc, *bounds, Dp, self.P, self.bits, np_dt, self.slot_bytes)
             else:
                 kc = _np_exact(np.pad(np.asarray(pg.k_codes[:t], np.float64), ((0, 0), (0, Dp - D))), np_dt)
@@ -339,7 +363,7 @@ class DevicePool:
                     st.append(PageStats(vals[0].copy(), vals[1].copy(), min(self.L, tc - jl * self.L)))
             pg = PhysicalPage(p, kv_head, self.P, tc, np.ascontiguousarray(kcodes[:tc]),
                               np.ascontiguousarray(vcodes[:tc]), ks, kz, vs, vz, st)
-            pg._origin = (self, s)  # lets select_pages score device-resident pages in place
+            _set_origin(pg, self, s)  # lets select_pages score device-resident pages in place
             pages.append(pg)
         return pages
 

@@ -716,8 +716,41 @@ int launch_cl(const DecodeParams& prm, int n_streams, cudaStream_t st) {
   return SK_OK;
 }
 
+// A non-portable 16-CTA cluster per stream when the streams are few enough
+// that 16 x n_streams CTAs (one per SM) fit as co-resident clusters: twice the
+// warps per stream, so a 128k union of ~66 pages is one page per warp.
+#ifndef SK_DEC_MAX_CLUSTER
+#define SK_DEC_MAX_CLUSTER 16
+#endif
+template <typename T, int KIND, int D, int P>
+bool cluster16_fits(int n_streams) {
+  if (SK_DEC_MAX_CLUSTER < 16 || n_streams > 9) return false;
+  static int max_clusters = -1;  // per template instance (kernel)
+  if (max_clusters < 0) {
+    auto kern = decode_kernel<T, KIND, D, P, 16>;
+    max_clusters = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(16, 1, 1);
+      cfg.blockDim = dim3(kDecThreads, 1, 1);
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 16;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess) max_clusters = n;
+    }
+    cudaGetLastError();  // clear a refused attribute / query
+  }
+  return n_streams <= max_clusters;
+}
+
 template <typename T, int KIND, int D, int P>
 int launch_one(const DecodeParams& prm, int n_streams, cudaStream_t st) {
+  if (cluster16_fits<T, KIND, D, P>(n_streams)) return launch_cl<T, KIND, D, P, 16>(prm, n_streams, st);
   switch (cluster_for(n_streams)) {
     case 8: return launch_cl<T, KIND, D, P, 8>(prm, n_streams, st);
     case 4: return launch_cl<T, KIND, D, P, 4>(prm, n_streams, st);

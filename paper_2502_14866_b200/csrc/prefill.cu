@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             mma_f16_ss(tmem + kOCol + t * 128, a, b, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
           }
         }
-        mma_commit(&sm.p_empty[t][jj & 1]);
+        if (!kTmemP) mma_commit(&sm.p_empty[t][jj & 1]);  // P in TMEM: no smem P buffer to release
         mma_commit(&sm.o_done[t]);
         if (t == 1) mma_commit(&sm.kv_empty[st]);
       }
@@ -368,7 +368,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       const float m_new = fmaxf(m_run, mx);
       const bool need = (m_run != -INFINITY) && (m_new > m_run + kRescaleThreshold);
       if (m_run == -INFINITY) m_run = m_new;
-      if (__any_sync(0xffffffffu, need)) {
+      const bool rescale = __any_sync(0xffffffffu, need);
+      if (rescale) {
         if (j > 0) mbar_wait(&sm.o_done[t], (j - 1) & 1);  // PV_{j-1} landed in O
         tc_fence_after();
         const float alpha = need ? exp2f(m_run - m_new) : 1.f;
@@ -413,6 +414,9 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         const float2 a = f2_unpack(f2_add(f2_add(rs[0], rs[1]), f2_add(rs[2], rs[3])));
         l_run += a.x + a.y;
       }
+      // every o_done phase is waited exactly once: phase j-1 here (PV_{j-1} ran
+      // while this softmax did; the wait is almost always already satisfied)
+      if (j > 0 && !rescale) mbar_wait(&sm.o_done[t], (j - 1) & 1);
       if (kTmemP) {
         // P over the first 32 columns of this S buffer: S_t,j+2 (the next
         // writer) is issued after PV_t,j, and tcgen05 MMAs run in order
@@ -432,11 +436,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.p_full[t][j & 1]);
     }
-    // epilogue: O / l -> out.  o_done completes one phase per PV; when the
-    // last S landed only PV_t,n-3 was certainly done, so the barrier may be
-    // two phases behind: wait for phase n-2 first (parity alone cannot tell
-    // phase n-1 from n-3), then for phase n-1.
-    if (n_blocks > 1) mbar_wait(&sm.o_done[t], (n_blocks - 2) & 1);
+    // epilogue: O / l -> out.  o_done completes one phase per PV; phases
+    // 0..n-2 were waited in the loop, so the last one is next.
     if (n_blocks > 0) {
       mbar_wait(&sm.o_done[t], (n_blocks - 1) & 1);
       tc_fence_after();

@@ -120,6 +120,20 @@ inline int check_pool(const sk_pool* p) {
   return SK_OK;
 }
 
+// SM count of the current device (cached per device; host only).
+inline int device_sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
 // streaming-window membership of page p among n pages (heads.py:107-125 at
 // query tile n-1): sink_end = min(sink, n), local_start = max(n - local, 0).
 __host__ __device__ inline bool in_lambda(int p, int n, int sink, int local) {

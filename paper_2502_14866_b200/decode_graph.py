@@ -9,6 +9,11 @@ replays them.  Token counters, page tables and workspaces are device
 resident, so replays need no host->device traffic besides the new q/k/v
 rows.  Per-engine host bookkeeping (token mirrors, step counters, ledger)
 is advanced exactly like Engine.decode_step would.
+
+Multi-GPU (KV-head sharding): with `group`, each layer's head
+outputs are all-gathered over NCCL right behind that layer's K3, inside the
+captured graph (one collective per layer, at the layer boundary), into
+`gathered[layer]` = [world, H/world, Dp] head-major.
 """
 
 from __future__ import annotations
@@ -25,7 +30,7 @@ from .selector import _Workspace, selection_size
 
 
 class DecodeGraph:
-    def __init__(self, engines: list, max_steps: int, head_dim: int, record_ledger: bool = True):
+    def __init__(self, engines: list, max_steps: int, head_dim: int, record_ledger: bool = True, group=None):
         if not engines:
             raise ValueError("need at least one engine")
         if record_ledger and any(not hasattr(e, "_plans") for e in engines):
@@ -74,6 +79,14 @@ class DecodeGraph:
         self.sel_ws = [torch.zeros(_lib.load().sk_select_workspace(self.h_kv, self.max_pages_hint),
                                    dtype=torch.uint8, device=self.dev) for _ in engines]
         self.graphs = {}
+        self.group = group
+        self.gathered = None
+        if group is not None:
+            import torch.distributed as dist
+            world = dist.get_world_size(group)
+            self.gathered = torch.zeros((L, world) + tuple(self.out.shape[1:]), dtype=self.dtype, device=self.dev)
+            dist.all_gather_into_tensor(self.gathered[0], self.out[0], group=group)  # communicator up before capture
+            torch.cuda.synchronize(self.dev)
         self._side = torch.cuda.Stream(device=self.dev)
         # prime selections (first step must select anyway) then capture
         self._capture()
@@ -99,6 +112,9 @@ class DecodeGraph:
                                 C.c_float(1.0 / math.sqrt(self.head_dim)), self.out[li].data_ptr(),
                                 self.g * self.dp, self.dp, _device.sk_dtype(self.dtype), 0, stream)
         _lib.check(rc)
+        if self.group is not None:  # layer boundary: head outputs of every rank
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(self.gathered[li], self.out[li], group=self.group)
         # K1 one-token append on a side stream: overlaps the next layer's attention
         side.wait_stream(main)
         rc = lib.sk_append_pages(C.byref(abi), self.h_kv, self.k[li].data_ptr(), self.v[li].data_ptr(), self.dp, 0,

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _device, _lib
-from .cache import DevicePool, PageStats, PhysicalPage
+from .cache import DevicePool, PageStats, PhysicalPage, page_origin
 
 
 def logical_page_score(q, stats: PageStats) -> float:
@@ -130,9 +130,9 @@ def _run_select(q_group, pages: Sequence[PhysicalPage], budget_pages: int, page_
     rows = q.shape[0]
     if rows > 8:
         raise ValueError("select_pages on the B200 path takes at most 8 query rows per KV head")
-    src = getattr(pages[0], "_origin", None)
+    src = page_origin(pages[0])
     pool = None
-    if src is not None and all(getattr(p, "_origin", None) == src for p in pages):
+    if src is not None and all(page_origin(p) == src for p in pages):
         cand, stream = src
         if [p.page_id for p in pages] == list(range(cand.page_count(stream))) and \
                 cand.kinds[stream] == _lib.SK_KIND_DENSE and cand.P == page_size:

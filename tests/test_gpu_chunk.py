@@ -11,7 +11,7 @@ import torch
 import paper_2502_14866_b200 as sk
 from oracle import sparsekv_oracle as O
 from test_gpu_parity import assert_close_attn
-from test_gpu_edges import fp16_vals
+from test_gpu_edges import bf16_vals, fp16_vals
 
 pytestmark = pytest.mark.gpu
 
@@ -24,7 +24,8 @@ def test_gather_is_snapshot_dequantised(bits, dtype):
     gates = [0.9, 0.1, 0.1, 0.1, 0.8, 0.2]  # KV head 1 all-streaming (ring), 0 and 2 dense
     cfg = sk.EngineConfig(quant_bits=bits, local_blocks=3)
     eng = sk.Engine(cfg, sk.classify_heads(gates, 0.5, 1, 3), dtype=dtype, device="cuda:0")
-    eng.load_context(fp16_vals(rng, s, h_kv, d), fp16_vals(rng, s, h_kv, d))
+    vals = fp16_vals if dtype == torch.float16 else bf16_vals
+    eng.load_context(vals(rng, s, h_kv, d), vals(rng, s, h_kv, d))
     pool = eng.cache.pool
     kg, vg = pool.gather()
     kg, vg = kg.float().cpu().numpy(), vg.float().cpu().numpy()

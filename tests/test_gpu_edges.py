@@ -35,6 +35,11 @@ def fp16_vals(rng, *shape):
     return rng.standard_normal(shape).astype(np.float16).astype(np.float32)
 
 
+def bf16_vals(rng, *shape):
+    """N(0,1) values exactly representable in bf16 (as float32)."""
+    return torch.from_numpy(rng.standard_normal(shape).astype(np.float32)).to(torch.bfloat16).float().numpy()
+
+
 def gates_for(h, rng):
     return rng.uniform(0, 1, h).tolist()
 

@@ -110,3 +110,22 @@ def test_gloo_world2_sharded_equals_unsharded():
     for i, st in enumerate(ref_steps):
         np.testing.assert_array_equal(dec_out[i], st.output)
         assert [tuple(t) for t in tables[i]] == [tuple(t) for t in st.tables]
+
+
+def test_bench_gpus_2_launches_two_ranks():
+    """`bench.py --gpus 2` without torchrun re-launches itself with 2 ranks
+    (torch.distributed.run on 127.0.0.1); the ranks' KV-head shards, gathered
+    over gloo, tile all 32 query / 8 KV heads."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--plan-only"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert res.returncode == 0, res.stderr[-3000:]
+    line = [ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1]
+    out = json.loads(line)
+    assert out["world"] == 2 and out["covers_all_heads"]
+    assert out["shards"] == [[0, 16, 0, 4], [16, 32, 4, 8]]
