@@ -115,35 +115,58 @@ int sk_append_pages(const sk_pool* pool, int32_t n_streams, const void* k_src, c
 int sk_gather_pages(const sk_pool* pool, int32_t n_streams, int32_t n_tokens, void* k_out, void* v_out,
                     int64_t out_stream_stride, int64_t out_token_stride, void* stream);
 
+/* Launch flags (sk_select_pages / sk_decode_attn). */
+#define SK_DECODE_APPEND 1u    /* decode: append the new token behind the attention */
+#define SK_LAUNCH_PDL 2u       /* programmatic dependent launch (see each entry point) */
+#define SK_DECODE_SEL_READY 4u /* decode: the selection predates the previous kernel */
+
 /*
  * K2 -- hierarchical page selection (Eq. 2).  Replaces
  * score_pages / select_pages / pinned_pages (selector.py:39-108) and the
  * call site engine.py:237-255.  For every stream with invoke[s] != 0 and a
- * non-zero retrieval row mask: scores every logical page in fp64 as
+ * non-zero retrieval row mask: scores every logical page as
  * sum_c max(q_c*kmax_c, q_c*kmin_c), takes the max over the retrieval rows
  * and over the logical pages of each physical page, then selects
  * K = budget_pages pages: all pages if K >= n; the pins {0, n-2, n-1} if
  * K <= |pins|; else pins + the best K-|pins| others ordered by
- * (score desc, page index asc).  Output is ascending.
+ * (score desc, page index asc).  Output is ascending.  The ranking is the
+ * reference's fp64 one, bit for bit: every page is scored on the tensor
+ * cores in fp32 with a rigorous error bound, and the pages whose bound
+ * straddles the K-th score are rescored exactly in fp64.
  *   q:         device; row r of stream s at q + s*q_stream_stride + r*q_row_stride.
- *   row_mask:  device [n_streams] bit r set = group row r is a retrieval row.
+ *   row_mask:  device [n_streams] bit r set = group row r (< group_rows <= 32) is a retrieval row.
  *   tokens:    device [n_streams] tokens currently in each stream.
  *   invoke:    device [n_streams] (NULL = all).
  *   sel_out:   device [n_streams][sel_stride] ascending page indices.
  *   sel_count: device [n_streams].
  *   max_pages_hint: >= ceil(max tokens / P), sizes the grid.
+ *   flags: SK_LAUNCH_PDL launches as a programmatic dependent of the previous kernel on
+ *          the stream (CUDA-graph decode): stats, tokens, row masks and invoke flags are
+ *          read before the dependency wait, so the previous kernel must not write them;
+ *          q after it.
  */
-/* Workspace bytes: [u32 ticket per stream, padded to 256 B | f64 page score
- * per (stream, page < max_pages)].  Zero it once; the kernel re-arms its
- * tickets, so one buffer serves every launch with a max_pages_hint it fits.
- * The scores of the last launch start at sk_select_scores_offset(n). */
+/* Workspace bytes: [u32 ticket per stream, padded to 256 B | (f32 score,
+ * f32 error bound) per (stream, page < max_pages) | f64 scratch per (stream,
+ * page)].  Zero it once; the kernel re-arms its tickets, so one buffer serves
+ * every launch with a max_pages_hint it fits.  The (score, bound) pairs of
+ * the last launch start at sk_select_scores_offset(n). */
 int64_t sk_select_workspace(int32_t n_streams, int32_t max_pages);
 int64_t sk_select_scores_offset(int32_t n_streams);
 int sk_select_pages(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
                     int64_t q_stream_stride, int64_t q_row_stride, const uint32_t* row_mask,
                     const int32_t* tokens, const uint8_t* invoke, int32_t budget_pages, int32_t max_pages_hint,
                     int32_t* sel_out, int32_t* sel_count, int32_t sel_stride, void* workspace,
-                    int64_t workspace_bytes, void* stream);
+                    int64_t workspace_bytes, uint32_t flags, void* stream);
+
+/*
+ * score_pages (selector.py:39-72): the exact fp64 physical-page score of
+ * every page p < min(ceil(tokens[s]/P), out_stride) of every stream, max over
+ * the retrieval rows of row_mask[s] (-inf for a stream without one), into
+ * scores_out[s*out_stride + p].  Same arithmetic as K2's exact rescoring.
+ */
+int sk_score_pages(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
+                   int64_t q_stream_stride, int64_t q_row_stride, const uint32_t* row_mask,
+                   const int32_t* tokens, double* scores_out, int32_t out_stride, void* stream);
 
 /*
  * K3 -- split-KV decode attention over the selected pages.  Replaces the
@@ -153,22 +176,32 @@ int sk_select_pages(const sk_pool* pool, int32_t n_streams, int32_t group_rows, 
  * selection (retrieval rows, bit r of row_mask[s] set) or the sink+local
  * window of the current page count (streaming rows, streaming_schedule at
  * qt = page_count - 1, heads.py:107-125), then the raw new token
- * in-register.  Pages are dequantised on the fly; the CTAs of a stream
- * merge their partials with log-sum-exp.
+ * in-register.  Pages are dequantised on the fly; the union of the
+ * stream's pages is cut into 32-token units spread over several CTAs, whose
+ * partials are merged with log-sum-exp by the stream's last CTA.
  *   row_window: device [n_streams][group_rows] u32 = sink_blocks | local_blocks << 16
  *               of each streaming row (its HeadProfile), or NULL for the pool's window.
  *               A streaming-pool stream only holds the pool's window: the caller must
  *               not ask for more (the reference raises "evicted" there).
- *   append_new: != 0 appends k_new/v_new (K1, one token) right behind the attention on
- *               the same stream (a second launch) and increments tokens[s].
+ *   flags: SK_DECODE_APPEND appends k_new/v_new (K1, one token) right behind the
+ *          attention on the same stream (a second launch) and increments tokens[s];
+ *          SK_LAUNCH_PDL launches as a programmatic dependent of the previous kernel on
+ *          the stream (CUDA-graph decode): the pool, tokens and page table -- and, with
+ *          SK_DECODE_SEL_READY, the selection -- are read before the dependency wait, so
+ *          the previous kernel must not write them; q / k_new / v_new are read after it.
  *   out: element (s, r, c) at out + s*out_stream_stride + r*out_row_stride + c, type out_dtype.
+ *   workspace: device, >= sk_decode_workspace(n_streams, group_rows, head_dim) bytes,
+ *              zeroed once (tickets re-arm themselves); launches that share one
+ *              workspace must be stream-ordered.  Page size: a multiple of 32.
  */
+int64_t sk_decode_workspace(int32_t n_streams, int32_t group_rows, int32_t head_dim);
 int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
                    int64_t q_stream_stride, int64_t q_row_stride, const void* k_new, const void* v_new,
                    int64_t new_stream_stride, const uint32_t* row_mask, const uint32_t* row_window,
                    const int32_t* sel, const int32_t* sel_count, int32_t sel_stride, int32_t* tokens,
                    float softmax_scale, void* out, int64_t out_stream_stride, int64_t out_row_stride,
-                   int32_t out_dtype, int32_t append_new, void* stream);
+                   int32_t out_dtype, uint32_t flags, void* workspace, int64_t workspace_bytes,
+                   void* stream);
 
 /*
  * K4 -- block-sparse causal prefill attention on tcgen05 tensor cores.

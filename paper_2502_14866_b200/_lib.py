@@ -14,14 +14,15 @@ import threading
 SK_OK, SK_EINVAL, SK_ECUDA, SK_EUNSUPPORTED = 0, -1, -2, -3
 SK_F16, SK_BF16, SK_F32 = 0, 1, 2
 SK_KIND_DENSE, SK_KIND_STREAMING = 0, 1
+SK_DECODE_APPEND, SK_LAUNCH_PDL, SK_DECODE_SEL_READY = 1, 2, 4  # launch flags (sparsekv_b200.h)
 
 LIB_PATH = os.environ.get("SK_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                        "libsparsekv_b200.so")
 
 # every symbol include/sparsekv_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ("sk_version", "sk_last_error", "sk_device_supported", "sk_slot_bytes", "sk_append_pages",
-           "sk_gather_pages", "sk_select_workspace", "sk_select_scores_offset", "sk_select_pages",
-           "sk_decode_attn", "sk_prefill_attn")
+           "sk_gather_pages", "sk_select_workspace", "sk_select_scores_offset", "sk_select_pages", "sk_score_pages",
+           "sk_decode_workspace", "sk_decode_attn", "sk_prefill_attn")
 
 
 class SkPool(C.Structure):
@@ -52,11 +53,14 @@ _SIGS = {
     "sk_select_scores_offset": (C.c_int64, [C.c_int32]),
     "sk_select_pages": (C.c_int, [C.POINTER(SkPool), C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_int64,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
-                                  C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]),
+                                  C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_uint32, C.c_void_p]),
+    "sk_score_pages": (C.c_int, [C.POINTER(SkPool), C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_int64,
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "sk_decode_workspace": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
     "sk_decode_attn": (C.c_int, [C.POINTER(SkPool), C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_int64,
                                  C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_int32, C.c_void_p, C.c_float, C.c_void_p, C.c_int64, C.c_int64,
-                                 C.c_int32, C.c_int32, C.c_void_p]),
+                                 C.c_int32, C.c_uint32, C.c_void_p, C.c_int64, C.c_void_p]),
     "sk_prefill_attn": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                   C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_void_p, C.c_int32,
                                   C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -78,6 +82,9 @@ def load():
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args
+            if hasattr(lib, "sk_debug_decode_stamps"):  # timing builds only
+                lib.sk_debug_decode_stamps.restype = C.c_int
+                lib.sk_debug_decode_stamps.argtypes = [C.c_void_p]
             _lib = lib
     return _lib
 

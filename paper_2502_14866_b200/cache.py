@@ -209,6 +209,16 @@ class DevicePool:
         self.tokens_host = [0] * self.n_streams
 
     # -- ABI view -------------------------------------------------------------
+    def decode_workspace(self, group_rows: int) -> torch.Tensor:
+        """K3's workspace for this pool (tickets + per-CTA partials), zeroed
+        once; the pool's decode launches are stream-ordered, so they share it."""
+        need = _lib.load().sk_decode_workspace(self.n_streams, group_rows, self.Dp)
+        ws = getattr(self, "_dec_ws", None)
+        if ws is None or ws.numel() < need or ws.device != self.device:
+            ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+            self._dec_ws = ws
+        return ws
+
     def abi(self, first_stream: int = 0) -> _lib.SkPool:
         s = first_stream
         return _lib.SkPool(

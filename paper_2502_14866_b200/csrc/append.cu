@@ -28,18 +28,26 @@ __global__ void __launch_bounds__(256) append_kernel(PoolView pv, const T* __res
   append_page<T>(pv, s, p, n0, n1, k_src + s * src_ss, v_src + s * src_ss, src_ts, smem);
 }
 
-// One new token per stream (decode): one CTA per stream, incremental page
-// update (append_one_token) or a fresh page, then the stream's counter.
+// One new token per stream (decode): a cluster of kAppendParts CTAs per
+// stream (append_one_part), or its first CTA alone for a fresh page / raw
+// pool (append_page); the cluster barrier orders every part's read of the
+// stream's token count before part 0 advances it.
 template <typename T>
 __global__ void __launch_bounds__(256) append_one_kernel(PoolView pv, const T* __restrict__ k_src,
                                                          const T* __restrict__ v_src, int64_t src_ss,
                                                          int32_t* __restrict__ tokens) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int s = blockIdx.x;
+  const int part = blockIdx.x, s = blockIdx.y;
   const int n0 = tokens[s];
-  append_one_token<T>(pv, s, n0, k_src + s * src_ss, v_src + s * src_ss, smem);
-  __syncthreads();
-  if (threadIdx.x == 0) tokens[s] = n0 + 1;
+  const T* kn = k_src + s * src_ss;
+  const T* vn = v_src + s * src_ss;
+  if (n0 % pv.P == 0 || pv.bits == 0) {
+    if (part == 0) append_page<T>(pv, s, n0 / pv.P, n0, n0 + 1, kn, vn, 0, smem);
+  } else {
+    append_one_part<T>(pv, s, part, n0, kn, vn, smem);
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (part == 0 && threadIdx.x == 0) tokens[s] = n0 + 1;
 }
 
 __global__ void advance_tokens_kernel(int32_t* tokens, int n, int m) {
@@ -61,16 +69,33 @@ int append_launch(const sk_pool* pool, int n_streams, const void* k_src, const v
   PoolView pv = make_view(*pool);
   if (m == 1) {
     size_t smem1 = append_smem_bytes(pv.D, pv.P);
-    size_t smem2 = append_one_smem_bytes(pv.D, pv.P);
+    size_t smem2 = append_part_smem_bytes(pv.D, pv.P);
     size_t sm = smem1 > smem2 ? smem1 : smem2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kAppendParts, n_streams, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kAppendParts;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e;
     if (pv.dtype == SK_F16) {
       cudaFuncSetAttribute(append_one_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      append_one_kernel<__half><<<n_streams, 256, sm, st>>>(pv, (const __half*)k_src, (const __half*)v_src, ss,
-                                                           tokens);
+      e = cudaLaunchKernelEx(&cfg, append_one_kernel<__half>, pv, (const __half*)k_src, (const __half*)v_src, ss,
+                             tokens);
     } else {
       cudaFuncSetAttribute(append_one_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      append_one_kernel<__nv_bfloat16><<<n_streams, 256, sm, st>>>(pv, (const __nv_bfloat16*)k_src,
-                                                                  (const __nv_bfloat16*)v_src, ss, tokens);
+      e = cudaLaunchKernelEx(&cfg, append_one_kernel<__nv_bfloat16>, pv, (const __nv_bfloat16*)k_src,
+                             (const __nv_bfloat16*)v_src, ss, tokens);
+    }
+    if (e != cudaSuccess) {
+      set_error(std::string("append_one_kernel: ") + cudaGetErrorString(e));
+      return SK_ECUDA;
     }
     SK_CHECK_LAUNCH("append_one_kernel");
     return SK_OK;

@@ -6,9 +6,6 @@
 
 namespace sk {
 
-__host__ __device__ inline size_t append_one_smem_bytes(int D, int P) {
-  return (size_t)2 * D * (4 + 3 * 8) + ((2 * D + 15) & ~15) + (size_t)2 * P * D * 2;
-}
 __host__ __device__ inline size_t append_smem_bytes(int D, int P) {
   return (size_t)2 * P * D * 2 + 6 * D * sizeof(double);
 }
@@ -233,146 +230,157 @@ __device__ void append_page(const PoolView& pv, int s, int p, int n0, int n1, co
 
 
 // Decode-step append of ONE token to stream s holding n_tok tokens, for an
-// open page that already has t_old = n_tok % P > 0 tokens.  Bit-identical
-// to append_page(): a channel whose min/max did not move keeps its lo and
-// scale, so only the new token's code changes; channels whose bounds moved
-// are re-coded for every token of the page from the raw staging copy.
-// Whole CTA; smem >= append_one_smem_bytes(D, P).
+// open page that already holds t_old = n_tok % P > 0 tokens, split over the
+// kAppendParts CTAs of a cluster (latency: one CTA per stream was a long
+// serial chain).  Part q < 4 re-codes the K words of page tokens
+// [q P/4, (q+1) P/4), part q >= 4 the V words of channels
+// [(q-4) D/4, (q-3) D/4).  Every part recomputes the bounds it needs from the
+// raw staging copy plus the new token and re-codes its words in full, so no
+// code word is read back: bit-identical to append_page() (a full rebuild of
+// the page, cache.py:211-251).  Part 0 also writes the K bounds, the open
+// logical page's key stats and the K staging row; part 4 the V staging row.
+constexpr int kAppendParts = 8;
+__host__ __device__ inline size_t append_part_smem_bytes(int D, int P) {
+  return (size_t)P * D * 2 + (size_t)2 * 256 * 4 + (size_t)3 * D * 8;
+}
+
 template <typename T>
-__device__ void append_one_token(const PoolView& pv, int s, int n_tok, const T* __restrict__ kn,
-                                 const T* __restrict__ vn, uint8_t* smem) {
+__device__ void append_one_part(const PoolView& pv, int s, int part, int n_tok, const T* __restrict__ kn,
+                                const T* __restrict__ vn, uint8_t* smem) {
   const int D = pv.D, P = pv.P;
-  const int t_old = n_tok % P;
-  const int p = n_tok / P;
-  if (t_old == 0 || pv.bits == 0) {
-    append_page<T>(pv, s, p, n_tok, n_tok + 1, kn, vn, 0, smem);
-    return;
-  }
-  const bool dense = pv.kind[s] == SK_KIND_DENSE;
-  uint8_t* slot = pv.slot_ptr(s, p);
-  T* bnd = reinterpret_cast<T*>(pv.bounds(slot));
-  const T* stg[2] = {reinterpret_cast<const T*>(pv.staging_ptr(s, 0)),
-                     reinterpret_cast<const T*>(pv.staging_ptr(s, 1))};
-  float* xnew = reinterpret_cast<float*>(smem);   // [2][D]
-  double* lo = reinterpret_cast<double*>(xnew + 2 * D);  // [2][D]
-  double* sc = lo + 2 * D;
-  double* inv = sc + 2 * D;
-  uint8_t* chg = reinterpret_cast<uint8_t*>(inv + 2 * D);  // [2][D]
-  T* raw = reinterpret_cast<T*>(chg + ((2 * D + 15) & ~15));  // [2][t_old][D] staged raw tokens
+  const int t_old = n_tok % P, p = n_tok / P, nt = t_old + 1;  // tokens in the page after the append
+  const bool isv = part >= 4;
+  const int q = part & 3;
+  const int c0 = isv ? q * (D / 4) : 0, nc = isv ? D / 4 : D;  // channels this part needs
+  const T* stg = reinterpret_cast<const T*>(pv.staging_ptr(s, isv ? 1 : 0));
+  const T* xn = isv ? vn : kn;
+  T* raw = reinterpret_cast<T*>(smem);                                // [nt][nc]
+  float* pmin = reinterpret_cast<float*>(raw + (size_t)P * D);        // [256]
+  float* pmax = pmin + 256;                                           // [256]
+  double* lo = reinterpret_cast<double*>(pmax + 256);                 // [nc]
+  double* sc = lo + D;
+  double* inv = sc + D;
   const int levels = (1 << pv.bits) - 1;
-  // the open page's raw tokens -> smem (one coalesced sweep; code_at reads them often)
-  for (int i = threadIdx.x; i < 2 * t_old * (D / 8); i += blockDim.x) {
-    const int which = i / (t_old * (D / 8)), rem = i % (t_old * (D / 8));
-    *reinterpret_cast<uint4*>(raw + (which * t_old) * D + rem * 8) =
-        *reinterpret_cast<const uint4*>(stg[which] + rem * 8);
-  }
-  for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) {
-    const int which = i / D, c = i % D;
-    const float x = DT<T>::to_f((which ? vn : kn)[c]);
-    const int pos = which ? vbound_pos(c, D) : kbound_pos(c, D);
-    const float olo = DT<T>::to_f(bnd[2 * which * D + pos]), ohi = DT<T>::to_f(bnd[(2 * which + 1) * D + pos]);
-    const float nlo = fminf(olo, x), nhi = fmaxf(ohi, x);
-    const bool changed = (nlo != olo) || (nhi != ohi);
-    if (changed) {
-      bnd[2 * which * D + pos] = DT<T>::from_f(nlo);
-      bnd[(2 * which + 1) * D + pos] = DT<T>::from_f(nhi);
-    }
-    double scl = ((double)nhi - (double)nlo) / levels;
-    if (!(scl > 0.0)) scl = 1.0;
-    xnew[i] = x;
-    lo[i] = nlo;
-    sc[i] = scl;
-    inv[i] = 1.0 / scl;
-    chg[i] = changed;
+  // 1. raw page (staging rows + the new token) -> smem, 16-byte vectors
+  const int vpr = nc / 8;  // vectors per row
+  for (int i = threadIdx.x; i < nt * vpr; i += blockDim.x) {
+    const int t = i / vpr, c = (i % vpr) * 8;
+    const T* src = t < t_old ? stg + (int64_t)t * D + c0 + c : xn + c0 + c;
+    *reinterpret_cast<uint4*>(raw + t * nc + c) = *reinterpret_cast<const uint4*>(src);
   }
   __syncthreads();
-  auto code_at = [&](int which, int t, int c) -> uint32_t {
-    if (t > t_old) return 0u;  // padding slots of the page
-    const float x = t == t_old ? xnew[which * D + c] : DT<T>::to_f(raw[(which * t_old + t) * D + c]);
-    const int i = which * D + c;
-    return quant_code((double)x, lo[i], sc[i], inv[i], levels);
+  // 2. per-channel bounds over the page's tokens: 256 / nc token splits per channel
+  {
+    const int ns = 256 / nc, c = threadIdx.x % nc, sp = threadIdx.x / nc;
+    float mn = INFINITY, mx = -INFINITY;
+    if (sp < ns)
+      for (int t = sp; t < nt; t += ns) {
+        const float x = DT<T>::to_f(raw[t * nc + c]);
+        mn = fminf(mn, x);
+        mx = fmaxf(mx, x);
+      }
+    pmin[threadIdx.x] = mn;
+    pmax[threadIdx.x] = mx;
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      for (int k = 1; k < ns; ++k) {
+        mn = fminf(mn, pmin[k * nc + c]);
+        mx = fmaxf(mx, pmax[k * nc + c]);
+      }
+      double scl = ((double)mx - (double)mn) / levels;
+      if (!(scl > 0.0)) scl = 1.0;
+      lo[c] = mn;
+      sc[c] = scl;
+      inv[c] = 1.0 / scl;
+      if (isv || part == 0) {  // exact: lo/hi are T values
+        T* bnd = reinterpret_cast<T*>(pv.bounds(pv.slot_ptr(s, p)));
+        const int ch = c0 + c;
+        const int pos = isv ? vbound_pos(ch, D) : kbound_pos(ch, D);
+        bnd[(isv ? 2 : 0) * D + pos] = DT<T>::from_f(mn);
+        bnd[(isv ? 3 : 1) * D + pos] = DT<T>::from_f(mx);
+      }
+    }
+    __syncthreads();
+  }
+  auto code_at = [&](int t, int c) -> uint32_t {  // c relative to c0; padding tokens -> 0
+    if (t >= nt) return 0u;
+    return quant_code((double)DT<T>::to_f(raw[t * nc + c]), lo[c], sc[c], inv[c], levels);
   };
-  uint32_t* kw = reinterpret_cast<uint32_t*>(pv.k_codes(slot));
-  uint32_t* vw = reinterpret_cast<uint32_t*>(pv.v_codes(slot));
+  // 3. this part's code words, fragment-native layout (sk_layout.cuh)
+  uint8_t* slot = pv.slot_ptr(s, p);
   const bool nib = pv.bits <= 4;
-  const int cpw = nib ? 8 : 4;                      // codes per 32-bit word
-  const int wpt = nib ? D / 8 : D / 4;              // K words per token
-  const int wpc = nib ? D / 32 : D / 16;            // K words per (token, j) chunk
-  const int vwl = nib ? P / 32 : P / 16;            // V words per (cn, lane)
-  // (q-th code of a word) -> (register index offset, e, bit position)
-  auto qmap = [&](int w, int q, int& ri, int& e, int& bit) {
-    if (nib) {
-      const int slt = q >> 1;
-      e = q & 1;
-      ri = 4 * w + slt;
-      bit = 4 * slt + 16 * e;
-    } else {
-      const int r2 = q >> 1;
-      e = q & 1;
-      ri = 2 * w + r2;
-      bit = 8 * (2 * r2 + e);
-    }
-  };
-  const uint32_t cmask = nib ? 0xFu : 0xFFu;
-  // K: words of tokens 0..t_old (token t_old fully rewritten, others only if a channel moved)
-  for (int wi = threadIdx.x; wi < (t_old + 1) * wpt; wi += blockDim.x) {
-    const int t = wi / wpt, rem = wi % wpt, j = rem / wpc, w = rem % wpc;
-    uint32_t word = t == t_old ? 0u : kw[t * wpt + rem];
-    bool dirty = t == t_old;
-    for (int q = 0; q < cpw; ++q) {
-      int ri, e, bit;
-      qmap(w, q, ri, e, bit);
-      const int d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j + e;
-      if (t == t_old || chg[d]) {
-        word = (word & ~(cmask << bit)) | (code_at(0, t, d) << bit);
-        dirty = true;
-      }
-    }
-    if (dirty) kw[t * wpt + rem] = word;
-  }
-  // V: a moved channel rewrites all its words; otherwise only the nibble/byte of token t_old
-  const int vwords = P * D / cpw;
-  for (int wi = threadIdx.x; wi < vwords; wi += blockDim.x) {
-    const int cn = wi / (32 * vwl), rem = wi % (32 * vwl), lane = rem / vwl, w = rem % vwl;
-    const int c = 8 * cn + lane / 4, j = lane % 4;
-    const bool moved = chg[D + c];
-    uint32_t word = moved ? 0u : vw[wi];
-    bool dirty = moved;
-    for (int q = 0; q < cpw; ++q) {
-      int ri, e, bit;
-      qmap(w, q, ri, e, bit);
-      const int t = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j + e;
-      if (moved || t == t_old) {
-        word = (word & ~(cmask << bit)) | (code_at(1, t, c) << bit);
-        dirty = true;
-      }
-    }
-    if (dirty) vw[wi] = word;
-  }
-  // logical-page key stats of the page's open logical page (dense pool)
-  if (dense && pv.stats != nullptr) {
-    const int L = pv.L;
-    T* st = reinterpret_cast<T*>(pv.stats_ptr(s, p * (P / L) + t_old / L));
-    const bool fresh = (t_old % L) == 0;
-    for (int c = threadIdx.x; c < D; c += blockDim.x) {
-      const float x = xnew[c];
-      if (fresh) {
-        st[c] = DT<T>::from_f(x);
-        st[D + c] = DT<T>::from_f(x);
+  if (!isv) {
+    uint32_t* kw = reinterpret_cast<uint32_t*>(pv.k_codes(slot));
+    const int wpt = nib ? D / 8 : D / 4, wpc = nib ? D / 32 : D / 16;  // words per token / per (token, j)
+    const int tq = P / 4, tfirst = q * tq;
+    for (int wi = threadIdx.x; wi < tq * wpt; wi += blockDim.x) {
+      const int t = tfirst + wi / wpt, rem = wi % wpt, j = rem / wpc, w = rem % wpc;
+      uint32_t word = 0;
+      if (nib) {
+#pragma unroll
+        for (int slt = 0; slt < 4; ++slt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int ri = 4 * w + slt, d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j + e;
+            word |= code_at(t, d) << (4 * slt + 16 * e);
+          }
       } else {
-        st[c] = DT<T>::from_f(fminf(DT<T>::to_f(st[c]), x));
-        st[D + c] = DT<T>::from_f(fmaxf(DT<T>::to_f(st[D + c]), x));
+#pragma unroll
+        for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int ri = 2 * w + r2, d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j + e;
+            word |= code_at(t, d) << (8 * (2 * r2 + e));
+          }
       }
+      kw[t * wpt + rem] = word;
+    }
+  } else {
+    uint32_t* vw = reinterpret_cast<uint32_t*>(pv.v_codes(slot));
+    const int vwl = nib ? P / 32 : P / 16;  // words per (cn, lane)
+    const int cn0 = c0 / 8, ncn = nc / 8;
+    for (int wi = threadIdx.x; wi < ncn * 32 * vwl; wi += blockDim.x) {
+      const int cnl = wi / (32 * vwl), rem = wi % (32 * vwl), lane = rem / vwl, w = rem % vwl;
+      const int c = 8 * cnl + lane / 4, j = lane % 4;  // relative channel
+      uint32_t word = 0;
+      if (nib) {
+#pragma unroll
+        for (int slt = 0; slt < 4; ++slt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int ri = 4 * w + slt, t = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j + e;
+            word |= code_at(t, c) << (4 * slt + 16 * e);
+          }
+      } else {
+#pragma unroll
+        for (int r2 = 0; r2 < 2; ++r2)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int ri = 2 * w + r2, t = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j + e;
+            word |= code_at(t, c) << (8 * (2 * r2 + e));
+          }
+      }
+      vw[(cn0 + cnl) * 32 * vwl + rem] = word;
     }
   }
-  // raw staging of the open page (unless the page is now full)
-  if (t_old + 1 < P) {
-    T* wk = reinterpret_cast<T*>(pv.staging_ptr(s, 0));
-    T* wv = reinterpret_cast<T*>(pv.staging_ptr(s, 1));
+  // 4. part 0: key stats of the open logical page (dense pool); parts 0 / 4: the staging row
+  if (part == 0 && pv.kind[s] == SK_KIND_DENSE && pv.stats != nullptr) {
+    const int L = pv.L, jl = t_old / L;
+    T* st = reinterpret_cast<T*>(pv.stats_ptr(s, p * (P / L) + jl));
     for (int c = threadIdx.x; c < D; c += blockDim.x) {
-      wk[t_old * D + c] = kn[c];
-      wv[t_old * D + c] = vn[c];
+      float mn = INFINITY, mx = -INFINITY;
+      for (int t = jl * L; t < nt; ++t) {
+        const float x = DT<T>::to_f(raw[t * nc + c]);
+        mn = fminf(mn, x);
+        mx = fmaxf(mx, x);
+      }
+      st[c] = DT<T>::from_f(mn);
+      st[D + c] = DT<T>::from_f(mx);
     }
+  }
+  if ((part == 0 || part == 4) && t_old + 1 < P) {
+    T* w = reinterpret_cast<T*>(pv.staging_ptr(s, isv ? 1 : 0));
+    for (int c = threadIdx.x; c < D; c += blockDim.x) w[t_old * D + c] = xn[c];
   }
 }
 

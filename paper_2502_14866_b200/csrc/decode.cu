@@ -4,34 +4,35 @@
 // engine.py:257-285), PhysicalPage.dequantize (cache.py:97-102) and
 // merge_block (attn.py:191-229).
 //
-// Work decomposition (latency-first: a 128k decode step reads ~5 MB, less
-// than a microsecond of HBM time, so the kernel is built around the number
-// of dependent memory round trips, not bandwidth):
-//   * one thread-block CLUSTER of kCl CTAs per stream (= one KV head of one
-//     sequence; kCl = 8 for a single sequence, down to 1 as batched
-//     sequences add streams -- cluster_for); the stream's page union -- the selection for retrieval
+// Work decomposition (latency-first: a 128k decode step of one layer reads
+// ~5 MB, under a microsecond of HBM time, so the kernel is built around the
+// number of dependent round trips and the length of each warp's dependent
+// compute chain, not bandwidth):
+//   * grid (cps, streams): cps CTAs per stream (= one KV head of one
+//     sequence), sized so that all the streams together fill the 148 SMs
+//     (decode_cps: 18 per stream for 8 streams, 1 once the streams alone
+//     fill the GPU).  The stream's page union -- the selection for retrieval
 //     rows plus the sink/local window for streaming rows, each page carrying
-//     the mask of group rows that attend it -- is dealt round-robin to the
-//     cluster's warps, one whole page per warp;
-//   * a warp issues every load of its page straight into registers
+//     the mask of group rows that attend it -- is cut into 32-token units
+//     (two 16-token MMA tiles), dealt round-robin over the stream's
+//     cps x 8 warps: at 128k each warp owns at most one unit;
+//   * a warp issues every load of its unit straight into registers
 //     (128-bit, coalesced: K1 writes the codes in the m16n8k16 fragment
 //     order, sk_layout.cuh) before doing any math, then runs QK and PV as
 //     m16n8k16 tensor-core MMAs on the stored codes through the
 //     dequantisation algebra
 //         q . khat_t = sum_d (q_d s_d) c_td + sum_d q_d lo_d
 //         sum_t p_t vhat_tc = s_c sum_t p_t c_tc + lo_c sum_t p_t
-//     (codes -> exact fp16 integers with one LOP3 + one HSUB2 per two);
-//     group rows sit in the MMA's M dimension, so GQA rows share each load;
-//   * one online-softmax state per (warp, row); warps merge in shared
-//     memory; every CTA then pushes its partial for each D/kCl-channel
-//     slice into the slice owner's shared-memory inbox (DSMEM stores + one
-//     release-arrive on the owner's mbarrier), and each owner finishes its
-//     slice plus the new token's raw K/V.  No global workspace, atomics or
-//     grid fences, and no blocking cluster barrier (the one split
-//     arrive/wait only orders the inbox initialisation).
+//     (codes -> exact fp16 integers with one LOP3 + one HSUB2 per two),
+//     TRANSPOSED so tokens / channels sit in the MMA's M dimension and the
+//     <= 8 group rows in N: S^T = K q'^T, O^T += V^T P^T;
+//   * one online-softmax state per (warp, row); the CTA's warps merge in
+//     shared memory; with cps > 1 each CTA writes its partial (m, l, O) to
+//     the workspace and the stream's last CTA (an acq_rel ticket) merges the
+//     cps partials with log-sum-exp together with the new token's raw K/V
+//     (engine.py:276-277) and writes the output.
 // Round trips on the critical path: {tokens, selection, q} -> page table ->
-// page data -> cluster barrier.
-#include <cooperative_groups.h>
+// unit data -> (partial, ticket) -> partials.
 #include <cstdlib>
 
 #include "append_impl.cuh"
@@ -42,26 +43,28 @@ int append_launch(const sk_pool* pool, int n_streams, const void* k_src, const v
                   int32_t* tokens, int m, int max_pages_touched, cudaStream_t st);
 }  // namespace sk
 
-namespace cg = cooperative_groups;
-
 namespace sk {
 namespace {
 
 constexpr int kDecThreads = 256;
 constexpr int kWarps = kDecThreads / 32;
-// CTAs per stream: a cluster of up to 8 (the portable maximum) when few
-// streams must fill the 148 SMs; fewer as the stream count grows, down to one
-// CTA per stream once the streams alone fill the GPU (a bigger cluster would
-// only multiply the waves: one CTA per SM at 255 registers).
-inline int cluster_for(int n_streams) {
-  if (n_streams <= 18) return 8;
-  if (n_streams <= 37) return 4;
-  if (n_streams <= 74) return 2;
-  return 1;
-}
 constexpr int kMaxRows = 8;    // group rows (query heads per KV head)
 constexpr int kMaxExtra = 64;  // sink + local pages
 constexpr int kMaxSel = 2048;  // selection entries staged in smem
+constexpr int kMaxCps = 32;    // CTAs per stream
+constexpr int kUnitTok = 32;   // tokens per work unit (two 16-token MMA tiles)
+
+// CTAs per stream: fill the SMs when the streams are few, never more CTAs
+// than the stream's largest possible union needs (8 units per CTA).
+inline int decode_cps(int n_streams, int max_units) {
+  int c = device_sm_count() / n_streams;
+  c = c < 1 ? 1 : (c > kMaxCps ? kMaxCps : c);
+  const int need = (max_units + kWarps - 1) / kWarps;
+  return c < need ? c : (need < 1 ? 1 : need);
+}
+// m[G], l[G], O[G][D], padded to 16 bytes (the last CTA bulk-copies the partials)
+__host__ __device__ inline int64_t part_floats(int G, int D) { return (2ll * G + (int64_t)G * D + 3) / 4 * 4; }
+inline int64_t ticket_bytes(int n_streams) { return ((int64_t)n_streams * 4 + 255) / 256 * 256; }
 
 struct DecodeParams {
   PoolView pv;
@@ -81,14 +84,42 @@ struct DecodeParams {
   void* out;
   int64_t out_ss, out_rs;
   int out_dtype;
+  uint32_t flags;    // SK_DECODE_* / SK_LAUNCH_PDL
+  int cps;           // CTAs per stream (gridDim.x)
+  float* part;       // [stream][cps][part_floats]
+  uint32_t* ticket;  // [stream]
 };
 
-// Ablation build (tools/decode_probe.py, never the shipped library):
-// -DSK_DEC_ABLATE_PAGES skips the page work, keeping every barrier and the merge.
-#ifdef SK_DEC_ABLATE_PAGES
-constexpr bool kAblatePages = true;
+// Timing build only (-DSK_DEC_TIMING, tools/decode_stamp_probe.py): globaltimer
+// stamps of each CTA's phases, read back with sk_debug_decode_stamps.
+#ifdef SK_DEC_TIMING
+__device__ uint64_t g_dec_stamps[4096][8];
+#define DSTAMP(i)                                                                   \
+  do {                                                                              \
+    if (threadIdx.x == 0) {                                                         \
+      uint64_t t_;                                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+      g_dec_stamps[(blockIdx.y * gridDim.x + blockIdx.x) & 4095][(i)] = t_;         \
+    }                                                                               \
+  } while (0)
+// warp-level: globaltimer + clock64 around one unit's compute (CTA 0 of stream 0)
+#define WSTAMP(i)                                                                          \
+  do {                                                                                     \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x == 0 && blockIdx.y == 0) {                   \
+      uint64_t t_, c_;                                                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_));                                   \
+      g_dec_stamps[4000 + (threadIdx.x >> 5)][2 * (i)] = t_;                               \
+      g_dec_stamps[4000 + (threadIdx.x >> 5)][2 * (i) + 1] = c_;                           \
+    }                                                                                      \
+  } while (0)
 #else
-constexpr bool kAblatePages = false;
+#define DSTAMP(i) \
+  do {            \
+  } while (0)
+#define WSTAMP(i) \
+  do {            \
+  } while (0)
 #endif
 
 // m16n8k16 MMA, fp32 accumulate.
@@ -183,87 +214,106 @@ struct RowState {
   float o[D / 16][4];  // [ct][2h + e]: channel 16ct + g + 8h, row 2j + e
 };
 
-// One whole page for one warp, computed TRANSPOSED so that the 16-row MMA
-// dimension carries tokens (QK) and channels (PV) and the group rows (<= 8)
-// sit in N = 8: S^T = K q'^T and O^T += V^T P^T, half the m16n8k16 MMAs of
-// the rows-in-M form.  The A fragments are exactly the bytes K1 already
-// stores per (token, lane%4) and (channel tile, lane) (sk_layout.cuh); P goes
-// from the S^T accumulator to the P^T operand with one movmatrix per 8x8.
+// One 32-token unit (tiles tt0, tt0+1 of a page) for one warp, computed
+// TRANSPOSED so that the 16-row MMA dimension carries tokens (QK) and
+// channels (PV) and the group rows (<= 8) sit in N = 8: S^T = K q'^T and
+// O^T += V^T P^T.  The A fragments are exactly the bytes K1 stores per
+// (token, lane%4) and (channel tile, lane) (sk_layout.cuh); P goes from the
+// S^T accumulator to the P^T operand with one movmatrix per 8x8.
 // KIND: 0 raw pages (MMA in T), 1 nibble codes, 2 byte codes (MMA in fp16).
 template <typename T, int KIND, int D, int P>
-__device__ __forceinline__ void page_attend(const uint8_t* pg, int tok_in_page, uint32_t att_mask,
-                                            const uint32_t (&qw)[D / 8], float sl2, float inv_levels,
-                                            RowState<D>& st) {
-  using MT = typename std::conditional<KIND == 0, T, __half>::type;
-  constexpr int NKS = D / 16;  // QK k-steps (16 dims)
-  constexpr int NCT = D / 16;  // PV M-tiles (16 channels)
-  constexpr int NTT = P / 16;  // 16-token tiles (QK M-tiles, PV k-steps)
-  constexpr int RB = KIND == 0 ? 2 * D : (KIND == 1 ? D / 2 : D);
-  constexpr int KW = KIND == 1 ? D / 32 : (KIND == 2 ? D / 16 : D / 8);  // words per (token, lane%4)
-  constexpr int VW = KIND == 1 ? P / 32 : (KIND == 2 ? P / 16 : P / 8);  // words per (cn, lane)
+struct UnitData {
+  static constexpr int RB = KIND == 0 ? 2 * D : (KIND == 1 ? D / 2 : D);
+  static constexpr int KW = KIND == 1 ? D / 32 : (KIND == 2 ? D / 16 : D / 8);  // words per (token, lane%4)
+  static constexpr int VW = KIND == 1 ? P / 32 : (KIND == 2 ? P / 16 : P / 8);  // words per (cn, lane), whole page
+  static constexpr int VU = KIND == 1 ? 1 : (KIND == 2 ? 2 : 4);                // of them used by one unit
+  uint32_t kw[2][2][KW];
+  uint32_t vw[D / 8][VU];
+  uint32_t kb_lo[D / 8], kb_hi[D / 8], vb_lo[D / 8], vb_hi[D / 8];
+};
+
+// Every load of one 32-token unit (tiles tt0, tt0+1 of the page in slot pg),
+// straight into registers -- issued before any math (one round trip), and
+// for the first unit before the kernel's dependency wait (PDL prologue).
+template <typename T, int KIND, int D, int P>
+__device__ __forceinline__ void unit_load(const uint8_t* pg, int tt0, UnitData<T, KIND, D, P>& u) {
+  using U = UnitData<T, KIND, D, P>;
+  constexpr int NCT = D / 16;
+  constexpr int RB = U::RB, KW = U::KW, VW = U::VW, VU = U::VU;
   const int lane = threadIdx.x & 31, g = lane >> 2, j = lane & 3;
   const uint8_t* kc = pg;
   const uint8_t* vc = pg + P * RB;
   const T* bnd = reinterpret_cast<const T*>(pg + 2 * P * RB);
-
-  // ---- loads, issued before any math (one round trip) ------------------------
   // K codes of tokens 16tt + g + 8h (A rows), this lane's dim chunk j
-  uint32_t kw[KIND == 0 ? 1 : NTT][2][KW];
-  auto load_k = [&](int tt, uint32_t (&dst)[2][KW]) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const uint8_t* src = kc + (16 * tt + 8 * h + g) * RB + j * (RB / 4);
+      const uint8_t* src = kc + (16 * (tt0 + i) + 8 * h + g) * RB + j * (RB / 4);
       if constexpr (KW == 2) {
         const uint2 v = ldg8(src);
-        dst[h][0] = v.x; dst[h][1] = v.y;
+        u.kw[i][h][0] = v.x; u.kw[i][h][1] = v.y;
       } else {
 #pragma unroll
-        for (int i = 0; i < KW / 4; ++i) {
-          const uint4 v = ldg16(src + 16 * i);
-          dst[h][4 * i] = v.x; dst[h][4 * i + 1] = v.y; dst[h][4 * i + 2] = v.z; dst[h][4 * i + 3] = v.w;
+        for (int w = 0; w < KW / 4; ++w) {
+          const uint4 v = ldg16(src + 16 * w);
+          u.kw[i][h][4 * w] = v.x; u.kw[i][h][4 * w + 1] = v.y; u.kw[i][h][4 * w + 2] = v.z; u.kw[i][h][4 * w + 3] = v.w;
         }
       }
     }
-  };
-  if constexpr (KIND != 0) {
+  // V codes of the unit's tokens: chunk (cn, lane), cn = 2ct + h
+  const int w0 = KIND == 1 ? tt0 / 2 : (KIND == 2 ? tt0 : 2 * tt0);  // first word of the unit
 #pragma unroll
-    for (int tt = 0; tt < NTT; ++tt) load_k(tt, kw[tt]);
+  for (int cn = 0; cn < 2 * NCT; ++cn) {
+    const uint8_t* src = vc + ((32 * cn + lane) * VW + w0) * 4;
+    if constexpr (VU == 1) {
+      u.vw[cn][0] = __ldg(reinterpret_cast<const uint32_t*>(src));
+    } else if constexpr (VU == 2) {
+      const uint2 v = ldg8(src);
+      u.vw[cn][0] = v.x; u.vw[cn][1] = v.y;
+    } else {
+      const uint4 v = ldg16(src);
+      u.vw[cn][0] = v.x; u.vw[cn][1] = v.y; u.vw[cn][2] = v.z; u.vw[cn][3] = v.w;
+    }
   }
   // bounds: K in kbound order (this lane's dims at j*D/4), V in vbound order
   // (channels 16ct + g + 8h at (g/2)*D/4 + 4ct + 2h + g%2)
-  uint32_t kb_lo[D / 8], kb_hi[D / 8], vb_lo[D / 8], vb_hi[D / 8];
   if constexpr (KIND != 0) {
 #pragma unroll
     for (int i = 0; i < D / 32; ++i) {
       const uint4 a = ldg16(bnd + j * (D / 4) + 8 * i), b = ldg16(bnd + D + j * (D / 4) + 8 * i);
       const uint4 c = ldg16(bnd + 2 * D + (g >> 1) * (D / 4) + 8 * i);
       const uint4 d = ldg16(bnd + 3 * D + (g >> 1) * (D / 4) + 8 * i);
-      kb_lo[4 * i] = a.x; kb_lo[4 * i + 1] = a.y; kb_lo[4 * i + 2] = a.z; kb_lo[4 * i + 3] = a.w;
-      kb_hi[4 * i] = b.x; kb_hi[4 * i + 1] = b.y; kb_hi[4 * i + 2] = b.z; kb_hi[4 * i + 3] = b.w;
-      vb_lo[4 * i] = c.x; vb_lo[4 * i + 1] = c.y; vb_lo[4 * i + 2] = c.z; vb_lo[4 * i + 3] = c.w;
-      vb_hi[4 * i] = d.x; vb_hi[4 * i + 1] = d.y; vb_hi[4 * i + 2] = d.z; vb_hi[4 * i + 3] = d.w;
+      u.kb_lo[4 * i] = a.x; u.kb_lo[4 * i + 1] = a.y; u.kb_lo[4 * i + 2] = a.z; u.kb_lo[4 * i + 3] = a.w;
+      u.kb_hi[4 * i] = b.x; u.kb_hi[4 * i + 1] = b.y; u.kb_hi[4 * i + 2] = b.z; u.kb_hi[4 * i + 3] = b.w;
+      u.vb_lo[4 * i] = c.x; u.vb_lo[4 * i + 1] = c.y; u.vb_lo[4 * i + 2] = c.z; u.vb_lo[4 * i + 3] = c.w;
+      u.vb_hi[4 * i] = d.x; u.vb_hi[4 * i + 1] = d.y; u.vb_hi[4 * i + 2] = d.z; u.vb_hi[4 * i + 3] = d.w;
     }
   }
-  // V codes: chunk (cn, lane) of the whole page, cn = 2ct + h (KIND 1/2)
-  uint32_t vw[KIND == 0 ? 1 : 2 * NCT][VW];
-  if constexpr (KIND != 0) {
-#pragma unroll
-    for (int cn = 0; cn < 2 * NCT; ++cn) {
-      const uint8_t* src = vc + (32 * cn + lane) * (VW * 4);
-      if constexpr (VW == 1) {
-        vw[cn][0] = __ldg(reinterpret_cast<const uint32_t*>(src));
-      } else if constexpr (VW == 2) {
-        const uint2 v = ldg8(src);
-        vw[cn][0] = v.x; vw[cn][1] = v.y;
-      } else {
-#pragma unroll
-        for (int i = 0; i < VW / 4; ++i) {
-          const uint4 v = ldg16(src + 16 * i);
-          vw[cn][4 * i] = v.x; vw[cn][4 * i + 1] = v.y; vw[cn][4 * i + 2] = v.z; vw[cn][4 * i + 3] = v.w;
-        }
-      }
-    }
-  }
+}
+
+// One 32-token unit (tiles tt0, tt0+1 of a page) for one warp, computed
+// TRANSPOSED so that the 16-row MMA dimension carries tokens (QK) and
+// channels (PV) and the group rows (<= 8) sit in N = 8: S^T = K q'^T and
+// O^T += V^T P^T.  The A fragments are exactly the bytes K1 stores per
+// (token, lane%4) and (channel tile, lane) (sk_layout.cuh); P goes from the
+// S^T accumulator to the P^T operand with one movmatrix per 8x8.
+// KIND: 0 raw pages (MMA in T), 1 nibble codes, 2 byte codes (MMA in fp16).
+template <typename T, int KIND, int D, int P>
+__device__ __forceinline__ void unit_compute(const UnitData<T, KIND, D, P>& u, int tt0, int tok_in_page,
+                                             uint32_t att_mask, const uint32_t (&qw)[D / 8], float sl2,
+                                             float inv_levels, RowState<D>& st) {
+  using MT = typename std::conditional<KIND == 0, T, __half>::type;
+  constexpr int NKS = D / 16;  // QK k-steps (16 dims)
+  constexpr int NCT = D / 16;  // PV M-tiles (16 channels)
+  constexpr int TT = 2;        // 16-token tiles per unit
+  const int lane = threadIdx.x & 31, g = lane >> 2, j = lane & 3;
+  const auto& kw = u.kw;
+  const auto& vw = u.vw;
+  const auto& kb_lo = u.kb_lo;
+  const auto& kb_hi = u.kb_hi;
+  const auto& vb_lo = u.vb_lo;
+  const auto& vb_hi = u.vb_hi;
 
   // ---- K side: B = q'^T with q' = q * s_k / smax (row g), qz_r = q_r . lo_k --------
   uint32_t bq[NKS][2];
@@ -305,50 +355,47 @@ __device__ __forceinline__ void page_attend(const uint8_t* pg, int tok_in_page, 
   // the S^T accumulator holds rows 2j, 2j+1: fetch their qz from lanes 8j, 8j+4
   const float qz0 = __shfl_sync(0xffffffffu, qz, 8 * j), qz1 = __shfl_sync(0xffffffffu, qz, 8 * j + 4);
 
-  // ---- S^T = K q'^T: tile tt gives tokens 16tt + g (+8), rows 2j, 2j+1 -------------
-  float sc[NTT][4];
+  // ---- S^T = K q'^T: tile i gives tokens 16(tt0+i) + g (+8), rows 2j, 2j+1 ---------
+  float sc[TT][4];
 #pragma unroll
-  for (int tt = 0; tt < NTT; ++tt) {
-    uint32_t kt[2][KW];
-    if constexpr (KIND == 0) load_k(tt, kt);
-    const uint32_t (&kr)[2][KW] = KIND == 0 ? kt : kw[KIND == 0 ? 0 : tt];
+  for (int i = 0; i < TT; ++i) {
     float c[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int ks = 0; ks < NKS; ++ks) {
       uint32_t a0, a1, a2, a3;  // (tok g, dims lo) (tok g+8, lo) (tok g, hi) (tok g+8, hi)
       const int ri0 = 2 * ks, ri1 = 2 * ks + 1;
       if constexpr (KIND == 1) {
-        a0 = nib2h(kr[0][ri0 / 4], ri0 % 4);
-        a1 = nib2h(kr[1][ri0 / 4], ri0 % 4);
-        a2 = nib2h(kr[0][ri1 / 4], ri1 % 4);
-        a3 = nib2h(kr[1][ri1 / 4], ri1 % 4);
+        a0 = nib2h(kw[i][0][ri0 / 4], ri0 % 4);
+        a1 = nib2h(kw[i][1][ri0 / 4], ri0 % 4);
+        a2 = nib2h(kw[i][0][ri1 / 4], ri1 % 4);
+        a3 = nib2h(kw[i][1][ri1 / 4], ri1 % 4);
       } else if constexpr (KIND == 2) {
-        a0 = byte2h(kr[0][ks], 0);
-        a1 = byte2h(kr[1][ks], 0);
-        a2 = byte2h(kr[0][ks], 1);
-        a3 = byte2h(kr[1][ks], 1);
+        a0 = byte2h(kw[i][0][ks], 0);
+        a1 = byte2h(kw[i][1][ks], 0);
+        a2 = byte2h(kw[i][0][ks], 1);
+        a3 = byte2h(kw[i][1][ks], 1);
       } else {
-        a0 = kr[0][ri0];
-        a1 = kr[1][ri0];
-        a2 = kr[0][ri1];
-        a3 = kr[1][ri1];
+        a0 = kw[i][0][ri0];
+        a1 = kw[i][1][ri0];
+        a2 = kw[i][0][ri1];
+        a3 = kw[i][1][ri1];
       }
       mma16816_full<MT>(c, a0, a1, a2, a3, bq[ks][0], bq[ks][1]);
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const bool ok = 16 * tt + 8 * h + g < tok_in_page;
-      sc[tt][2 * h] = ok ? (c[2 * h] * smax + qz0) * sl2 : -INFINITY;
-      sc[tt][2 * h + 1] = ok ? (c[2 * h + 1] * smax + qz1) * sl2 : -INFINITY;
+      const bool ok = 16 * (tt0 + i) + 8 * h + g < tok_in_page;
+      sc[i][2 * h] = ok ? (c[2 * h] * smax + qz0) * sl2 : -INFINITY;
+      sc[i][2 * h + 1] = ok ? (c[2 * h + 1] * smax + qz1) * sl2 : -INFINITY;
     }
   }
 
-  // ---- per-row page max, rescale, probabilities -----------------------------------
+  // ---- per-row unit max, rescale, probabilities -----------------------------------
   float tmax[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-  for (int tt = 0; tt < NTT; ++tt) {
-    tmax[0] = fmax3(tmax[0], sc[tt][0], sc[tt][2]);
-    tmax[1] = fmax3(tmax[1], sc[tt][1], sc[tt][3]);
+  for (int i = 0; i < TT; ++i) {
+    tmax[0] = fmax3(tmax[0], sc[i][0], sc[i][2]);
+    tmax[1] = fmax3(tmax[1], sc[i][1], sc[i][3]);
   }
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
@@ -364,19 +411,19 @@ __device__ __forceinline__ void page_attend(const uint8_t* pg, int tok_in_page, 
     m_new[e] = att[e] ? fmaxf(st.m[e], tmax[e]) : st.m[e];
     alpha[e] = att[e] ? exp2f(st.m[e] - m_new[e]) : 1.f;  // exp2(-inf) = 0
   }
-  uint32_t pb[NTT][2];  // P^T B fragments: (tokens 2j.., row g) / (tokens 2j+8.., row g)
+  uint32_t pb[TT][2];  // P^T B fragments: (tokens 2j.., row g) / (tokens 2j+8.., row g)
   float psum[2] = {0.f, 0.f};
 #pragma unroll
-  for (int tt = 0; tt < NTT; ++tt)
+  for (int i = 0; i < TT; ++i)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const float p0 = att[0] ? fast_exp2(sc[tt][2 * h] - m_new[0]) : 0.f;
-      const float p1 = att[1] ? fast_exp2(sc[tt][2 * h + 1] - m_new[1]) : 0.f;
+      const float p0 = att[0] ? fast_exp2(sc[i][2 * h] - m_new[0]) : 0.f;
+      const float p1 = att[1] ? fast_exp2(sc[i][2 * h + 1] - m_new[1]) : 0.f;
       const uint32_t pk = pack2<MT>(p0, p1);  // (token 16tt + 8h + g, rows 2j, 2j+1)
       const float2 pr = unpack2<MT>(pk);     // the rounded values the MMA sees
       psum[0] += pr.x;
       psum[1] += pr.y;
-      pb[tt][h] = transpose8x8(pk);
+      pb[i][h] = transpose8x8(pk);
     }
   float prow[2];
 #pragma unroll
@@ -392,44 +439,27 @@ __device__ __forceinline__ void page_attend(const uint8_t* pg, int tok_in_page, 
   // ---- O^T = alpha O^T + s_v (V^T P^T) + lo_v sum(P) -----------------------------
 #pragma unroll
   for (int ct = 0; ct < NCT; ++ct) {
-    uint32_t vt[2][KIND == 0 ? NTT * 2 : 1];
-    if constexpr (KIND == 0) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint8_t* src = vc + (32 * (2 * ct + h) + lane) * (P / 2);
-#pragma unroll
-        for (int i = 0; i < NTT / 2; ++i) {
-          const uint4 v = ldg16(src + 16 * i);
-          vt[h][4 * i] = v.x; vt[h][4 * i + 1] = v.y; vt[h][4 * i + 2] = v.z; vt[h][4 * i + 3] = v.w;
-        }
-        if constexpr (NTT % 2) {
-          const uint2 v = ldg8(src + 16 * (NTT / 2));
-          vt[h][NTT * 2 - 2] = v.x; vt[h][NTT * 2 - 1] = v.y;
-        }
-      }
-    }
     float c[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int tt = 0; tt < NTT; ++tt) {
+    for (int i = 0; i < TT; ++i) {
       uint32_t a0, a1, a2, a3;  // (ch g, tok lo) (ch g+8, lo) (ch g, hi) (ch g+8, hi)
-      const int ri0 = 2 * tt, ri1 = 2 * tt + 1;
-      if constexpr (KIND == 1) {
-        a0 = nib2h(vw[2 * ct][ri0 / 4], ri0 % 4);
-        a1 = nib2h(vw[2 * ct + 1][ri0 / 4], ri0 % 4);
-        a2 = nib2h(vw[2 * ct][ri1 / 4], ri1 % 4);
-        a3 = nib2h(vw[2 * ct + 1][ri1 / 4], ri1 % 4);
+      if constexpr (KIND == 1) {  // the unit's word: slots 2i, 2i+1 are tiles tt0+i
+        a0 = nib2h(vw[2 * ct][0], 2 * i);
+        a1 = nib2h(vw[2 * ct + 1][0], 2 * i);
+        a2 = nib2h(vw[2 * ct][0], 2 * i + 1);
+        a3 = nib2h(vw[2 * ct + 1][0], 2 * i + 1);
       } else if constexpr (KIND == 2) {
-        a0 = byte2h(vw[2 * ct][tt], 0);
-        a1 = byte2h(vw[2 * ct + 1][tt], 0);
-        a2 = byte2h(vw[2 * ct][tt], 1);
-        a3 = byte2h(vw[2 * ct + 1][tt], 1);
+        a0 = byte2h(vw[2 * ct][i], 0);
+        a1 = byte2h(vw[2 * ct + 1][i], 0);
+        a2 = byte2h(vw[2 * ct][i], 1);
+        a3 = byte2h(vw[2 * ct + 1][i], 1);
       } else {
-        a0 = vt[0][ri0];
-        a1 = vt[1][ri0];
-        a2 = vt[0][ri1];
-        a3 = vt[1][ri1];
+        a0 = vw[2 * ct][2 * i];
+        a1 = vw[2 * ct + 1][2 * i];
+        a2 = vw[2 * ct][2 * i + 1];
+        a3 = vw[2 * ct + 1][2 * i + 1];
       }
-      mma16816_full<MT>(c, a0, a1, a2, a3, pb[tt][0], pb[tt][1]);
+      mma16816_full<MT>(c, a0, a1, a2, a3, pb[i][0], pb[i][1]);
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -450,76 +480,61 @@ __device__ __forceinline__ void page_attend(const uint8_t* pg, int tok_in_page, 
   }
 }
 
-template <typename T, int KIND, int D, int P, int kCl>
+// Merge of a stream's partials (m, l, O over channel c) with the new token
+// (score s_new, value v_c) and write of the normalised output.
+template <typename T>
+__device__ __forceinline__ void finish_out(const DecodeParams& prm, int s, int rr, int c, float M, float L, float O) {
+  const int64_t oi = s * prm.out_ss + (int64_t)rr * prm.out_rs + c;
+  O /= L;
+  if (prm.out_dtype == SK_F32) reinterpret_cast<float*>(prm.out)[oi] = O;
+  else if (prm.out_dtype == SK_F16) reinterpret_cast<__half*>(prm.out)[oi] = __float2half_rn(O);
+  else reinterpret_cast<__nv_bfloat16*>(prm.out)[oi] = __float2bfloat16_rn(O);
+}
+
+template <typename T, int KIND, int D, int P>
 __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_constant__ DecodeParams prm) {
-  constexpr int QR = D / 4;
+  constexpr int UPP = P / kUnitTok;  // units per page
   __shared__ int s_sel[kMaxSel];
   __shared__ int s_extra[kWarps][kMaxExtra];
   __shared__ float s_m[kWarps][kMaxRows], s_l[kWarps][kMaxRows];
   __shared__ __align__(16) float s_o[kWarps][kMaxRows][D];
-  // the CTA's partial, read by cluster rank 0 through DSMEM
-  // inbox of this CTA's output slice: every cluster CTA pushes its partial
-  // (m, l, O[:, slice]) here through DSMEM, then arrives on inbox_bar
-  constexpr int CPC = D / kCl;  // channels finished per CTA
-  __shared__ float in_m[kCl][kMaxRows], in_l[kCl][kMaxRows];
-  __shared__ __align__(16) float in_o[kCl][kMaxRows][CPC];
-  __shared__ uint64_t inbox_bar;
-  __shared__ float s_fac[kWarps][kMaxRows], s_self[kMaxRows], s_self_m[kMaxRows], s_self_l[kMaxRows];
-
-  cg::cluster_group cluster = cg::this_cluster();
-  if (threadIdx.x == 0) {
-    mbar_init(&inbox_bar, kCl);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  // split cluster barrier: arrive now, wait right before the first remote
-  // access, so every inbox barrier is initialised without a blocking sync
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  __shared__ float s_self[kMaxRows];
+  __shared__ uint32_t s_last;
+  __shared__ uint64_t s_bar;
+  extern __shared__ __align__(16) float s_part[];  // last CTA: [cps][part_floats] (dynamic)
+  DSTAMP(0);
   const PoolView& pv = prm.pv;
   const int s = blockIdx.y;
-  const int rank = blockIdx.x;  // == cluster rank (the cluster spans grid.x)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = lane >> 2, g = r, j = lane & 3;
   const int G = prm.G;
 
-  // ---- round trip 1: header, selection, q (all independent) -----------------
+  // Programmatic dependent launch (SK_LAUNCH_PDL): let the next kernel's CTAs
+  // start their own prologue as SMs free up, and read nothing the previous
+  // kernel may write -- q, the new token, and (unless SK_DECODE_SEL_READY)
+  // the selection -- before griddepcontrol.wait.
+  const bool pdl = prm.flags & SK_LAUNCH_PDL;
+  const bool early_sel = !pdl || (prm.flags & SK_DECODE_SEL_READY);
+  if (pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // ---- round trip 1: header and selection (independent loads) ---------------
   const int n_tok = prm.tokens[s];
   const uint32_t rm_raw = prm.row_mask[s];
   // per-row streaming windows (HeadProfile.sink_blocks / local_blocks, engine.py:264-267)
   uint32_t win = (uint32_t)pv.sink | ((uint32_t)pv.local << 16);
   if (prm.row_window != nullptr && lane < G) win = __ldg(prm.row_window + (int64_t)s * G + lane);
+  if (!early_sel) asm volatile("griddepcontrol.wait;" ::: "memory");
   const int cnt_raw = prm.sel_count[s];
   const int32_t* sel = prm.sel + (int64_t)s * prm.sel_stride;
   const int sel_w = min(prm.sel_stride, kMaxSel);
-  for (int i = tid; i < sel_w; i += kDecThreads) s_sel[i] = __ldg(sel + i);
-  const bool row_ok = r < G;
-  uint32_t qw[D / 8];  // this lane's q values of row r (pairs, input dtype)
-  {
-    const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)(row_ok ? r : 0) * prm.q_rs;
-#pragma unroll
-    for (int ri = 0; ri < D / 8; ++ri) {
-      const int d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j;
-      qw[ri] = row_ok ? __ldg(reinterpret_cast<const uint32_t*>(qrow + d)) : 0u;
-    }
-  }
-  // scores of the new token (raw K, in-register; merged last, engine.py:276-277)
-  if (warp < G) {
-    const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)warp * prm.q_rs;
-    const T* kn = reinterpret_cast<const T*>(prm.k_new) + s * prm.new_ss;
-    float dot = 0.f;
-#pragma unroll
-    for (int c = lane; c < D; c += 32) dot = fmaf(DT<T>::to_f(qrow[c]), DT<T>::to_f(kn[c]), dot);
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
-    if (lane == 0) s_self[warp] = dot * prm.scale_log2;
-  }
+  for (int i = tid; i < sel_w; i += kDecThreads) s_sel[i] = __ldcg(sel + i);
   const int n_pages = (n_tok + pv.P - 1) / pv.P;
   const uint32_t gmask = (G >= 32) ? 0xffffffffu : ((1u << G) - 1u);
   const uint32_t rmask = rm_raw & gmask;
   const uint32_t smask = gmask & ~rmask;
   const int nsel = rmask ? min(cnt_raw, sel_w) : 0;
   // lane r (< G) holds row r's window; the union over streaming rows is
-  // [0, max sink) u [n - max local, n), and each page carries the mask of the
-  // streaming rows whose own window contains it
+  // [0, max sink) u [n - max local, n), and each page carries the mask of
+  // the streaming rows whose own window contains it
   const bool srow = lane < G && ((smask >> lane) & 1u);
   const int my_sink = srow ? min((int)(win & 0xFFFFu), n_pages) : 0;
   const int my_loc = srow ? max(n_pages - (int)(win >> 16), 0) : n_pages;
@@ -534,6 +549,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     return __ballot_sync(0xffffffffu, srow && (pg < my_sink || pg >= my_loc));
   };
   __syncthreads();
+  DSTAMP(1);
   // ---- the stream's page union: selection + sink/local pages it lacks.  Each
   //      warp derives it itself (a ballot over <= 32 candidates against the
   //      staged selection), so no second CTA barrier sits on the critical path.
@@ -554,9 +570,9 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     ne = min(ne, kMaxExtra);
   }
   __syncwarp();
-  const int U = kAblatePages ? 0 : nsel + ne;
+  const int NU = (nsel + ne) * UPP;  // 32-token units of the union
 
-  // ---- this warp's pages: unit u = rank + kCl * (warp + kWarps * i) -----------
+  // ---- this warp's units: u = warp index in the stream + k * (cps * kWarps) ----
   RowState<D> st;
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
@@ -569,194 +585,190 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     for (int i = 0; i < 4; ++i) st.o[ct][i] = 0.f;
   const float sl2 = prm.scale_log2;
   const float inv_levels = KIND == 0 ? 1.f : 1.f / float((1 << pv.bits) - 1);
-  constexpr int RBY = KIND == 0 ? 2 * D : (KIND == 1 ? D / 2 : D);
-  constexpr int kSlotUsed = 2 * P * RBY + (KIND == 0 ? 0 : 8 * D);  // bytes of a slot the kernel reads
   auto unit_page = [&](int u, uint32_t& um) -> int {
-    const int pg = u < nsel ? s_sel[u] : w_extra[u - nsel];
-    um = (u < nsel ? rmask : 0u) | (smask ? win_rows(pg) : 0u);
+    const int pi = u / UPP;
+    const int pg = pi < nsel ? s_sel[pi] : w_extra[pi - nsel];
+    um = (pi < nsel ? rmask : 0u) | (smask ? win_rows(pg) : 0u);
     return pg;
   };
-  // software pipeline across a warp's pages: the next page's table entry is
-  // loaded and its bytes prefetched into L2 while the current page computes
-  int u = rank + kCl * warp;
+  const int ustride = prm.cps * kWarps;
+  int u = blockIdx.x * kWarps + warp;
   int pg_next = 0;
   uint32_t um_next = 0;
   const uint8_t* slot_next = nullptr;
-  if (u < U) {
+  UnitData<T, KIND, D, P> ud;
+  if (u < NU) {
     pg_next = unit_page(u, um_next);
     slot_next = pv.slot_ptr(s, pg_next);  // round trip 2 (page table)
+    if (16 * 2 * (u % UPP) < min(P, n_tok - pg_next * P)) unit_load<T, KIND, D, P>(slot_next, 2 * (u % UPP), ud);
   }
-  for (; u < U; u += kCl * kWarps) {
+  if (pdl && early_sel) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // ---- q and the new token: the previous kernel's outputs in a model --------
+  const bool row_ok = r < G;
+  uint32_t qw[D / 8];  // this lane's q values of row r (pairs, input dtype)
+  {
+    const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)(row_ok ? r : 0) * prm.q_rs;
+#pragma unroll
+    for (int ri = 0; ri < D / 8; ++ri) {
+      const int d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j;
+      qw[ri] = row_ok ? __ldcg(reinterpret_cast<const uint32_t*>(qrow + d)) : 0u;
+    }
+  }
+  // scores of the new token (raw K, in-register; merged last, engine.py:276-277)
+  if (warp < G) {
+    const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)warp * prm.q_rs;
+    const T* kn = reinterpret_cast<const T*>(prm.k_new) + s * prm.new_ss;
+    float dot = 0.f;
+#pragma unroll
+    for (int c = lane; c < D; c += 32) dot = fmaf(DT<T>::to_f(__ldcg(qrow + c)), DT<T>::to_f(__ldcg(kn + c)), dot);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+    if (lane == 0) s_self[warp] = dot * prm.scale_log2;
+  }
+  bool first = true;
+  for (; u < NU; u += ustride) {
     const int pg = pg_next;
     const uint32_t um = um_next;
     const uint8_t* slot = slot_next;
-    const int un = u + kCl * kWarps;
-    if (un < U) {
+    const int un = u + ustride;
+    if (un < NU) {  // next unit's table entry + its bytes into L2 while this one computes
       pg_next = unit_page(un, um_next);
       slot_next = pv.slot_ptr(s, pg_next);
+      constexpr int kSlotUsed = (KIND == 0 ? 4 * P * D : (KIND == 1 ? P * D : 2 * P * D)) + (KIND == 0 ? 0 : 8 * D);
       for (int off = lane * 128; off < kSlotUsed; off += 32 * 128)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(slot_next + off));
     }
-    page_attend<T, KIND, D, P>(slot, min(P, n_tok - pg * P), um & gmask, qw, sl2, inv_levels, st);
+    const int tok_in_page = min(P, n_tok - pg * P), tt0 = 2 * (u % UPP);
+    if (16 * tt0 < tok_in_page) {  // a unit past the open page's last token holds nothing
+      if (!first) unit_load<T, KIND, D, P>(slot, tt0, ud);
+      WSTAMP(0);
+      unit_compute<T, KIND, D, P>(ud, tt0, tok_in_page, um & gmask, qw, sl2, inv_levels, st);
+      WSTAMP(1);
+    }
+    first = false;
   }
+  DSTAMP(2);
 
   // ---- merge the CTA's warps ---------------------------------------------------
-  {
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      float lt = st.l[e];
-      lt += __shfl_xor_sync(0xffffffffu, lt, 4);
-      lt += __shfl_xor_sync(0xffffffffu, lt, 8);
-      lt += __shfl_xor_sync(0xffffffffu, lt, 16);
-      if (g == 0) {
-        s_m[warp][2 * j + e] = st.m[e];
-        s_l[warp][2 * j + e] = lt;
-      }
+  for (int e = 0; e < 2; ++e) {
+    float lt = st.l[e];
+    lt += __shfl_xor_sync(0xffffffffu, lt, 4);
+    lt += __shfl_xor_sync(0xffffffffu, lt, 8);
+    lt += __shfl_xor_sync(0xffffffffu, lt, 16);
+    if (g == 0) {
+      s_m[warp][2 * j + e] = st.m[e];
+      s_l[warp][2 * j + e] = lt;
     }
-#pragma unroll
-    for (int ct = 0; ct < D / 16; ++ct)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) s_o[warp][2 * j + e][16 * ct + 8 * h + g] = st.o[ct][2 * h + e];
   }
+#pragma unroll
+  for (int ct = 0; ct < D / 16; ++ct)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) s_o[warp][2 * j + e][16 * ct + 8 * h + g] = st.o[ct][2 * h + e];
   __syncthreads();
-  if (tid < G) {
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_m[w][tid]);
-    float L = 0.f;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const float f = M == -INFINITY ? 0.f : exp2f(s_m[w][tid] - M);
-      s_fac[w][tid] = f;
-      L = fmaf(f, s_l[w][tid], L);
-    }
-    s_self_m[tid] = M;
-    s_self_l[tid] = L;
-  }
-  __syncthreads();
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every inbox is initialised
-  // ---- push this CTA's partial to the owners of each channel slice ------------
-  if (tid < kCl * G) {
-    const int r = tid / G, rr = tid % G;
-    *cluster.map_shared_rank(&in_m[rank][rr], r) = s_self_m[rr];
-    *cluster.map_shared_rank(&in_l[rank][rr], r) = s_self_l[rr];
-  }
+  DSTAMP(3);
+  // every thread merges the warps for its own output elements (no serial
+  // per-row step, one barrier): M = max_w m_w, O = sum_w 2^(m_w - M) O_w
+  const T* vn = reinterpret_cast<const T*>(prm.v_new) + s * prm.new_ss;
+  const int64_t PF = part_floats(G, D);
+  float* mine = prm.part + ((int64_t)s * prm.cps + blockIdx.x) * PF;
   for (int i = tid; i < G * D; i += kDecThreads) {
     const int rr = i / D, c = i % D;
-    float O = 0.f;
+    float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) O = fmaf(s_fac[w][rr], s_o[w][rr][c], O);
-    *cluster.map_shared_rank(&in_o[rank][rr][c % CPC], c / CPC) = O;
+    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_m[w][rr]);
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const float f = M == -INFINITY ? 0.f : fast_exp2(s_m[w][rr] - M);
+      L = fmaf(f, s_l[w][rr], L);
+      O = fmaf(f, s_o[w][rr][c], O);
+    }
+    if (prm.cps == 1) {  // the CTA holds the whole stream: finish with the new token
+      const float s_new = s_self[rr], Mt = fmaxf(M, s_new);
+      const float f = M == -INFINITY ? 0.f : fast_exp2(M - Mt), fs = fast_exp2(s_new - Mt);
+      finish_out<T>(prm, s, rr, c, Mt, fmaf(f, L, fs), fmaf(f, O, fs * DT<T>::to_f(__ldcg(vn + c))));
+    } else {
+      mine[2 * G + i] = O;
+      if (c == 0) {
+        mine[rr] = M;
+        mine[G + rr] = L;
+      }
+    }
+  }
+  if (prm.cps == 1) {
+    DSTAMP(6);
+    return;
+  }
+  // ---- partial -> workspace; the stream's last CTA merges them -----------------
+  __syncthreads();
+  if (tid == 0) {  // bar.sync + a gpu-scope acq_rel RMW: releases this partial, acquires the others
+    uint32_t t;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(prm.ticket + s) : "memory");
+    s_last = (t == (uint32_t)prm.cps - 1);
+    if (s_last) {
+      prm.ticket[s] = 0;  // re-arm for the next launch
+      // every partial of the stream (contiguous) -> shared memory, one bulk copy
+      // (generic-proxy writes of the other CTAs, acquired above, read by the async proxy)
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      const uint32_t bytes = (uint32_t)(prm.cps * PF * 4);
+      mbar_init(&s_bar, 1);
+      fence_barrier_init();
+      mbar_arrive_expect_tx(&s_bar, bytes);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(s_part)),
+                   "l"(prm.part + (int64_t)s * prm.cps * PF), "r"(bytes), "r"(smem_u32(&s_bar))
+                   : "memory");
+    }
   }
   __syncthreads();
-  if (tid < kCl) {  // one release-arrive per owner CTA
-    asm volatile("fence.acq_rel.cluster;" ::: "memory");
-    uint32_t remote;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(&inbox_bar)), "r"(tid));
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
-  }
-
-  // ---- finish channels [rank*CPC, +CPC) of every row from the inbox + the new
-  //      token (no remote reads, so no closing cluster barrier is needed) ------
-  {
-    uint32_t ok = 0;
-    while (!ok)
-      asm volatile(
-          "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], 0;\n\t"
-          "selp.b32 %0, 1, 0, P;\n\t}\n"
-          : "=r"(ok)
-          : "r"(smem_u32(&inbox_bar))
-          : "memory");
-  }
-  for (int i = tid; i < G * CPC; i += kDecThreads) {
-    const int rr = i / CPC, cc = i % CPC, c = rank * CPC + cc;
+  DSTAMP(4);
+  if (!s_last) return;
+  mbar_wait(&s_bar, 0);
+  DSTAMP(5);
+  for (int i = tid; i < G * D; i += kDecThreads) {
+    const int rr = i / D, c = i % D;
     const float s_new = s_self[rr];
     float M = s_new;
-#pragma unroll
-    for (int cr = 0; cr < kCl; ++cr) M = fmaxf(M, in_m[cr][rr]);
-    const float fs = exp2f(s_new - M);
-    float L = fs, O = fs * DT<T>::to_f(reinterpret_cast<const T*>(prm.v_new)[s * prm.new_ss + c]);
-#pragma unroll
-    for (int cr = 0; cr < kCl; ++cr) {
-      const float pm = in_m[cr][rr];
-      const float f = pm == -INFINITY ? 0.f : exp2f(pm - M);
-      L = fmaf(f, in_l[cr][rr], L);
-      O = fmaf(f, in_o[cr][rr][cc], O);
+    for (int b = 0; b < prm.cps; ++b) M = fmaxf(M, s_part[b * PF + rr]);
+    const float fs = fast_exp2(s_new - M);
+    float L = fs, O = fs * DT<T>::to_f(__ldcg(vn + c));
+#pragma unroll 4
+    for (int b = 0; b < prm.cps; ++b) {
+      const float pm = s_part[b * PF + rr];
+      const float f = pm == -INFINITY ? 0.f : fast_exp2(pm - M);
+      L = fmaf(f, s_part[b * PF + G + rr], L);
+      O = fmaf(f, s_part[b * PF + 2 * G + i], O);
     }
-    O /= L;
-    const int64_t oi = s * prm.out_ss + (int64_t)rr * prm.out_rs + c;
-    if (prm.out_dtype == SK_F32) reinterpret_cast<float*>(prm.out)[oi] = O;
-    else if (prm.out_dtype == SK_F16) reinterpret_cast<__half*>(prm.out)[oi] = __float2half_rn(O);
-    else reinterpret_cast<__nv_bfloat16*>(prm.out)[oi] = __float2bfloat16_rn(O);
+    finish_out<T>(prm, s, rr, c, M, L, O);
   }
+  DSTAMP(6);
 }
 
-template <typename T, int KIND, int D, int P, int CL>
-int launch_cl(const DecodeParams& prm, int n_streams, cudaStream_t st) {
+template <typename T, int KIND, int D, int P>
+int launch_one(const DecodeParams& prm, int n_streams, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(CL, n_streams, 1);
+  cfg.gridDim = dim3(prm.cps, n_streams, 1);
   cfg.blockDim = dim3(kDecThreads, 1, 1);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = prm.cps > 1 ? (size_t)prm.cps * part_floats(prm.G, D) * 4 : 0;
+  if (cfg.dynamicSmemBytes > 0)  // static + dynamic exceeds the 48 KB default
+    cudaFuncSetAttribute(decode_kernel<T, KIND, D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)cfg.dynamicSmemBytes);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, KIND, D, P, CL>, prm);
+  cfg.numAttrs = (prm.flags & SK_LAUNCH_PDL) ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, KIND, D, P>, prm);
   if (e != cudaSuccess) {
     set_error(std::string("decode_kernel: ") + cudaGetErrorString(e));
     return SK_ECUDA;
   }
   SK_CHECK_LAUNCH("decode_kernel");
   return SK_OK;
-}
-
-// A non-portable 16-CTA cluster per stream when the streams are few enough
-// that 16 x n_streams CTAs (one per SM) fit as co-resident clusters: twice the
-// warps per stream, so a 128k union of ~66 pages is one page per warp.
-#ifndef SK_DEC_MAX_CLUSTER
-#define SK_DEC_MAX_CLUSTER 16
-#endif
-template <typename T, int KIND, int D, int P>
-bool cluster16_fits(int n_streams) {
-  if (SK_DEC_MAX_CLUSTER < 16 || n_streams > 9) return false;
-  static int max_clusters = -1;  // per template instance (kernel)
-  if (max_clusters < 0) {
-    auto kern = decode_kernel<T, KIND, D, P, 16>;
-    max_clusters = 0;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(16, 1, 1);
-      cfg.blockDim = dim3(kDecThreads, 1, 1);
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = 16;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess) max_clusters = n;
-    }
-    cudaGetLastError();  // clear a refused attribute / query
-  }
-  return n_streams <= max_clusters;
-}
-
-template <typename T, int KIND, int D, int P>
-int launch_one(const DecodeParams& prm, int n_streams, cudaStream_t st) {
-  if (cluster16_fits<T, KIND, D, P>(n_streams)) return launch_cl<T, KIND, D, P, 16>(prm, n_streams, st);
-  switch (cluster_for(n_streams)) {
-    case 8: return launch_cl<T, KIND, D, P, 8>(prm, n_streams, st);
-    case 4: return launch_cl<T, KIND, D, P, 4>(prm, n_streams, st);
-    case 2: return launch_cl<T, KIND, D, P, 2>(prm, n_streams, st);
-    default: return launch_cl<T, KIND, D, P, 1>(prm, n_streams, st);
-  }
 }
 
 template <typename T, int KIND>
@@ -777,12 +789,21 @@ int launch_kind(const DecodeParams& prm, int n_streams, cudaStream_t st) {
 }  // namespace
 }  // namespace sk
 
+extern "C" int64_t sk_decode_workspace(int32_t n_streams, int32_t group_rows, int32_t head_dim) {
+  using namespace sk;
+  if (n_streams < 1 || group_rows < 1 || head_dim < 1) return 0;
+  // n x decode_cps(n) <= max(SMs, n): one buffer also serves launches over a subset of the streams
+  const int64_t parts = (int64_t)(device_sm_count() > n_streams ? device_sm_count() : n_streams) + kMaxCps;
+  return ticket_bytes(n_streams) + parts * part_floats(group_rows, head_dim) * 4;
+}
+
 extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
                               int64_t q_stream_stride, int64_t q_row_stride, const void* k_new, const void* v_new,
                               int64_t new_stream_stride, const uint32_t* row_mask, const uint32_t* row_window,
                               const int32_t* sel, const int32_t* sel_count, int32_t sel_stride, int32_t* tokens,
                               float softmax_scale, void* out, int64_t out_stream_stride, int64_t out_row_stride,
-                              int32_t out_dtype, int32_t append_new, void* stream) {
+                              int32_t out_dtype, uint32_t flags, void* workspace, int64_t workspace_bytes,
+                              void* stream) {
   using namespace sk;
   int rc = check_pool(pool);
   if (rc) return rc;
@@ -795,6 +816,10 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   SK_CHECK_ARG(q_row_stride % 2 == 0 && q_stream_stride % 2 == 0, "decode: q strides must be even");
   SK_CHECK_ARG(reinterpret_cast<uintptr_t>(pool->arena) % 16 == 0 && pool->slot_bytes % 16 == 0,
                "decode: arena slots must be 16-byte aligned");
+  SK_CHECK_ARG(pool->page_size % kUnitTok == 0, "decode: page size must be a multiple of 32");
+  SK_CHECK_ARG(workspace != nullptr &&
+                   workspace_bytes >= sk_decode_workspace(n_streams, group_rows, pool->head_dim),
+               "decode: workspace missing or smaller than sk_decode_workspace()");
   DecodeParams prm;
   prm.pv = make_view(*pool);
   prm.G = group_rows;
@@ -815,6 +840,11 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
   prm.out_ss = out_stream_stride;
   prm.out_rs = out_row_stride;
   prm.out_dtype = out_dtype;
+  prm.flags = flags;
+  // units: at most the selection width (+ the window) pages of P / 32 units each
+  prm.cps = decode_cps(n_streams, (sel_stride + pool->sink + pool->local) * (pool->page_size / kUnitTok));
+  prm.ticket = static_cast<uint32_t*>(workspace);
+  prm.part = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + ticket_bytes(n_streams));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int kind = pool->bits == 0 ? 0 : (pool->bits <= 4 ? 1 : 2);
   int rc2;
@@ -826,8 +856,18 @@ extern "C" int sk_decode_attn(const sk_pool* pool, int32_t n_streams, int32_t gr
                     : (kind == 1 ? launch_kind<__nv_bfloat16, 1>(prm, n_streams, st)
                                  : launch_kind<__nv_bfloat16, 2>(prm, n_streams, st));
   }
-  if (rc2 != SK_OK || !append_new) return rc2;
+  if (rc2 != SK_OK || !(flags & SK_DECODE_APPEND)) return rc2;
   // the new token is appended by K1's one-token kernel right behind the
   // attention (stream order: every read of its page has completed)
   return append_launch(pool, n_streams, k_new, v_new, new_stream_stride, 0, tokens, 1, 1, st);
 }
+
+#ifdef SK_DEC_TIMING
+extern "C" int sk_debug_decode_stamps(uint64_t* host_out) {  // 4096 x 8 u64
+  return cudaMemcpyFromSymbol(host_out, sk::g_dec_stamps, sizeof(sk::g_dec_stamps)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int sk_debug_decode_stamps_clear() {
+  static uint64_t zero[4096][8];
+  return cudaMemcpyToSymbol(sk::g_dec_stamps, zero, sizeof(zero)) == cudaSuccess ? 0 : 1;
+}
+#endif

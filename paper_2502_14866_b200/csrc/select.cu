@@ -1,30 +1,44 @@
 // K2 -- hierarchical page selection (LServe Eq. 2).
 //
 // Replaces score_pages / _stacked_stats / pinned_pages / select_pages
-// (reference selector.py:39-108) in ONE kernel, grid (page chunks, streams):
+// (reference selector.py:39-108) in ONE kernel, grid (page chunks, streams).
+// The reference ranks pages by an fp64 score; fp64 on every page is what made
+// the round-1 kernel slow (conversions + DFMA + fp64 butterflies, 38 us for
+// the 33.6 MB of a 128k layer).  Here the exact fp64 score is only computed
+// where it can change the answer:
 //
-// Scoring (HBM-bound).  Each warp owns kPagesPerWarp consecutive physical
-//   pages and streams their contiguous (k_min, k_max) rows through a
-//   double-buffered pair of shared-memory slots with 1-D bulk copies
-//   (cp.async.bulk, mbarrier completion): the copy of batch i+1 is in flight
-//   while batch i is scored, so the selector's 33.6 MB at 128k is read at
-//   close to HBM rate by ~1 CTA per SM.  Each lane scores its D/32 channels
-//   of every logical page in fp64:
-//       score(r, j) = sum_c q+_rc * kmax_jc + q-_rc * kmin_jc
-//   (q+ = max(q,0), q- = min(q,0): one of the two products is exactly 0, so
-//   each term equals the reference's max(q*kmax, q*kmin); fp16 products are
-//   exact in fp64 and the sums are exact for fp16-valued inputs, matching
-//   the reference's BLAS centre/radius form bit-for-bit -- SURVEY Appendix
-//   A.4).  A multi-value butterfly reduces all (row, logical page) sums of
-//   the warp at once; the physical-page score is their max over retrieval
-//   rows and logical pages.  Only the stream's retrieval rows are computed.
+// Phase A (every CTA, HBM-bound).  Eq. 2 as a tensor-core contraction:
+//     score(j, r) = sum_c q-_rc kmin_jc + q+_rc kmax_jc
+//   (q- = min(q, 0), q+ = max(q, 0): one of the two products is exactly 0,
+//   so each term is the reference's max(q kmax, q kmin)).  A = the stats rows
+//   of 16 logical pages (M) over the 2D channels [kmin | kmax] (K), loaded
+//   straight from HBM into registers, 128-bit and fully coalesced; B = the
+//   retrieval rows' [q- | q+] (N = 8 rows per n-tile), staged once per CTA in
+//   shared memory in the same channel permutation as A.  m16n8k16 MMAs with
+//   fp32 accumulation: every product of two fp16/bf16 values is exact in
+//   fp32, only the sums round.  A second MMA of |A| and |B| gives
+//   sum_c |q_c k_c|, and the page's error bound is
+//       err = 2^-12 * sum|t| + 1e-30
+//   (fp32 summation of <= 256 exact terms errs by < 256 * 2^-23 * sum|t| =
+//   2^-15 sum|t| even with truncating accumulation: 8x margin; the absolute
+//   term covers underflow).  A non-finite bound (bf16 overflow) makes the
+//   page undecidable in fp32 -> err = inf.  The physical page keeps the max
+//   score / max bound over its logical pages and rows: (score, err) -> ws.
 //
-// Top-k (the last CTA of each stream, found with an acq_rel ticket).  Radix
-//   select of the (K - |pins|)-th largest score among non-pinned pages on the
-//   order-preserving 64-bit image of the fp64 score, starting at the first
-//   byte where the candidates' keys differ; ties go to the lower page index
-//   (selector.py:106); union with the pins; ascending compaction by a
-//   block-wide scan over page order.
+// Phase B (the stream's last CTA, found with an acq_rel ticket).  With T =
+//   the K'-th largest approximate score (K' = K - |pins|, radix select on the
+//   order-preserving 32-bit image) and E = the largest bound:
+//     approx > T + 2E  -> certainly among the top K' (true score > true K'-th)
+//     approx < T - 2E  -> certainly not
+//     otherwise        -> the band: rescored EXACTLY in fp64 (the round-1
+//                         arithmetic, sum_c q+ kmax + q- kmin, bit-identical
+//                         to the reference on fp16/bf16-valued inputs --
+//                         SURVEY Appendix A.4) and ranked by (score desc,
+//                         page index asc), selector.py:106.
+//   A typical 128k band holds a handful of pages.  If it exceeds kBandCap
+//   (massive ties, overflow) every page is scored exactly and the exact
+//   radix select of round 1 (topk_exact) decides: slower, same answer.
+// Output: pins + chosen pages, ascending (block scan over page order).
 #include <cstdlib>
 
 #include "sk_common.cuh"
@@ -33,40 +47,96 @@
 namespace sk {
 namespace {
 
-constexpr int kScoreThreads = 256;
-constexpr int kScoreWarps = kScoreThreads / 32;
-constexpr int kBatchesPerWarp = 4;  // slots a warp streams through
-constexpr int kTopkThreads = kScoreThreads;
-constexpr int kTopkWarps = kTopkThreads / 32;
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxRows = 32;         // retrieval rows per stream (group rows)
+constexpr int kBandCap = 256;        // band pages resolved by the fast path
+constexpr int kRadixBits = 11;       // fast-path radix digit (2048 bins)
+constexpr int kNB = 1 << kRadixBits;
+constexpr float kErrRel = 1.0f / 4096.0f;  // 2^-12
+constexpr float kErrAbs = 1e-30f;
 
-__device__ __forceinline__ int pins_of(int n, int* pin) {  // selector.py:75-78
-  int c = 0;
-  pin[c++] = 0;
-  int a = n - 2 > 0 ? n - 2 : 0;
-  if (a != 0) pin[c++] = a;
-  if (n - 1 != 0 && n - 1 != a) pin[c++] = n - 1;
-  return c;
-}
+struct SelParams {
+  PoolView pv;
+  const void* q;
+  int64_t q_ss, q_rs;
+  const uint32_t* row_mask;
+  const int32_t* tokens;
+  const uint8_t* invoke;
+  int K;            // budget pages
+  int group_rows;
+  float2* approx;   // [stream][ws_pages] (fp32 score, error bound) of phase A
+  double* exact;    // [stream][ws_pages] fp64 scores of the slow path
+  uint32_t* ticket;
+  int ws_pages;
+  int tiles_per_warp;
+  int32_t* sel_out;
+  int32_t* sel_count;
+  int sel_stride;
+  int smem_bytes;
+  uint32_t flags;  // SK_LAUNCH_PDL
+};
+
 __device__ __forceinline__ bool is_pin(int i, int n) { return i == 0 || i == n - 1 || i == (n - 2 > 0 ? n - 2 : 0); }
+__device__ __forceinline__ int n_pins(int n) { return n <= 1 ? 1 : (n == 2 ? 2 : 3); }  // selector.py:75-78
 
-// Order-preserving unsigned image of a double (larger score -> larger key).
-// Never 0 for a real score, so 0 marks "not a candidate".
+// Order-preserving unsigned images (larger value -> larger key; never 0 for a
+// finite value, so 0 marks "not a candidate").
 __device__ __forceinline__ uint64_t order_key(double x) {
   x = x + 0.0;  // -0.0 -> +0.0 (equal scores tie on the index, like Python's sort)
   uint64_t u = __double_as_longlong(x);
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
+__device__ __forceinline__ uint32_t order_key32(float x) {
+  x = x + 0.0f;
+  uint32_t u = __float_as_uint(x);
+  return (u >> 31) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key32_value(uint32_t k) {
+  return __uint_as_float((k >> 31) ? (k & 0x7FFFFFFFu) : ~k);
+}
 
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
+template <typename T>
+__device__ __forceinline__ void mma_f32(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                        uint32_t b0, uint32_t b1) {
+  if constexpr (std::is_same<T, __half>::value) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  } else {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  }
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {  // read once: no L1 allocation
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+// |x| of both halves.  volatile: keeps the masking inside the n-tile loop
+// (hoisted, the 2 x 2D/2 masked words would double the live registers).
+__device__ __forceinline__ uint32_t abs2(uint32_t x) {
+  uint32_t y;
+  asm volatile("and.b32 %0, %1, 0x7FFF7FFF;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t word_of(const uint4& v, int w) {
+  return w == 0 ? v.x : (w == 1 ? v.y : (w == 2 ? v.z : v.w));
 }
 
 // NV values per lane; after the call lane l holds the full-warp sum of value
 // index (l >> (5 - log2 NV)) in v[0].  Step OFF halves the live values: the
 // lane with bit OFF set keeps the upper half, its partner the lower half.
+// Every value is summed over the xor tree 16, 8, 4, 2, 1 -- the same
+// pairing as a plain xor reduction.
 template <int NV, int OFF>
 struct Butterfly {
   static __device__ __forceinline__ void run(double* v, int lane) {
@@ -86,302 +156,167 @@ struct Butterfly {
   }
 };
 
-// fp16/bf16 bit patterns -> exact doubles
-template <typename T>
-__device__ __forceinline__ void to_f64x4(uint2 w, double* o) {
-  const float2 a = DT<T>::to_f2(w.x), b = DT<T>::to_f2(w.y);
-  o[0] = a.x;
-  o[1] = a.y;
-  o[2] = b.x;
-  o[3] = b.y;
-}
-
-// Retrieval rows [rbase, rbase + RMAX) for this lane's channels.  Up to two
-// rows use the sign-select form max(q*kmax, q*kmin) = q * (q > 0 ? kmax :
-// kmin): qa = q (fp64) and per 32-bit word of stats a mask picking k_max
-// where q > 0, so each (row, channel) costs one conversion and one DFMA.
-// Four rows share the converted k_min/k_max instead: qa = q+, qb = q-.
-// Either way the fp64 sum sees exactly the same non-zero terms in the same
-// order (sum over channels of q+*kmax + q-*kmin), so scores are identical.
-template <typename T, int RMAX>
-__device__ __forceinline__ void load_rows(const T* q, int64_t q_rs, uint32_t rmask, int rbase, int rows, int D,
-                                          double (&qd)[RMAX][4], double (&qb)[RMAX][4], uint32_t (&qsel)[RMAX][2]) {
-  const int lane = threadIdx.x & 31, cpl = D / 32;
-  uint32_t mbits = rmask;
-  for (int r = 0; r < rbase; ++r) mbits &= mbits - 1;
+// ---- exact fp64 physical-page score (warp-cooperative) ------------------------
+// max over the retrieval rows and the page's logical pages of
+// sum_c q_c * (q_c > 0 ? kmax_c : kmin_c), each lane summing its D/32
+// channels in order before the butterfly -- the round-1 arithmetic.
+template <typename T, int D>
+__device__ double exact_page_score(const PoolView& pv, int s, int page, int n_log, const T* qs, int64_t q_rs,
+                                   const int* row_idx, int rows) {
+  constexpr int CPL = D / 32;
+  using W = typename std::conditional<CPL == 4, uint2, uint32_t>::type;  // CPL values of T
+  const int lane = threadIdx.x & 31;
+  const int LP = pv.P / pv.L;
+  const int la = page * LP, nl = min(la + LP, n_log) - la;
+  const int V = rows * nl;
+  double best = -INFINITY;
+  for (int v0 = 0; v0 < V; v0 += 8) {
+    W wq[8], wmin[8], wmax[8];  // every load of the chunk issued before any math
 #pragma unroll
-  for (int r = 0; r < RMAX; ++r) {
-    const int g = __ffs(mbits) - 1;
-    const bool ok = rbase + r < rows && g >= 0;
-    if (ok) mbits &= mbits - 1;
-    const T* qr = q + (int64_t)(ok ? g : 0) * q_rs + lane * cpl;
-    qsel[r][0] = qsel[r][1] = 0u;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const double x = (ok && c < cpl) ? (double)DT<T>::to_f(qr[c]) : 0.0;
-      if constexpr (RMAX <= 2) {
-        qd[r][c] = x;
-        if (x > 0.0) qsel[r][c >> 1] |= (c & 1) ? 0xFFFF0000u : 0x0000FFFFu;
-      } else {
-        qd[r][c] = x > 0.0 ? x : 0.0;
-        qb[r][c] = x < 0.0 ? x : 0.0;
-      }
+    for (int jj = 0; jj < 8; ++jj) {
+      const int vi = min(v0 + jj, V - 1);
+      const int r = vi / nl, l = la + vi % nl;
+      const T* st = reinterpret_cast<const T*>(pv.stats_ptr(s, l)) + lane * CPL;
+      wq[jj] = *reinterpret_cast<const W*>(qs + (int64_t)row_idx[r] * q_rs + lane * CPL);
+      wmin[jj] = __ldcg(reinterpret_cast<const W*>(st));
+      wmax[jj] = __ldcg(reinterpret_cast<const W*>(st + D));
     }
-  }
-}
-
-template <typename T, int RMAX>
-__device__ __forceinline__ void row_scores(uint2 wmin, uint2 wmax, const double (&qd)[RMAX][4],
-                                           const double (&qb)[RMAX][4], const uint32_t (&qsel)[RMAX][2],
-                                           double* acc_out) {
-  if constexpr (RMAX > 2) {
-    double kmin[4], kmax[4];
-    to_f64x4<T>(wmin, kmin);
-    to_f64x4<T>(wmax, kmax);
+    double v[8];
 #pragma unroll
-    for (int r = 0; r < RMAX; ++r) {
+    for (int jj = 0; jj < 8; ++jj) {
+      const T* qv = reinterpret_cast<const T*>(&wq[jj]);
+      const T* kn = reinterpret_cast<const T*>(&wmin[jj]);
+      const T* kx = reinterpret_cast<const T*>(&wmax[jj]);
       double acc = 0.0;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        acc = fma(qd[r][c], kmax[c], acc);
-        acc = fma(qb[r][c], kmin[c], acc);
+      for (int c = 0; c < CPL; ++c) {
+        const double qd = (double)DT<T>::to_f(qv[c]);
+        acc = fma(qd, (double)DT<T>::to_f(qd > 0.0 ? kx[c] : kn[c]), acc);
       }
-      acc_out[r] = acc;
+      v[jj] = acc;
     }
-    return;
+    Butterfly<8, 16>::run(v, lane);
+    double mine = (v0 + (lane >> 2) < V) ? v[0] : -INFINITY;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) mine = fmax(mine, __shfl_xor_sync(0xffffffffu, mine, off));
+    best = fmax(best, mine);
   }
+  return best;
+}
+
+// ---- phase A: approximate scores + bounds of this warp's tiles ----------------
+// Tile = 16 logical pages.  Thread (g = lane/4, t = lane%4) loads logical
+// pages g and g+8 of the tile, bytes [64i + 16t, +16) of each 2D-channel row
+// for i < 2D/32 (each load instruction covers 8 x 64 contiguous bytes), and
+// k-step ks uses words 2(ks&1), 2(ks&1)+1 of chunk ks/2 -- i.e. the channel
+// permutation ch(ks, k) = (ks/2)*32 + t*8 + 4(ks&1) + {0,1 | 2,3}; bfrag holds
+// q' = [q- | q+] in the same permutation (built in select_kernel).
+template <typename T, int D>
+__device__ __forceinline__ void load_tile(const SelParams& p, int s, int n_log, int ti, uint4 (&a)[2][D / 16]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int l0 = ti * 16 + g, l1 = l0 + 8;
+  const T* r0 = reinterpret_cast<const T*>(p.pv.stats_ptr(s, min(l0, n_log - 1))) + t * 8;
+  const T* r1 = reinterpret_cast<const T*>(p.pv.stats_ptr(s, min(l1, n_log - 1))) + t * 8;
 #pragma unroll
-  for (int r = 0; r < RMAX; ++r) {
-    uint2 w;
-    w.x = (wmax.x & qsel[r][0]) | (wmin.x & ~qsel[r][0]);
-    w.y = (wmax.y & qsel[r][1]) | (wmin.y & ~qsel[r][1]);
-    double k[4];
-    to_f64x4<T>(w, k);
-    double acc = 0.0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc = fma(qd[r][c], k[c], acc);
-    acc_out[r] = acc;
+  for (int i = 0; i < D / 16; ++i) {
+    a[0][i] = ldg_stream(r0 + i * 32);
+    a[1][i] = ldg_stream(r1 + i * 32);
   }
 }
 
-// Scores of the np pages staged in sbuf (nl_rel valid logical pages) for
-// rows [rbase, rbase + RMAX); lane 0 writes (first row chunk) or max-merges
-// (later chunks) each page's score into out[].  LPC logical pages per
-// butterfly pass (RMAX * LPC <= 16).
-template <typename T, int RMAX, int LPC>
-__device__ __forceinline__ void score_batch(const uint8_t* sbuf, int np, int lp_per, int nl_rel, int D,
-                                            const double (&qd)[RMAX][4], const double (&qb)[RMAX][4], const uint32_t (&qsel)[RMAX][2], int rbase,
-                                            int rows, double* out) {
-  constexpr int NV = RMAX * LPC;
-  const int lane = threadIdx.x & 31;
-  const int cpl = D / 32;
-  const int row_bytes = 2 * D * 2;  // (k_min, k_max) of one logical page
-  for (int pi = 0; pi < np; ++pi) {
-    double best = -INFINITY;
-    for (int l0 = 0; l0 < lp_per; l0 += LPC) {
-      double v[NV];
+// The warp's first tile arrives in `a` (its loads were issued before the B
+// fragments were built, so that DRAM round trip overlaps the q loads).
+template <typename T, int D, int NT>
+__device__ __forceinline__ void score_tiles(const SelParams& p, int s, int n_log, int n_pages, int rows,
+                                            const uint2* bfrag, float2* approx, uint4 (&a)[2][D / 16]) {
+  constexpr int KS = D / 8;     // k-steps over 2D channels
+  const int LP = p.pv.P / p.pv.L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int n_tiles = (n_log + 15) >> 4;
+  const int tile0 = (blockIdx.x * kWarps + warp) * p.tiles_per_warp;
+  const int tile1 = min(tile0 + p.tiles_per_warp, n_tiles);
+  float run_v = -INFINITY, run_e = 0.f;  // LP = 32: a page spans two tiles of this warp
+  for (int ti = tile0; ti < tile1; ++ti) {
+    const int l0 = ti * 16 + g, l1 = l0 + 8;
+    if (ti != tile0) load_tile<T, D>(p, s, n_log, ti, a);
+    // n-tiles innermost: each k-step's |A| words are formed once and die with it
+    float c[NT][4], m[NT][4];
 #pragma unroll
-      for (int jj = 0; jj < LPC; ++jj) {
-        const int lrel = pi * lp_per + l0 + jj;
-        const T* st = reinterpret_cast<const T*>(sbuf + (int64_t)min(lrel, nl_rel - 1) * row_bytes);
-        uint2 wmin, wmax;
-        if (cpl == 4) {
-          wmin = *reinterpret_cast<const uint2*>(st + lane * 4);
-          wmax = *reinterpret_cast<const uint2*>(st + D + lane * 4);
-        } else {
-          wmin = make_uint2(*reinterpret_cast<const uint32_t*>(st + lane * 2), 0u);
-          wmax = make_uint2(*reinterpret_cast<const uint32_t*>(st + D + lane * 2), 0u);
-        }
-        double acc[RMAX];
-        row_scores<T, RMAX>(wmin, wmax, qd, qb, qsel, acc);
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int r = 0; r < RMAX; ++r) v[r * LPC + jj] = acc[r];
+      for (int e = 0; e < 4; ++e) c[nt][e] = m[nt][e] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int i = ks >> 1, w = (ks & 1) * 2;
+      const uint32_t a0 = word_of(a[0][i], w), a1 = word_of(a[1][i], w);
+      const uint32_t a2 = word_of(a[0][i], w + 1), a3 = word_of(a[1][i], w + 1);
+      const uint32_t m0 = abs2(a0), m1 = abs2(a1), m2 = abs2(a2), m3 = abs2(a3);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const uint2 b = bfrag[(nt * KS + ks) * 32 + lane];
+        mma_f32<T>(c[nt], a0, a1, a2, a3, b.x, b.y);
+        mma_f32<T>(m[nt], m0, m1, m2, m3, abs2(b.x), abs2(b.y));
       }
-      Butterfly<NV, 16>::run(v, lane);
-      const int idx = lane >> (6 - __ffs(NV));  // value index owned by this lane
-      const int r = idx / LPC, jj = idx % LPC;
-      const bool valid = rbase + r < rows && l0 + jj < lp_per && pi * lp_per + l0 + jj < nl_rel;
-      double mine = valid ? v[0] : -INFINITY;
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) mine = fmax(mine, __shfl_xor_sync(0xffffffffu, mine, off));
-      best = fmax(best, mine);
     }
-    if (lane == 0) out[pi] = rbase == 0 ? best : fmax(out[pi], best);
+    // accumulator: c0/c1 = (page g, rows 2t, 2t+1), c2/c3 = (page g+8, ...)
+    float v0 = -INFINITY, v1 = -INFINITY, e0 = 0.f, e1 = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (nt * 8 + 2 * t + e >= rows) continue;
+        const bool f0 = isfinite(m[nt][e]), f1 = isfinite(m[nt][2 + e]);
+        v0 = fmaxf(v0, f0 ? c[nt][e] : 0.f);
+        e0 = fmaxf(e0, f0 ? fmaf(m[nt][e], kErrRel, kErrAbs) : INFINITY);
+        v1 = fmaxf(v1, f1 ? c[nt][2 + e] : 0.f);
+        e1 = fmaxf(e1, f1 ? fmaf(m[nt][2 + e], kErrRel, kErrAbs) : INFINITY);
+      }
+    if (l0 >= n_log) { v0 = -INFINITY; e0 = 0.f; }
+    if (l1 >= n_log) { v1 = -INFINITY; e1 = 0.f; }
+    // rows: reduce over the quad
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+      v0 = fmaxf(v0, __shfl_xor_sync(0xffffffffu, v0, off));
+      v1 = fmaxf(v1, __shfl_xor_sync(0xffffffffu, v1, off));
+      e0 = fmaxf(e0, __shfl_xor_sync(0xffffffffu, e0, off));
+      e1 = fmaxf(e1, __shfl_xor_sync(0xffffffffu, e1, off));
+    }
+    float2* out = approx + (int64_t)s * p.ws_pages;
+    if (LP < 16) {
+      // logical pages of one physical page: lanes whose g differ in the low log2(LP) bits
+      for (int off = 4; off < 4 * LP; off <<= 1) {
+        v0 = fmaxf(v0, __shfl_xor_sync(0xffffffffu, v0, off));
+        v1 = fmaxf(v1, __shfl_xor_sync(0xffffffffu, v1, off));
+        e0 = fmaxf(e0, __shfl_xor_sync(0xffffffffu, e0, off));
+        e1 = fmaxf(e1, __shfl_xor_sync(0xffffffffu, e1, off));
+      }
+      if (t == 0 && g % LP == 0) {
+        const int pg0 = l0 / LP, pg1 = l1 / LP;
+        if (l0 < n_log && pg0 < p.ws_pages) out[pg0] = make_float2(v0, e0);
+        if (l1 < n_log && pg1 < p.ws_pages) out[pg1] = make_float2(v1, e1);
+      }
+    } else {
+      float v = fmaxf(v0, v1), e = fmaxf(e0, e1);
+#pragma unroll
+      for (int off = 4; off <= 16; off <<= 1) {
+        v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+        e = fmaxf(e, __shfl_xor_sync(0xffffffffu, e, off));
+      }
+      run_v = fmaxf(run_v, v);
+      run_e = fmaxf(run_e, e);
+      const int tpp = LP / 16;
+      if ((ti % tpp) == tpp - 1 || ti == n_tiles - 1) {
+        const int pg = ti / tpp;
+        if (lane == 0 && pg < n_pages && pg < p.ws_pages) out[pg] = make_float2(run_v, run_e);
+        run_v = -INFINITY;
+        run_e = 0.f;
+      }
+    }
   }
 }
 
-// Grouped form for LP = P/L logical pages per physical page with RMAX * LP
-// dividing 32: PG = 32 / (RMAX * LP) physical pages share one butterfly, so
-// the dependent shuffle chain (5 butterfly levels + log2(32/PG) max levels)
-// is paid once per PG pages instead of once per page.
-template <typename T, int RMAX, int LP>
-__device__ __forceinline__ void score_batch_grouped(const uint8_t* sbuf, int np, int nl_rel, int D,
-                                                    const double (&qd)[RMAX][4], const double (&qb)[RMAX][4],
-                                                    const uint32_t (&qsel)[RMAX][2], int rbase, int rows,
-                                                    double* out) {
-  constexpr int PG = 32 / (RMAX * LP);
-  constexpr int NV = 32;
-  const int lane = threadIdx.x & 31;
-  const int cpl = D / 32;
-  const int row_bytes = 2 * D * 2;
-  for (int g0 = 0; g0 < np; g0 += PG) {
-    double v[NV];
-#pragma unroll
-    for (int pg = 0; pg < PG; ++pg) {
-#pragma unroll
-      for (int lp = 0; lp < LP; ++lp) {
-        const int lrel = (g0 + pg) * LP + lp;
-        const T* st = reinterpret_cast<const T*>(sbuf + (int64_t)min(lrel, nl_rel - 1) * row_bytes);
-        uint2 wmin, wmax;
-        if (cpl == 4) {
-          wmin = *reinterpret_cast<const uint2*>(st + lane * 4);
-          wmax = *reinterpret_cast<const uint2*>(st + D + lane * 4);
-        } else {
-          wmin = make_uint2(*reinterpret_cast<const uint32_t*>(st + lane * 2), 0u);
-          wmax = make_uint2(*reinterpret_cast<const uint32_t*>(st + D + lane * 2), 0u);
-        }
-        double acc[RMAX];
-        row_scores<T, RMAX>(wmin, wmax, qd, qb, qsel, acc);
-#pragma unroll
-        for (int r = 0; r < RMAX; ++r) v[(pg * RMAX + r) * LP + lp] = acc[r];
-      }
-    }
-    Butterfly<NV, 16>::run(v, lane);  // lane l now holds value l
-    const int pg = lane / (RMAX * LP), r = (lane / LP) % RMAX, lp = lane % LP;
-    const bool valid = rbase + r < rows && g0 + pg < np && (g0 + pg) * LP + lp < nl_rel;
-    double mine = valid ? v[0] : -INFINITY;
-#pragma unroll
-    for (int off = 1; off < RMAX * LP; off <<= 1) mine = fmax(mine, __shfl_xor_sync(0xffffffffu, mine, off));
-    if (lane % (RMAX * LP) == 0 && g0 + pg < np) out[g0 + pg] = rbase == 0 ? mine : fmax(out[g0 + pg], mine);
-  }
-}
-
-template <typename T, int RMAX, int LPC>
-__device__ __forceinline__ void score_rows(const uint8_t* sbuf, int np, int lp_per, int nl_rel, int D,
-                                           const T* q, int64_t q_rs, uint32_t rmask, int rows, double* out) {
-  for (int rb = 0; rb < rows; rb += RMAX) {
-    double qd[RMAX][4], qb[RMAX][4];
-    uint32_t qsel[RMAX][2];
-    load_rows<T, RMAX>(q, q_rs, rmask, rb, rows, D, qd, qb, qsel);
-    if constexpr (LPC * RMAX <= 32 && 32 % (LPC * RMAX) == 0 && 32 / (LPC * RMAX) > 1) {
-      if (lp_per == LPC) {
-        score_batch_grouped<T, RMAX, LPC>(sbuf, np, nl_rel, D, qd, qb, qsel, rb, rows, out);
-        continue;
-      }
-    }
-    score_batch<T, RMAX, LPC>(sbuf, np, lp_per, nl_rel, D, qd, qb, qsel, rb, rows, out);
-  }
-}
-
-__device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, int stage_cap, int32_t* sel_out,
-                         int32_t* sel_count);
-constexpr int kRegTopkMax = 24 * kTopkThreads;                 // n <= 6144 pages (384k tokens at P=64)
-constexpr int kRegTopkBits = 11;                               // radix digit: 2048 bins
-constexpr int kRegTopkSmem = 2 * (1 << kRegTopkBits) * 4;      // two histograms
-template <int KPT>
-__device__ void topk_cta_reg(int n, int K, const double* scores, uint32_t* hist2, int32_t* sel_out,
-                             int32_t* sel_count);
-
-template <typename T, int LPC>
-#ifndef SK_SEL_MINB
-#define SK_SEL_MINB 1
-#endif
-#ifndef SK_SEL_LOG_PER_SLOT
-#define SK_SEL_LOG_PER_SLOT 16
-#endif
-__global__ void __launch_bounds__(kScoreThreads, SK_SEL_MINB) select_kernel(PoolView pv, const T* __restrict__ q, int64_t q_ss,
-                                                               int64_t q_rs, const uint32_t* __restrict__ row_mask,
-                                                               const int32_t* __restrict__ tokens,
-                                                               const uint8_t* __restrict__ invoke, int K,
-                                                               double* ws_scores, uint32_t* ws_ticket,
-                                                               int ws_pages, int pps, int32_t* sel_out_all,
-                                                               int32_t* sel_count_all, int sel_stride,
-                                                               int smem_bytes, int dbg) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bar[kScoreWarps][2];
-  __shared__ uint32_t is_last;
-  const int s = blockIdx.y;
-  if (invoke != nullptr && invoke[s] == 0) return;
-  const uint32_t rmask = row_mask[s];
-  if (rmask == 0) return;
-  const int n_tok = tokens[s];
-  const int P = pv.P, L = pv.L, D = pv.D, LP = P / L;
-  const int n_pages = (n_tok + P - 1) / P;
-  const int n_log = (n_tok + L - 1) / L;
-  int32_t* sel_out = sel_out_all + (int64_t)s * sel_stride;
-  double* scores = ws_scores + (int64_t)s * ws_pages;
-  int pin[3];
-  const int npins = pins_of(n_pages, pin);
-  if (K >= n_pages || K <= npins) {  // selector.py:98-103: no scoring
-    if (blockIdx.x == 0) {
-      if (K >= n_pages) {
-        for (int i = threadIdx.x; i < n_pages; i += blockDim.x) sel_out[i] = i;
-      } else if (threadIdx.x == 0) {
-        for (int i = 0; i < npins; ++i) sel_out[i] = pin[i];
-      }
-      if (threadIdx.x == 0) sel_count_all[s] = K >= n_pages ? n_pages : npins;
-    }
-    return;
-  }
-  // ---- scoring: the warp streams kBatchesPerWarp batches of pps pages -------
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t row_bytes = 2 * D * 2;
-  const uint32_t slot = (uint32_t)pps * LP * row_bytes;
-  const int wp0 = (blockIdx.x * kScoreWarps + warp) * pps * kBatchesPerWarp;  // warp's first page
-  const int nb = (dbg == 1 || dbg == 3) ? 0 : max(0, min(kBatchesPerWarp, (n_pages - wp0 + pps - 1) / pps));
-  uint8_t* wbuf = smem + (size_t)warp * 2 * slot;
-  auto issue = [&](int b) {  // lane 0: bulk copy of batch b into slot b&1
-    const int p0 = wp0 + b * pps;
-    const int nl = min(min(pps, n_pages - p0) * LP, n_log - p0 * LP);
-    mbar_arrive_expect_tx(&bar[warp][b & 1], nl * row_bytes);
-    bulk_g2s(wbuf + (b & 1) * slot, pv.stats_ptr(s, p0 * LP), nl * row_bytes, &bar[warp][b & 1]);
-  };
-  if (lane == 0) {
-    mbar_init(&bar[warp][0], 1);
-    mbar_init(&bar[warp][1], 1);
-    fence_barrier_init();
-    if (nb > 0 && dbg != 5) issue(0);
-    if (nb > 1 && dbg != 5) issue(1);
-  }
-  __syncwarp();
-  const T* qs = q + s * q_ss;
-  const int rows = __popc(rmask);
-  for (int b = 0; b < nb; ++b) {
-    const int p0 = wp0 + b * pps;
-    const int np = min(pps, n_pages - p0);
-    const int nl = min(np * LP, n_log - p0 * LP);
-    if (dbg != 5) mbar_wait(&bar[warp][b & 1], (b >> 1) & 1);
-    const uint8_t* sb = wbuf + (b & 1) * slot;
-    if (dbg == 4) {
-    } else if (rows == 1) score_rows<T, 1, (LPC < 16 ? LPC : 16)>(sb, np, LP, nl, D, qs, q_rs, rmask, rows, scores + p0);
-    else if (rows == 2) score_rows<T, 2, (LPC < 8 ? LPC : 8)>(sb, np, LP, nl, D, qs, q_rs, rmask, rows, scores + p0);
-    else score_rows<T, 4, (LPC < 4 ? LPC : 4)>(sb, np, LP, nl, D, qs, q_rs, rmask, rows, scores + p0);
-    __syncwarp();  // every lane is done with the slot before it is refilled
-    if (lane == 0 && b + 2 < nb && dbg != 5) issue(b + 2);
-  }
-  // ---- CTA ticket: the stream's last CTA runs the top-k --------------------------
-  // bar.sync orders the CTA's score stores before thread 0's acq_rel fence +
-  // relaxed atomic (the release pattern of CUTLASS's generic barrier)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    const uint32_t t = atomicAdd(ws_ticket + s, 1u);
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    is_last = (t == gridDim.x - 1);
-    if (is_last) ws_ticket[s] = 0;  // re-arm for the next invocation
-  }
-  __syncthreads();
-  if (!is_last || dbg == 2 || dbg == 3) return;
-  if (n_pages <= 16 * kTopkThreads && smem_bytes >= kRegTopkSmem && dbg != 7)  // keys per thread: as few as fit
-    topk_cta_reg<16>(n_pages, K, scores, reinterpret_cast<uint32_t*>(smem), sel_out, sel_count_all + s);
-  else if (n_pages <= kRegTopkMax && smem_bytes >= kRegTopkSmem && dbg != 7)
-    topk_cta_reg<24>(n_pages, K, scores, reinterpret_cast<uint32_t*>(smem), sel_out, sel_count_all + s);
-  else
-    topk_cta(n_pages, K, scores, reinterpret_cast<uint64_t*>(smem), smem_bytes / 8, sel_out, sel_count_all + s);
-}
-
-// Block-wide exclusive scan of one value per thread (kTopkThreads threads)
-// in thread order; returns the thread's exclusive prefix and the block total.
+// Block-wide exclusive scan of one value per thread in thread order; returns
+// the thread's exclusive prefix and the block total.
 __device__ __forceinline__ uint32_t block_scan(uint32_t x, uint32_t* warp_tot, uint32_t& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t incl = x;
@@ -393,60 +328,46 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t x, uint32_t* warp_tot, u
   if (lane == 31) warp_tot[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    const uint32_t t = lane < kTopkWarps ? warp_tot[lane] : 0u;
+    const uint32_t t = lane < kWarps ? warp_tot[lane] : 0u;
     uint32_t ti = t;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const uint32_t o = __shfl_up_sync(0xffffffffu, ti, off);
       if (lane >= off) ti += o;
     }
-    if (lane < kTopkWarps) warp_tot[lane] = ti - t;  // exclusive warp offsets
-    if (lane == kTopkWarps - 1) warp_tot[kTopkWarps] = ti;
+    if (lane < kWarps) warp_tot[lane] = ti - t;  // exclusive warp offsets
+    if (lane == kWarps - 1) warp_tot[kWarps] = ti;
   }
   __syncthreads();
   const uint32_t res = warp_tot[warp] + incl - x;
-  total = warp_tot[kTopkWarps];
+  total = warp_tot[kWarps];
   __syncthreads();
   return res;
 }
 
-// Top-k of one stream by the whole CTA (kTopkThreads threads); the trivial
-// cases (every page / pins only) are handled by the caller.
-__device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, int stage_cap, int32_t* sel_out,
-                         int32_t* sel_count) {
+// ---- exact top-k (slow path): every non-pinned page scored in fp64 ------------
+// Pins, then the best K-|pins| others by (score desc, index asc), ascending.
+// Keys staged in shared memory when they fit, else re-read from the slots.
+__device__ void topk_exact(int n, int K, const double* scores, uint64_t* s_keys, int stage_cap, int32_t* sel_out,
+                           int32_t* sel_count) {
   __shared__ uint32_t hist[256];
-  __shared__ uint32_t whist[kTopkWarps * 256];
-  __shared__ uint32_t warp_tot[kTopkWarps + 1];
-  __shared__ uint64_t s_max[kTopkWarps], s_min[kTopkWarps];
+  __shared__ uint32_t whist[kWarps * 256];
+  __shared__ uint32_t warp_tot[kWarps + 1];
+  __shared__ uint64_t s_max[kWarps], s_min[kWarps];
   __shared__ uint32_t sh_bin, sh_kk, sh_done;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int pin[3];
-  const int npins = pins_of(n, pin);
   const bool staged = n <= stage_cap;
   auto key_at = [&](int i) -> uint64_t {
     if (staged) return s_keys[i];
     return is_pin(i, n) ? 0ull : order_key(__ldcg(scores + i));
   };
-  // keys + the candidates' max/min (to skip the leading bytes they share)
   uint64_t kmax = 0, kmin = ~0ull;
-  constexpr int kU = 8;  // loads in flight per thread
-  for (int base = 0; base < n; base += kU * kTopkThreads) {
-    double sc[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int i = base + u * kTopkThreads + tid;
-      sc[u] = i < n ? __ldcg(scores + i) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int i = base + u * kTopkThreads + tid;
-      if (i >= n) continue;
-      const uint64_t k = is_pin(i, n) ? 0ull : order_key(sc[u]);
-      if (staged) s_keys[i] = k;
-      if (k) {
-        kmax = k > kmax ? k : kmax;
-        kmin = k < kmin ? k : kmin;
-      }
+  for (int i = tid; i < n; i += kThreads) {
+    const uint64_t k = is_pin(i, n) ? 0ull : order_key(__ldcg(scores + i));
+    if (staged) s_keys[i] = k;
+    if (k) {
+      kmax = k > kmax ? k : kmax;
+      kmin = k < kmin ? k : kmin;
     }
   }
 #pragma unroll
@@ -460,17 +381,16 @@ __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, i
     s_min[warp] = kmin;
   }
   if (tid == 0) {
-    sh_kk = K - npins;
+    sh_kk = K - n_pins(n);
     sh_done = 0;
   }
   __syncthreads();
   kmax = 0;
   kmin = ~0ull;
-  for (int w = 0; w < kTopkWarps; ++w) {
+  for (int w = 0; w < kWarps; ++w) {
     kmax = s_max[w] > kmax ? s_max[w] : kmax;
     kmin = s_min[w] < kmin ? s_min[w] : kmin;
   }
-  // radix passes start at the first byte where the candidates differ
   const int common = kmax == kmin ? 64 : __clzll(kmax ^ kmin);
   int shift = 56 - 8 * (common / 8);
   uint64_t mask = shift >= 56 ? 0ull : (~0ull << (shift + 8));
@@ -479,17 +399,14 @@ __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, i
   if (common == 64) {  // every candidate has the same key: the lowest indices win
     mask = ~0ull;
     prefix = kmax;
-    done = false;
     shift = -8;
   }
-  // thread t owns the consecutive indices [t*kpt, t*kpt + kpt): one pass over
-  // its keys per radix digit, and page order is thread order for compaction
-  const int kpt = (n + kTopkThreads - 1) / kTopkThreads;
+  const int kpt = (n + kThreads - 1) / kThreads;
   const int i0 = tid * kpt, i1 = min(n, i0 + kpt);
   for (; shift >= 0; shift -= 8) {
-    for (int b = tid; b < kTopkWarps * 256; b += kTopkThreads) whist[b] = 0;
+    for (int b = tid; b < kWarps * 256; b += kThreads) whist[b] = 0;
     __syncthreads();
-    for (int i = i0; i < i1; ++i) {  // per-warp histograms: contention stays inside a warp
+    for (int i = i0; i < i1; ++i) {
       const uint64_t key = key_at(i);
       if (key && (key & mask) == prefix) atomicAdd(&whist[warp * 256 + (uint32_t(key >> shift) & 255u)], 1u);
     }
@@ -497,12 +414,11 @@ __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, i
     {
       uint32_t h = 0;
 #pragma unroll
-      for (int w = 0; w < kTopkWarps; ++w) h += whist[w * 256 + tid];  // kTopkThreads == 256 bins
+      for (int w = 0; w < kWarps; ++w) h += whist[w * 256 + tid];
       hist[tid] = h;
     }
     __syncthreads();
     if (warp == 0) {
-      // bins from the top: lane l covers bins 255-8l .. 248-8l
       const uint32_t kk = sh_kk;
       uint32_t sum = 0;
 #pragma unroll
@@ -534,13 +450,11 @@ __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, i
     prefix |= (uint64_t)sh_bin << shift;
     mask |= (uint64_t)0xFF << shift;
     done = sh_done;
-    __syncthreads();  // sh_* are rewritten by the next pass
+    __syncthreads();
     if (done) break;
   }
-  const bool all_equal_taken = done;  // every key matching the prefix is selected
-  const uint32_t take_eq = sh_kk;     // else: this many keys == prefix, lowest index first
-  // ordered compaction: rank of equal keys, then output positions, by two
-  // block-wide scans over thread (= page) order
+  const bool all_equal_taken = done;
+  const uint32_t take_eq = sh_kk;
   uint32_t n_eq = 0;
   for (int i = i0; i < i1; ++i) {
     const uint64_t key = key_at(i);
@@ -569,82 +483,114 @@ __device__ void topk_cta(int n, int K, const double* scores, uint64_t* s_keys, i
     if (cand && km == prefix) take = take || all_equal_taken || eq_rank++ < take_eq;
     if (take) sel_out[out_pos++] = i;
   }
-  if (tid == kTopkThreads - 1) *sel_count = out_pos;
+  if (tid == kThreads - 1) *sel_count = out_pos;
 }
 
-// Top-k of one stream, keys in registers (n <= kRegTopkMax).  Same result
-// as topk_cta -- pins, then the best K-|pins| others by (score desc, index
-// asc), ascending -- with far fewer block barriers: one shared 2048-bin
-// histogram per 11-bit radix pass (random scores rarely collide, so no
-// per-warp copies), double-buffered so zeroing the next one needs no extra
-// barrier, the boundary bin found with one block scan (3 barriers per pass),
-// and one packed scan (strict | equal counts) for the ordered compaction.
-template <int KPT>
-__device__ void topk_cta_reg(int n, int K, const double* scores, uint32_t* hist2, int32_t* sel_out,
-                             int32_t* sel_count) {
-  constexpr int NB = 1 << kRegTopkBits;
-  constexpr int BPT = NB / kTopkThreads;  // bins per thread (8)
-  __shared__ uint32_t wtot[kTopkWarps + 1];
-  __shared__ uint64_t s_max[kTopkWarps], s_min[kTopkWarps];
-  __shared__ uint32_t sh_bin, sh_kk, sh_done;
+// ---- phase B, fast path ----------------------------------------------------------
+// Returns false (nothing written) when the band is larger than kBandCap.
+#ifdef SK_SEL_TIMING  // timing builds only: globaltimer stamps of phase B into the f64 scratch
+#define SK_STAMP(i)                                                                               \
+  do {                                                                                            \
+    if (threadIdx.x == 0) {                                                                       \
+      uint64_t t_;                                                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                      \
+      reinterpret_cast<uint64_t*>(p.exact)[(int64_t)s * p.ws_pages + (i)] = t_;                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define SK_STAMP(i) \
+  do {              \
+  } while (0)
+#endif
+
+// The K'-th largest approximate score is located by 11-bit radix passes over
+// the order-preserving 32-bit images (thread t holds pages [t*kpt, +kpt)),
+// from the first bit where the candidates differ, and only until its bin is
+// narrower than 2E: any T in the bin [lo_b, hi_b] then gives
+//   certain-in   approx > hi_b + 2E   (true score > true K'-th score)
+//   certain-out  approx < lo_b - 2E
+// and the band in between is rescored exactly.  Counters and the band list
+// use shared-memory atomics (the list order is irrelevant: the rank compares
+// (exact score, page index)); one block scan orders the output.
+template <typename T, int D, int KPT>
+__device__ bool topk_filtered(const SelParams& p, int s, int n, int n_log, const T* qs, const int* row_idx, int rows,
+                              uint32_t* hist2) {
+  constexpr int BPT = kNB / kThreads;  // bins per thread (8)
+  __shared__ uint32_t wtot[kWarps + 1];
+  __shared__ uint32_t s_max[kWarps], s_min[kWarps], s_emax[kWarps];
+  __shared__ uint32_t sh_bin, sh_kk, s_nb, s_nin;
+  __shared__ int band_idx[kBandCap];
+  __shared__ uint64_t band_key[kBandCap];
+  __shared__ uint32_t chosen_bits[64 * kThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int pin[3];
-  const int npins = pins_of(n, pin);
-  const int kpt = (n + kTopkThreads - 1) / kTopkThreads;
+  const float2* approx = p.approx + (int64_t)s * p.ws_pages;
+  const int kpt = (n + kThreads - 1) / kThreads;
   const int i0 = tid * kpt;
-  uint64_t key[KPT];
-  uint64_t kmax = 0, kmin = ~0ull;
+  uint32_t key[KPT];
+  float emax = 0.f;
+  uint32_t kmax = 0, kmin = ~0u;
 #pragma unroll
   for (int j = 0; j < KPT; ++j) {
     const int i = i0 + j;
     key[j] = 0;
-    if (j < kpt && i < n && !is_pin(i, n)) key[j] = order_key(__ldcg(scores + i));
-    if (key[j]) {
-      kmax = key[j] > kmax ? key[j] : kmax;
-      kmin = key[j] < kmin ? key[j] : kmin;
+    if (j < kpt && i < n && !is_pin(i, n)) {
+      const float2 ae = __ldcg(approx + i);
+      key[j] = order_key32(ae.x);
+      emax = fmaxf(emax, ae.y);
+      kmax = max(kmax, key[j]);
+      kmin = min(kmin, key[j]);
     }
   }
-  for (int b = tid; b < NB; b += kTopkThreads) hist2[b] = 0;
+  for (int b = tid; b < kNB; b += kThreads) hist2[b] = 0;
+  for (int b = tid; b < (n + 31) / 32; b += kThreads) chosen_bits[b] = 0;
+  if (tid == 0) s_nb = s_nin = 0;
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
-    const uint64_t a = __shfl_xor_sync(0xffffffffu, kmax, off), c = __shfl_xor_sync(0xffffffffu, kmin, off);
-    kmax = a > kmax ? a : kmax;
-    kmin = c < kmin ? c : kmin;
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
+    emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, off));
   }
   if (lane == 0) {
     s_max[warp] = kmax;
     s_min[warp] = kmin;
+    s_emax[warp] = __float_as_uint(emax);
   }
+  SK_STAMP(1);
   __syncthreads();
   kmax = 0;
-  kmin = ~0ull;
+  kmin = ~0u;
+  emax = 0.f;
 #pragma unroll
-  for (int w = 0; w < kTopkWarps; ++w) {
-    kmax = s_max[w] > kmax ? s_max[w] : kmax;
-    kmin = s_min[w] < kmin ? s_min[w] : kmin;
+  for (int w = 0; w < kWarps; ++w) {
+    kmax = max(kmax, s_max[w]);
+    kmin = min(kmin, s_min[w]);
+    emax = fmaxf(emax, __uint_as_float(s_emax[w]));
   }
-  uint32_t kk = K - npins;  // keys still to take at/below the current prefix
-  // bits below `hi` are unresolved; the candidates agree on every bit above
-  int hi = kmax == kmin ? 0 : 64 - __clzll(kmax ^ kmin);
-  uint64_t mask = hi >= 64 ? 0ull : (~0ull << hi);
-  uint64_t prefix = kmax & mask;
+  const double w2 = 2.0 * (double)emax * (1.0 + 0x1p-20);  // 2E, widened for the threshold roundings
+  uint32_t kk = p.K - n_pins(n);                            // K' >= 1 here
+  const uint32_t kq = kk;
+  int hi = kmax == kmin ? 0 : 32 - __clz(kmax ^ kmin);
+  uint32_t mask = hi >= 32 ? 0u : (~0u << hi);
+  uint32_t prefix = kmax & mask;
   int cur = 0;
-  while (hi > 0) {
-    const int w = hi < kRegTopkBits ? hi : kRegTopkBits;
+  // the bin's value range, clamped to the candidates' (no NaN/inf encodings)
+  auto bin_hi = [&]() { return (double)key32_value(min(prefix | ~mask, kmax)); };
+  auto bin_lo = [&]() { return (double)key32_value(max(prefix, kmin)); };
+  while (hi > 0 && bin_hi() - bin_lo() > w2) {
+    const int w = hi < kRadixBits ? hi : kRadixBits;
     const int shift = hi - w;
     const uint32_t dm = (1u << w) - 1u;
-    uint32_t* h = hist2 + cur * NB;
+    uint32_t* h = hist2 + cur * kNB;
 #pragma unroll
     for (int j = 0; j < KPT; ++j)
-      if (key[j] && (key[j] & mask) == prefix) atomicAdd(&h[uint32_t(key[j] >> shift) & dm], 1u);
-    uint32_t* hn = hist2 + (cur ^ 1) * NB;
-    for (int b = tid; b < NB; b += kTopkThreads) hn[b] = 0;
+      if (key[j] && (key[j] & mask) == prefix) atomicAdd(&h[(key[j] >> shift) & dm], 1u);
+    uint32_t* hn = hist2 + (cur ^ 1) * kNB;
+    for (int b = tid; b < kNB; b += kThreads) hn[b] = 0;
     __syncthreads();  // A: histogram complete
-    // thread t owns bins NB-1-BPT*t .. NB-BPT*(t+1), scanned from the top
     uint32_t loc[BPT], sum = 0;
 #pragma unroll
     for (int e = 0; e < BPT; ++e) {
-      loc[e] = h[NB - 1 - BPT * tid - e];
+      loc[e] = h[kNB - 1 - BPT * tid - e];
       sum += loc[e];
     }
     uint32_t incl = sum;
@@ -657,92 +603,265 @@ __device__ void topk_cta_reg(int n, int K, const double* scores, uint32_t* hist2
     __syncthreads();  // B: warp totals
     uint32_t excl = incl - sum;
 #pragma unroll
-    for (int w2 = 0; w2 < kTopkWarps; ++w2) excl += w2 < warp ? wtot[w2] : 0u;
+    for (int w3 = 0; w3 < kWarps; ++w3) excl += w3 < warp ? wtot[w3] : 0u;
     if (excl < kk && kk <= excl + sum) {
       uint32_t cum = excl;
 #pragma unroll
       for (int e = 0; e < BPT; ++e) {
         if (cum + loc[e] >= kk && cum < kk) {
-          sh_bin = NB - 1 - BPT * tid - e;
+          sh_bin = kNB - 1 - BPT * tid - e;
           sh_kk = kk - cum;
-          sh_done = loc[e] == kk - cum ? 1u : 0u;
         }
         cum += loc[e];
       }
     }
     __syncthreads();  // C: boundary bin published
-    const uint32_t bin = sh_bin;
+    prefix |= sh_bin << shift;
+    mask |= dm << shift;
     kk = sh_kk;
-    const bool done = sh_done;
-    prefix |= (uint64_t)bin << shift;
-    mask |= (uint64_t)dm << shift;
     hi = shift;
     cur ^= 1;
-    if (done) break;  // every key of the boundary bin is taken
   }
-  // ordered compaction: pins and keys above the prefix are taken; of the keys
-  // equal to it, the kk lowest indices.  One scan of packed (taken | equal << 16).
-  uint32_t n_take = 0, n_eq = 0;
+  SK_STAMP(2);
+  const double hiT = bin_hi() + w2, loT = bin_lo() - w2;
+  uint64_t inb = 0, bnd = 0;
+  uint32_t c_in = 0;
 #pragma unroll
   for (int j = 0; j < KPT; ++j) {
-    const int i = i0 + j;
-    if (j >= kpt || i >= n) continue;
-    const uint64_t km = key[j] & mask;
-    if (is_pin(i, n) || (key[j] && km > prefix)) ++n_take;
-    else if (key[j] && km == prefix) ++n_eq;
+    if (!key[j]) continue;
+    const double x = (double)key32_value(key[j]);
+    if (x > hiT) {
+      inb |= 1ull << j;
+      ++c_in;
+    } else if (x >= loT) {
+      bnd |= 1ull << j;
+      const uint32_t slot = atomicAdd(&s_nb, 1u);
+      if (slot < (uint32_t)kBandCap) band_idx[slot] = i0 + j;
+    }
   }
+  c_in = __reduce_add_sync(0xffffffffu, c_in);
+  if (lane == 0 && c_in) atomicAdd(&s_nin, c_in);
+  __syncthreads();
+  const uint32_t nb = s_nb, n_in = s_nin;
+  SK_STAMP(3);
+  if (nb > (uint32_t)kBandCap) return false;
+  const uint32_t need = kq - n_in;  // in [1, nb]
+  if (need < nb) {
+    for (uint32_t b = warp; b < nb; b += kWarps) {
+      const double sc = exact_page_score<T, D>(p.pv, s, band_idx[b], n_log, qs, p.q_rs, row_idx, rows);
+      if (lane == 0) band_key[b] = order_key(sc);
+    }
+    __syncthreads();
+    if (tid < (int)nb) {
+      const uint64_t mk = band_key[tid];
+      const int mi = band_idx[tid];
+      uint32_t rank = 0;
+      for (uint32_t b = 0; b < nb; ++b) {
+        const uint64_t o = band_key[b];
+        rank += (o > mk || (o == mk && band_idx[b] < mi)) ? 1u : 0u;
+      }
+      if (rank < need) atomicOr(&chosen_bits[mi >> 5], 1u << (mi & 31));
+    }
+    __syncthreads();
+  }
+  SK_STAMP(4);
+  // ordered compaction: pins, certain-in, chosen band pages
+  const bool all_band = need >= nb;
+  int32_t* sel_out = p.sel_out + (int64_t)s * p.sel_stride;
+  auto taken = [&](int j) -> bool {
+    const int i = i0 + j;
+    if (j >= kpt || i >= n) return false;
+    if (is_pin(i, n) || ((inb >> j) & 1ull)) return true;
+    return ((bnd >> j) & 1ull) && (all_band || ((chosen_bits[i >> 5] >> (i & 31)) & 1u));
+  };
+  uint32_t n_take = 0;
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) n_take += taken(j);
   uint32_t tot;
-  const uint32_t ex = block_scan(n_take | (n_eq << 16), wtot, tot);
-  uint32_t eq_rank = ex >> 16;
-  uint32_t pos = (ex & 0xFFFFu) + (eq_rank < kk ? eq_rank : kk);
+  uint32_t pos = block_scan(n_take, wtot, tot);
 #pragma unroll
-  for (int j = 0; j < KPT; ++j) {
-    const int i = i0 + j;
-    if (j >= kpt || i >= n) continue;
-    const uint64_t km = key[j] & mask;
-    bool take = is_pin(i, n) || (key[j] && km > prefix);
-    if (!take && key[j] && km == prefix) take = eq_rank++ < kk;
-    if (take) sel_out[pos++] = i;
-  }
-  if (tid == kTopkThreads - 1) *sel_count = (tot & 0xFFFFu) + ((tot >> 16) < kk ? (tot >> 16) : kk);
+  for (int j = 0; j < KPT; ++j)
+    if (taken(j)) sel_out[pos++] = i0 + j;
+  if (tid == kThreads - 1) p.sel_count[s] = pos;
+  SK_STAMP(5);
+  return true;
 }
 
-template <typename T>
-int select_dispatch(const PoolView& pv, int n_streams, const void* q, int64_t q_ss, int64_t q_rs,
-                    const uint32_t* row_mask, const int32_t* tokens, const uint8_t* invoke, int K, int max_pages,
-                    int32_t* sel_out, int32_t* sel_count, int sel_stride, double* scores, uint32_t* ticket,
-                    cudaStream_t st) {
-  const int LP = pv.P / pv.L;
-  const int pps = LP >= SK_SEL_LOG_PER_SLOT ? 1 : SK_SEL_LOG_PER_SLOT / LP;  // pages per bulk copy
-  const size_t slot = (size_t)pps * LP * 2 * pv.D * 2;
-  size_t smem = 2 * kScoreWarps * slot;
-  if (smem > 200 * 1024) {
-    set_error("select: page/logical-page geometry needs too much shared memory");
-    return SK_EUNSUPPORTED;
+template <typename T, int D>
+__global__ void __launch_bounds__(kThreads, 2) select_kernel(const __grid_constant__ SelParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int row_idx[kMaxRows];
+  __shared__ uint32_t is_last;
+  const int s = blockIdx.y;
+  if (p.flags & SK_LAUNCH_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (p.invoke != nullptr && p.invoke[s] == 0) return;
+  const uint32_t gmask = p.group_rows >= 32 ? 0xffffffffu : ((1u << p.group_rows) - 1u);
+  const uint32_t rmask = p.row_mask[s] & gmask;
+  if (rmask == 0) return;
+  const int n_tok = p.tokens[s];
+  const int P = p.pv.P, L = p.pv.L;
+  const int n_pages = min((n_tok + P - 1) / P, p.ws_pages);
+  const int n_log = min((n_tok + L - 1) / L, n_pages * (P / L));
+  const int tid = threadIdx.x;
+  int32_t* sel_out = p.sel_out + (int64_t)s * p.sel_stride;
+  const int npins = n_pins(n_pages);
+  if (n_pages <= 0) return;
+  if (p.K >= n_pages || p.K <= npins) {  // selector.py:98-103: no scoring
+    if (blockIdx.x == 0) {
+      if (p.K >= n_pages) {
+        for (int i = tid; i < n_pages; i += kThreads) sel_out[i] = i;
+      } else if (tid == 0) {  // pins {0, n-2, n-1}, ascending and deduplicated
+        sel_out[0] = 0;
+        if (n_pages >= 2) sel_out[npins - 1] = n_pages - 1;
+        if (n_pages >= 3) sel_out[1] = n_pages - 2;
+      }
+      if (tid == 0) p.sel_count[s] = p.K >= n_pages ? n_pages : npins;
+    }
+    return;
   }
-  const int ppc = kScoreWarps * kBatchesPerWarp * pps;  // pages per CTA
-  dim3 grid((max_pages + ppc - 1) / ppc, n_streams);
-  const T* qt = static_cast<const T*>(q);
-  // ablation builds for timing the phases (tools/decode_probe.py; never the shipped library):
-  // -DSK_SEL_ABLATE=1 no scoring, 2 no top-k, 3 neither, 4 copies without scoring
-#ifndef SK_SEL_ABLATE
+  const int rows = __popc(rmask);
+  if (tid == 0) {
+    uint32_t m = rmask;
+    for (int r = 0; r < rows; ++r) {
+      row_idx[r] = __ffs(m) - 1;
+      m &= m - 1;
+    }
+  }
+  __syncthreads();
+  const T* qs = reinterpret_cast<const T*>(p.q) + s * p.q_ss;
+  uint4 a0[2][D / 16];  // the warp's first tile, in flight while the B fragments are built
+  {
+    const int first = (blockIdx.x * kWarps + (tid >> 5)) * p.tiles_per_warp;
+    if (first < ((n_log + 15) >> 4)) load_tile<T, D>(p, s, n_log, first, a0);
+  }
+  // programmatic dependent launch: the stats, tokens and masks above were read
+  // before the dependency wait; q (the previous kernel's output in a model) after
+  if (p.flags & SK_LAUNCH_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // ---- B fragments: q' = [q- | q+] of the retrieval rows, A's channel permutation
+  constexpr int KS = D / 8;
+  const int NT = (rows + 7) >> 3;
+  uint2* bfrag = reinterpret_cast<uint2*>(smem);
+  for (int e = tid; e < NT * KS * 32; e += kThreads) {
+    const int nt = e / (KS * 32), ks = (e / 32) % KS, ln = e & 31;
+    const int r = nt * 8 + (ln >> 2), tt = ln & 3;
+    uint32_t w[2] = {0u, 0u};
+    if (r < rows) {
+      const int ch = (ks >> 1) * 32 + tt * 8 + (ks & 1) * 4;  // in [0, 2D); 4 channels, one half
+      const uint16_t* qr = reinterpret_cast<const uint16_t*>(qs + (int64_t)row_idx[r] * p.q_rs) + (ch % D);
+      const bool neg_half = ch < D;  // kmin channels take q-, kmax channels q+
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint16_t x = __ldcg(qr + c);
+        const bool neg = x & 0x8000u;
+        const uint32_t v = (neg == neg_half) ? x : 0u;
+        w[c >> 1] |= v << (16 * (c & 1));
+      }
+    }
+    bfrag[e] = make_uint2(w[0], w[1]);
+  }
+  __syncthreads();
+  // ---- phase A
+  float2* approx = p.approx;
+  switch (NT) {
+    case 1: score_tiles<T, D, 1>(p, s, n_log, n_pages, rows, bfrag, approx, a0); break;
+    case 2: score_tiles<T, D, 2>(p, s, n_log, n_pages, rows, bfrag, approx, a0); break;
+    case 3: score_tiles<T, D, 3>(p, s, n_log, n_pages, rows, bfrag, approx, a0); break;
+    default: score_tiles<T, D, 4>(p, s, n_log, n_pages, rows, bfrag, approx, a0); break;
+  }
+  // ---- CTA ticket: the stream's last CTA runs phase B
+#ifndef SK_SEL_ABLATE  // timing builds only (tools/ab_variant.sh): 1 = phase A only, 2 = no phase B
 #define SK_SEL_ABLATE 0
 #endif
-  const int dbg = SK_SEL_ABLATE;
-#define SK_SEL(LPV)                                                                                          \
-  do {                                                                                                       \
-    cudaFuncSetAttribute(select_kernel<T, LPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
-    select_kernel<T, LPV><<<grid, kScoreThreads, smem, st>>>(pv, qt, q_ss, q_rs, row_mask, tokens, invoke, K, \
-                                                             scores, ticket, max_pages, pps, sel_out,         \
-                                                             sel_count, sel_stride, (int)smem, dbg);          \
-  } while (0)
-  if (LP == 1) SK_SEL(1);
-  else if (LP == 2) SK_SEL(2);
-  else if (LP == 4) SK_SEL(4);
-  else if (LP == 8) SK_SEL(8);
-  else if (LP == 16) SK_SEL(16);
-  else SK_SEL(32);
-#undef SK_SEL
+  if (SK_SEL_ABLATE == 1) return;
+  __syncthreads();
+  if (tid == 0) {  // bar.sync + a gpu-scope acq_rel RMW: releases the CTA's slots, acquires the others'
+    uint32_t t;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(p.ticket + s) : "memory");
+    is_last = (t == gridDim.x - 1);
+    if (is_last) p.ticket[s] = 0;  // re-arm for the next invocation
+  }
+  __syncthreads();
+  if (!is_last || SK_SEL_ABLATE == 2) return;
+  uint32_t* hist2 = reinterpret_cast<uint32_t*>(smem);
+  SK_STAMP(0);
+  bool ok = false;
+  if (n_pages <= 8 * kThreads) ok = topk_filtered<T, D, 8>(p, s, n_pages, n_log, qs, row_idx, rows, hist2);
+  else if (n_pages <= 16 * kThreads) ok = topk_filtered<T, D, 16>(p, s, n_pages, n_log, qs, row_idx, rows, hist2);
+  else if (n_pages <= 32 * kThreads) ok = topk_filtered<T, D, 32>(p, s, n_pages, n_log, qs, row_idx, rows, hist2);
+  else if (n_pages <= 64 * kThreads) ok = topk_filtered<T, D, 64>(p, s, n_pages, n_log, qs, row_idx, rows, hist2);
+  if (ok) return;
+  // ---- slow path: exact fp64 score of every non-pinned page, exact radix select
+  __syncthreads();
+  double* exact = p.exact + (int64_t)s * p.ws_pages;
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int i = warp; i < n_pages; i += kWarps) {
+    if (is_pin(i, n_pages)) continue;
+    const double sc = exact_page_score<T, D>(p.pv, s, i, n_log, qs, p.q_rs, row_idx, rows);
+    if (lane == 0) exact[i] = sc;
+  }
+  __syncthreads();
+  topk_exact(n_pages, p.K, exact, reinterpret_cast<uint64_t*>(smem), p.smem_bytes / 8, sel_out, p.sel_count + s);
+}
+
+// ---- sk_score_pages: exact fp64 scores of every page (score_pages) -------------
+template <typename T, int D>
+__global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__ SelParams p, double* out,
+                                                          int out_stride) {
+  __shared__ int row_idx[kMaxRows];
+  const int s = blockIdx.y;
+  const uint32_t gmask = p.group_rows >= 32 ? 0xffffffffu : ((1u << p.group_rows) - 1u);
+  const uint32_t rmask = p.row_mask[s] & gmask;
+  const int rows = __popc(rmask);
+  if (threadIdx.x == 0) {
+    uint32_t m = rmask;
+    for (int r = 0; r < rows; ++r) {
+      row_idx[r] = __ffs(m) - 1;
+      m &= m - 1;
+    }
+  }
+  __syncthreads();
+  const int n_tok = p.tokens[s];
+  const int n_pages = min((n_tok + p.pv.P - 1) / p.pv.P, out_stride);
+  const int n_log = (n_tok + p.pv.L - 1) / p.pv.L;
+  const T* qs = reinterpret_cast<const T*>(p.q) + s * p.q_ss;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = blockIdx.x * kWarps + warp; i < n_pages; i += gridDim.x * kWarps) {
+    const double sc = rows ? exact_page_score<T, D>(p.pv, s, i, n_log, qs, p.q_rs, row_idx, rows) : -INFINITY;
+    if (lane == 0) out[(int64_t)s * out_stride + i] = sc;
+  }
+}
+
+constexpr int kSmemBytes = 2 * kNB * 4;  // phase B histograms (>= the B fragments: 4 x 16 x 32 x 8 B)
+static_assert(kSmemBytes >= 4 * 16 * 32 * 8, "B fragments must fit the dynamic shared memory");
+
+template <typename T, int D>
+int select_launch(const SelParams& p0, int n_streams, int max_pages, cudaStream_t st) {
+  SelParams p = p0;
+  const int LP = p.pv.P / p.pv.L;
+  const int n_tiles = (max_pages * LP + 15) / 16;
+  // ~2 CTAs per SM in total: each warp streams tiles_per_warp tiles (8 KB each)
+  const int sms = device_sm_count();
+  int tpw = (int)(((int64_t)n_streams * n_tiles + (int64_t)kWarps * 2 * sms - 1) / ((int64_t)kWarps * 2 * sms));
+  tpw = tpw < 1 ? 1 : tpw;
+  if (LP > 16) tpw = (tpw + LP / 16 - 1) / (LP / 16) * (LP / 16);  // a page's tiles stay in one warp
+  p.tiles_per_warp = tpw;
+  p.smem_bytes = kSmemBytes;
+  cudaFuncSetAttribute(select_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((n_tiles + kWarps * tpw - 1) / (kWarps * tpw), n_streams, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (p.flags & SK_LAUNCH_PDL) ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, select_kernel<T, D>, p);
+  if (e != cudaSuccess) {
+    set_error(std::string("select_kernel: ") + cudaGetErrorString(e));
+    return SK_ECUDA;
+  }
   SK_CHECK_LAUNCH("select_kernel");
   return SK_OK;
 }
@@ -753,36 +872,86 @@ int select_dispatch(const PoolView& pv, int n_streams, const void* q, int64_t q_
 extern "C" int64_t sk_select_scores_offset(int32_t n_streams) { return ((int64_t)n_streams * 4 + 255) / 256 * 256; }
 
 extern "C" int64_t sk_select_workspace(int32_t n_streams, int32_t max_pages) {
-  return sk_select_scores_offset(n_streams) + (int64_t)n_streams * max_pages * 8;  // tickets + scores
+  return sk_select_scores_offset(n_streams) + (int64_t)n_streams * max_pages * 16;  // tickets + 2 x 8 B per page
 }
+
+namespace {
+int fill_params(sk::SelParams& p, const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
+                int64_t q_ss, int64_t q_rs, const uint32_t* row_mask, const int32_t* tokens) {
+  using namespace sk;
+  int rc = check_pool(pool);
+  if (rc) return rc;
+  SK_CHECK_ARG(pool->stats != nullptr, "select: pool has no stats");
+  SK_CHECK_ARG(n_streams >= 1 && n_streams <= 65535 && group_rows >= 1 && group_rows <= kMaxRows,
+               "select: bad stream/row counts");
+  SK_CHECK_ARG(q && row_mask && tokens, "select: NULL pointer");
+  SK_CHECK_ARG(reinterpret_cast<uintptr_t>(pool->stats) % 16 == 0, "select: stats must be 16-byte aligned");
+  SK_CHECK_ARG(reinterpret_cast<uintptr_t>(q) % 8 == 0 && q_ss % 4 == 0 && q_rs % 4 == 0,
+               "select: q must be 8-byte aligned with strides a multiple of 4 elements");
+  p = SelParams{};
+  p.pv = make_view(*pool);
+  p.q = q;
+  p.q_ss = q_ss;
+  p.q_rs = q_rs;
+  p.row_mask = row_mask;
+  p.tokens = tokens;
+  p.group_rows = group_rows;
+  return SK_OK;
+}
+}  // namespace
 
 extern "C" int sk_select_pages(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
                                int64_t q_stream_stride, int64_t q_row_stride, const uint32_t* row_mask,
                                const int32_t* tokens, const uint8_t* invoke, int32_t budget_pages,
                                int32_t max_pages_hint, int32_t* sel_out, int32_t* sel_count, int32_t sel_stride,
-                               void* workspace, int64_t workspace_bytes, void* stream) {
+                               void* workspace, int64_t workspace_bytes, uint32_t flags, void* stream) {
   using namespace sk;
-  int rc = check_pool(pool);
+  SelParams p;
+  int rc = fill_params(p, pool, n_streams, group_rows, q, q_stream_stride, q_row_stride, row_mask, tokens);
   if (rc) return rc;
-  SK_CHECK_ARG(pool->stats != nullptr, "select: pool has no stats");
-  SK_CHECK_ARG(n_streams >= 1 && n_streams <= 65535 && group_rows >= 1 && group_rows <= 32,
-               "select: bad stream/row counts");
   SK_CHECK_ARG(budget_pages >= 1, "select: budget below one page");
   SK_CHECK_ARG(max_pages_hint >= 1 && max_pages_hint <= pool->max_pages, "select: bad max_pages_hint");
   SK_CHECK_ARG(sel_stride >= budget_pages || sel_stride >= max_pages_hint, "select: sel_stride too small");
   SK_CHECK_ARG(workspace_bytes >= sk_select_workspace(n_streams, max_pages_hint), "select: workspace too small");
-  SK_CHECK_ARG(q && row_mask && tokens && sel_out && sel_count && workspace, "select: NULL pointer");
-  SK_CHECK_ARG(reinterpret_cast<uintptr_t>(pool->stats) % 16 == 0, "select: stats must be 16-byte aligned");
-  PoolView pv = make_view(*pool);
-  // workspace = [tickets: n_streams x u32, padded to 256 B][scores: n_streams x max_pages_hint f64]; the
-  // tickets sit at a fixed offset so one zeroed buffer serves any max_pages_hint it is large enough for
-  uint32_t* ticket = static_cast<uint32_t*>(workspace);
-  double* scores = reinterpret_cast<double*>(static_cast<uint8_t*>(workspace) + sk_select_scores_offset(n_streams));
+  SK_CHECK_ARG(sel_out && sel_count && workspace, "select: NULL pointer");
+  p.invoke = invoke;
+  p.K = budget_pages;
+  p.ticket = static_cast<uint32_t*>(workspace);
+  p.approx = reinterpret_cast<float2*>(static_cast<uint8_t*>(workspace) + sk_select_scores_offset(n_streams));
+  p.exact = reinterpret_cast<double*>(p.approx + (int64_t)n_streams * max_pages_hint);
+  p.ws_pages = max_pages_hint;
+  p.sel_out = sel_out;
+  p.sel_count = sel_count;
+  p.sel_stride = sel_stride;
+  p.flags = flags;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (pool->dtype == SK_F16)
-    return select_dispatch<__half>(pv, n_streams, q, q_stream_stride, q_row_stride, row_mask, tokens, invoke,
-                                   budget_pages, max_pages_hint, sel_out, sel_count, sel_stride, scores, ticket, st);
-  return select_dispatch<__nv_bfloat16>(pv, n_streams, q, q_stream_stride, q_row_stride, row_mask, tokens, invoke,
-                                        budget_pages, max_pages_hint, sel_out, sel_count, sel_stride, scores, ticket,
-                                        st);
+  const bool f16 = pool->dtype == SK_F16;
+  if (pool->head_dim == 128)
+    return f16 ? select_launch<__half, 128>(p, n_streams, max_pages_hint, st)
+               : select_launch<__nv_bfloat16, 128>(p, n_streams, max_pages_hint, st);
+  return f16 ? select_launch<__half, 64>(p, n_streams, max_pages_hint, st)
+             : select_launch<__nv_bfloat16, 64>(p, n_streams, max_pages_hint, st);
+}
+
+extern "C" int sk_score_pages(const sk_pool* pool, int32_t n_streams, int32_t group_rows, const void* q,
+                              int64_t q_stream_stride, int64_t q_row_stride, const uint32_t* row_mask,
+                              const int32_t* tokens, double* scores_out, int32_t out_stride, void* stream) {
+  using namespace sk;
+  SelParams p;
+  int rc = fill_params(p, pool, n_streams, group_rows, q, q_stream_stride, q_row_stride, row_mask, tokens);
+  if (rc) return rc;
+  SK_CHECK_ARG(scores_out != nullptr && out_stride >= 1, "score: bad output");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int blocks = (out_stride + kWarps - 1) / kWarps;
+  dim3 grid(blocks < 1024 ? blocks : 1024, n_streams);
+  const bool f16 = pool->dtype == SK_F16;
+  if (pool->head_dim == 128) {
+    if (f16) score_kernel<__half, 128><<<grid, kThreads, 0, st>>>(p, scores_out, out_stride);
+    else score_kernel<__nv_bfloat16, 128><<<grid, kThreads, 0, st>>>(p, scores_out, out_stride);
+  } else {
+    if (f16) score_kernel<__half, 64><<<grid, kThreads, 0, st>>>(p, scores_out, out_stride);
+    else score_kernel<__nv_bfloat16, 64><<<grid, kThreads, 0, st>>>(p, scores_out, out_stride);
+  }
+  SK_CHECK_LAUNCH("score_kernel");
+  return SK_OK;
 }

@@ -103,14 +103,20 @@ class DecodeGraph:
             rc = lib.sk_select_pages(C.byref(abi), self.h_kv, self.g, self.q[li].data_ptr(), self.g * self.dp,
                                      self.dp, e._row_mask.data_ptr(), pool.tokens.data_ptr(), None, self.k_pages,
                                      self.max_pages_hint, self.sel[li].data_ptr(), self.cnt[li].data_ptr(),
-                                     self.sel[li].shape[1], ws.data_ptr(), ws.numel(), stream)
+                                     self.sel[li].shape[1], ws.data_ptr(), ws.numel(), _lib.SK_LAUNCH_PDL, stream)
             _lib.check(rc)
+        dws = pool.decode_workspace(self.g)
+        # programmatic dependent launches: each kernel's prologue (page table, the
+        # pages themselves, and on reuse steps the selection) overlaps the previous
+        # kernel's tail; q / the new token are read after the dependency wait
+        flags = _lib.SK_LAUNCH_PDL | (0 if select else _lib.SK_DECODE_SEL_READY)
         rc = lib.sk_decode_attn(C.byref(abi), self.h_kv, self.g, self.q[li].data_ptr(), self.g * self.dp, self.dp,
                                 self.k[li].data_ptr(), self.v[li].data_ptr(), self.dp, e._row_mask.data_ptr(),
                                 e.row_window_ptr(), self.sel[li].data_ptr(), self.cnt[li].data_ptr(),
                                 self.sel[li].shape[1], pool.tokens.data_ptr(),
                                 C.c_float(1.0 / math.sqrt(self.head_dim)), self.out[li].data_ptr(),
-                                self.g * self.dp, self.dp, _device.sk_dtype(self.dtype), 0, stream)
+                                self.g * self.dp, self.dp, _device.sk_dtype(self.dtype), flags, dws.data_ptr(),
+                                dws.numel(), stream)
         _lib.check(rc)
         if self.group is not None:  # layer boundary: head outputs of every rank
             import torch.distributed as dist

@@ -452,11 +452,12 @@ class Engine:
             self._check_windows(n_pages)
         out = torch.empty((h_kv * g, pool.Dp), dtype=self._dtype, device=dev)
         abi = pool.abi()
+        dws = pool.decode_workspace(g)
         rc = _lib.load().sk_decode_attn(
             C.byref(abi), h_kv, g, q.data_ptr(), g * pool.Dp, pool.Dp, kn.data_ptr(), vn.data_ptr(), pool.Dp,
             self._row_mask.data_ptr(), self.row_window_ptr(), sel.data_ptr(), cnt.data_ptr(), sel.shape[1],
             pool.tokens.data_ptr(), C.c_float(1.0 / math.sqrt(head_dim)), out.data_ptr(), g * pool.Dp, pool.Dp,
-            _device.sk_dtype(self._dtype), 1, _device.stream_ptr(dev))
+            _device.sk_dtype(self._dtype), 1, dws.data_ptr(), dws.numel(), _device.stream_ptr(dev))
         _lib.check(rc)
         for s in range(h_kv):
             pool.tokens_host[s] += 1

@@ -1,9 +1,11 @@
 """Query-aware page selection (LServe Eq. 2) on the device.
 
 API mirrors the reference ``sparsekv.selector`` (selector.py:22-189).  The
-scoring and top-K run in the K2 kernel (csrc/select.cu) in fp64 with the
-reference's tie-break (lower page index); results are bit-identical to the
-reference for inputs exactly representable in the device dtype.  The two
+scoring and top-K run in the K2 kernel (csrc/select.cu): tensor-core fp32
+scores with a rigorous error bound, the pages near the K-th score rescored
+exactly in fp64, the reference's tie-break (lower page index); results are
+bit-identical to the reference for inputs exactly representable in the
+device dtype.  The two
 scalar helpers ``logical_page_score`` / ``physical_page_score`` evaluate
 Eq. 2 for a single page on the host, like the reference's.
 """
@@ -70,21 +72,14 @@ class _Workspace:
 
     @staticmethod
     def _pages(ws: torch.Tensor, n_streams: int) -> int:
-        return (ws.numel() - _lib.load().sk_select_scores_offset(n_streams)) // (8 * n_streams)
-
-    @staticmethod
-    def scores(ws: torch.Tensor, n_streams: int, max_pages: int) -> torch.Tensor:
-        """f64 [n_streams, max_pages] page scores of the last launch on ws."""
-        off = _lib.load().sk_select_scores_offset(n_streams)
-        return ws[off:off + 8 * n_streams * max_pages].view(torch.float64).view(n_streams, max_pages)
+        return (ws.numel() - _lib.load().sk_select_scores_offset(n_streams)) // (16 * n_streams)
 
 
 def select_streams(pool: DevicePool, q: torch.Tensor, q_stream_stride: int, q_row_stride: int, group_rows: int,
                    row_mask: torch.Tensor, budget_pages: int, out: torch.Tensor, count: torch.Tensor,
                    first_stream: int = 0, n_streams: int | None = None, invoke: torch.Tensor | None = None,
                    max_pages_hint: int | None = None) -> torch.Tensor:
-    """Launch K2 over streams [first, first+n) of `pool`; returns the workspace
-    (its first n*max_pages_hint doubles hold the page scores)."""
+    """Launch K2 over streams [first, first+n) of `pool`; returns the workspace."""
     n = pool.n_streams - first_stream if n_streams is None else n_streams
     mp = max_pages_hint or max(1, max(pool.page_count(s) for s in range(first_stream, first_stream + n)))
     ws = _Workspace.get(pool.device, n, mp)
@@ -92,7 +87,7 @@ def select_streams(pool: DevicePool, q: torch.Tensor, q_stream_stride: int, q_ro
     rc = _lib.load().sk_select_pages(
         C.byref(abi), n, group_rows, q.data_ptr(), q_stream_stride, q_row_stride, row_mask.data_ptr(),
         pool.tokens.data_ptr() + 4 * first_stream, invoke.data_ptr() if invoke is not None else None,
-        budget_pages, mp, out.data_ptr(), count.data_ptr(), out.shape[-1], ws.data_ptr(), ws.numel(),
+        budget_pages, mp, out.data_ptr(), count.data_ptr(), out.shape[-1], ws.data_ptr(), ws.numel(), 0,
         _device.stream_ptr(pool.device))
     _lib.check(rc)
     return ws
@@ -119,8 +114,7 @@ def _pool_for_pages(pages: Sequence[PhysicalPage], page_size: int, device) -> De
     return pool
 
 
-def _run_select(q_group, pages: Sequence[PhysicalPage], budget_pages: int, page_size: int, device=None):
-    dev = _device.device_of(device)
+def _select_inputs(q_group, pages: Sequence[PhysicalPage], page_size: int, dev):
     for p in pages:
         if not p.stats:
             raise ValueError(f"page {p.page_id} carries no key statistics")
@@ -128,8 +122,8 @@ def _run_select(q_group, pages: Sequence[PhysicalPage], budget_pages: int, page_
     if q.ndim == 1:
         q = q[None, :]
     rows = q.shape[0]
-    if rows > 8:
-        raise ValueError("select_pages on the B200 path takes at most 8 query rows per KV head")
+    if rows > 32:
+        raise ValueError("select_pages on the B200 path takes at most 32 query rows per KV head")
     src = page_origin(pages[0])
     pool = None
     if src is not None and all(page_origin(p) == src for p in pages):
@@ -140,7 +134,13 @@ def _run_select(q_group, pages: Sequence[PhysicalPage], budget_pages: int, page_
     if pool is None:
         pool, first = _pool_for_pages(pages, page_size, dev), 0
     qd = _device.to_device(q, pool.dtype, pool.device, pool.Dp)
-    mask = torch.tensor([(1 << rows) - 1], dtype=torch.int32, device=pool.device)
+    mask = torch.tensor([(1 << rows) - 1], dtype=torch.int64, device=pool.device).to(torch.int32)
+    return pool, first, qd, mask, rows
+
+
+def _run_select(q_group, pages: Sequence[PhysicalPage], budget_pages: int, page_size: int, device=None):
+    dev = _device.device_of(device)
+    pool, first, qd, mask, rows = _select_inputs(q_group, pages, page_size, dev)
     k_out = max(1, min(budget_pages, len(pages)))
     out = torch.empty((1, max(k_out, 4)), dtype=torch.int32, device=pool.device)
     cnt = torch.empty(1, dtype=torch.int32, device=pool.device)
@@ -165,13 +165,17 @@ def select_pages(q_group, pages: Sequence[PhysicalPage], budget_tokens: int, pag
 
 def score_pages(q_group, pages: Sequence[PhysicalPage], *, device=None) -> np.ndarray:
     """selector.py:39-72 -- fp64 physical-page scores (max over group rows),
-    read back from the K2 kernel's scoring phase."""
+    by sk_score_pages (the exact arithmetic K2 ranks its boundary pages with)."""
     pages = list(pages)
-    n = len(pages)
-    padded = pages + [pages[0]] * max(0, 5 - n)  # K2 scores only when |pins| < K < n
-    out, cnt, ws = _run_select(q_group, padded, 4, pages[0].capacity, device)
-    torch.cuda.current_stream().synchronize()
-    return _Workspace.scores(ws, 1, len(padded))[0, :n].cpu().numpy().copy()
+    dev = _device.device_of(device)
+    pool, first, qd, mask, rows = _select_inputs(q_group, pages, pages[0].capacity, dev)
+    out = torch.empty((1, len(pages)), dtype=torch.float64, device=pool.device)
+    abi = pool.abi(first)
+    rc = _lib.load().sk_score_pages(C.byref(abi), 1, rows, qd.data_ptr(), 0, pool.Dp, mask.data_ptr(),
+                                    pool.tokens.data_ptr() + 4 * first, out.data_ptr(), len(pages),
+                                    _device.stream_ptr(pool.device))
+    _lib.check(rc)
+    return out[0].cpu().numpy().copy()
 
 
 def exact_top_k_pages(q_group, keys, budget_tokens: int, page_size: int, *, device=None) -> list:

@@ -40,10 +40,10 @@ def test_pure_host_entry_points(lib):
     assert b"sm_100a" in L.sk_version()
     assert L.sk_slot_bytes(128, 64, 4, 0) == 9216          # KV4 page: 8 KB codes + 1 KB bounds
     assert L.sk_slot_bytes(128, 64, 0, 0) == 32768         # fp16 page
-    assert L.sk_select_workspace(8, 2048) >= 8 * 2048 * 8
+    assert L.sk_select_workspace(8, 2048) >= 8 * 2048 * 16
     off = L.sk_select_scores_offset(8)
     assert off >= 8 * 4 and off % 256 == 0                 # tickets first, scores 256-B aligned after them
-    assert L.sk_select_workspace(8, 2048) == off + 8 * 2048 * 8
+    assert L.sk_select_workspace(8, 2048) == off + 8 * 2048 * 16
 
 
 def test_sass_contains_tcgen05_and_tma(lib):

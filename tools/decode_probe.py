@@ -69,11 +69,12 @@ for name, gates in [("balanced", [0.9 - 0.001 * h if h % 4 < 2 else 0.1 + 0.001 
     n_pages = -(-pool.tokens_host[0] // 64)
     ws = _Workspace.get(pool.device, HKV, n_pages)
     abi = pool.abi()
+    dws = pool.decode_workspace(g)
 
     def sel_call():
         rc = lib.sk_select_pages(C.byref(abi), HKV, g, q.data_ptr(), g * D, D, e._row_mask.data_ptr(),
                                  pool.tokens.data_ptr(), None, kp, n_pages, sel.data_ptr(), cnt.data_ptr(), kp,
-                                 ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
+                                 ws.data_ptr(), ws.numel(), 0, torch.cuda.current_stream().cuda_stream)
         _lib.check(rc)
 
     print(name, "select us", round(time_it(sel_call), 2))
@@ -84,7 +85,7 @@ for name, gates in [("balanced", [0.9 - 0.001 * h if h % 4 < 2 else 0.1 + 0.001 
             rc = lib.sk_decode_attn(C.byref(abi), HKV, g, q.data_ptr(), g * D, D, kn.data_ptr(), kn.data_ptr(), D,
                                     e._row_mask.data_ptr(), None, sel.data_ptr(), cnt.data_ptr(), kp,
                                     pool.tokens.data_ptr(), C.c_float(1 / math.sqrt(D)), out.data_ptr(), g * D, D,
-                                    _lib.SK_F16, fuse, torch.cuda.current_stream().cuda_stream)
+                                    _lib.SK_F16, fuse, dws.data_ptr(), dws.numel(), torch.cuda.current_stream().cuda_stream)
             _lib.check(rc)
 
         print(name, f"decode append={fuse} us", round(time_it(dec_call), 2))

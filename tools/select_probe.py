@@ -60,7 +60,7 @@ def probe(name, pool, row_mask, n_streams, g):
     def sel_call():
         rc = lib.sk_select_pages(C.byref(abi), n_streams, g, q.data_ptr(), g * D, D, row_mask.data_ptr(),
                                  pool.tokens.data_ptr(), None, kp, n_pages, sel.data_ptr(), cnt.data_ptr(), kp,
-                                 ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
+                                 ws.data_ptr(), ws.numel(), 0, torch.cuda.current_stream().cuda_stream)
         _lib.check(rc)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
