@@ -102,6 +102,18 @@ int sk_append_pages(const sk_pool* pool, int32_t n_streams, const void* k_src, c
                     int32_t max_pages_touched, void* stream);
 
 /*
+ * K1, decode step: one new token for every stream of n_layers pools that share
+ * dtype, head_dim, page_size and bits, in ONE launch (the appends of several
+ * layers of a decode step).  Layer l: pools[l] (host array), tokens[l] (host
+ * array of device counters, advanced by one); k / v of layer l, stream s at
+ * k_src / v_src + l*src_layer_stride + s*src_stream_stride (elements).  Same
+ * result as n_layers sk_append_pages(..., m_tokens = 1, ...) calls.
+ */
+int sk_append_token_layers(const sk_pool* pools, int32_t n_layers, int32_t n_streams, const void* k_src,
+                           const void* v_src, int64_t src_layer_stride, int64_t src_stream_stride,
+                           int32_t* const* tokens, void* stream);
+
+/*
  * K1b -- pool gather (chunked prefill).  Dequantises the resident pages of
  * streams [0, n_streams) (first n_tokens tokens, every stream holds that
  * many) into a token-major history: element (s, t, c) of K / V at

@@ -21,6 +21,7 @@ LIB_PATH = os.environ.get("SK_LIB_PATH") or os.path.join(os.path.dirname(os.path
 
 # every symbol include/sparsekv_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ("sk_version", "sk_last_error", "sk_device_supported", "sk_slot_bytes", "sk_append_pages",
+           "sk_append_token_layers",
            "sk_gather_pages", "sk_select_workspace", "sk_select_scores_offset", "sk_select_pages", "sk_score_pages",
            "sk_decode_workspace", "sk_decode_attn", "sk_prefill_attn")
 
@@ -47,6 +48,8 @@ _SIGS = {
     "sk_slot_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "sk_append_pages": (C.c_int, [C.POINTER(SkPool), C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                   C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "sk_append_token_layers": (C.c_int, [C.POINTER(SkPool), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
+                                         C.c_int64, C.POINTER(C.c_void_p), C.c_void_p]),
     "sk_gather_pages": (C.c_int, [C.POINTER(SkPool), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
                                   C.c_int64, C.c_void_p]),
     "sk_select_workspace": (C.c_int64, [C.c_int32, C.c_int32]),

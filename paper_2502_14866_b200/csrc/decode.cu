@@ -52,7 +52,7 @@ constexpr int kMaxRows = 8;    // group rows (query heads per KV head)
 constexpr int kMaxExtra = 64;  // sink + local pages
 constexpr int kMaxSel = 2048;  // selection entries staged in smem
 constexpr int kMaxCps = 32;    // CTAs per stream
-constexpr int kUnitTok = 32;   // tokens per work unit (two 16-token MMA tiles)
+constexpr int kUnitTok = 32;   // tokens per work unit when a stream spans several CTAs (two 16-token tiles)
 
 // CTAs per stream: fill the SMs when the streams are few, never more CTAs
 // than the stream's largest possible union needs (8 units per CTA).
@@ -221,13 +221,13 @@ struct RowState {
 // (token, lane%4) and (channel tile, lane) (sk_layout.cuh); P goes from the
 // S^T accumulator to the P^T operand with one movmatrix per 8x8.
 // KIND: 0 raw pages (MMA in T), 1 nibble codes, 2 byte codes (MMA in fp16).
-template <typename T, int KIND, int D, int P>
+template <typename T, int KIND, int D, int P, int UT>
 struct UnitData {
   static constexpr int RB = KIND == 0 ? 2 * D : (KIND == 1 ? D / 2 : D);
   static constexpr int KW = KIND == 1 ? D / 32 : (KIND == 2 ? D / 16 : D / 8);  // words per (token, lane%4)
   static constexpr int VW = KIND == 1 ? P / 32 : (KIND == 2 ? P / 16 : P / 8);  // words per (cn, lane), whole page
-  static constexpr int VU = KIND == 1 ? 1 : (KIND == 2 ? 2 : 4);                // of them used by one unit
-  uint32_t kw[2][2][KW];
+  static constexpr int VU = KIND == 1 ? UT / 2 : (KIND == 2 ? UT : 2 * UT);     // of them used by one unit
+  uint32_t kw[UT][2][KW];
   uint32_t vw[D / 8][VU];
   uint32_t kb_lo[D / 8], kb_hi[D / 8], vb_lo[D / 8], vb_hi[D / 8];
 };
@@ -235,9 +235,9 @@ struct UnitData {
 // Every load of one 32-token unit (tiles tt0, tt0+1 of the page in slot pg),
 // straight into registers -- issued before any math (one round trip), and
 // for the first unit before the kernel's dependency wait (PDL prologue).
-template <typename T, int KIND, int D, int P>
-__device__ __forceinline__ void unit_load(const uint8_t* pg, int tt0, UnitData<T, KIND, D, P>& u) {
-  using U = UnitData<T, KIND, D, P>;
+template <typename T, int KIND, int D, int P, int UT>
+__device__ __forceinline__ void unit_load(const uint8_t* pg, int tt0, UnitData<T, KIND, D, P, UT>& u) {
+  using U = UnitData<T, KIND, D, P, UT>;
   constexpr int NCT = D / 16;
   constexpr int RB = U::RB, KW = U::KW, VW = U::VW, VU = U::VU;
   const int lane = threadIdx.x & 31, g = lane >> 2, j = lane & 3;
@@ -246,7 +246,7 @@ __device__ __forceinline__ void unit_load(const uint8_t* pg, int tt0, UnitData<T
   const T* bnd = reinterpret_cast<const T*>(pg + 2 * P * RB);
   // K codes of tokens 16tt + g + 8h (A rows), this lane's dim chunk j
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < UT; ++i)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint8_t* src = kc + (16 * (tt0 + i) + 8 * h + g) * RB + j * (RB / 4);
@@ -272,8 +272,11 @@ __device__ __forceinline__ void unit_load(const uint8_t* pg, int tt0, UnitData<T
       const uint2 v = ldg8(src);
       u.vw[cn][0] = v.x; u.vw[cn][1] = v.y;
     } else {
-      const uint4 v = ldg16(src);
-      u.vw[cn][0] = v.x; u.vw[cn][1] = v.y; u.vw[cn][2] = v.z; u.vw[cn][3] = v.w;
+#pragma unroll
+      for (int w = 0; w < VU / 4; ++w) {
+        const uint4 v = ldg16(src + 16 * w);
+        u.vw[cn][4 * w] = v.x; u.vw[cn][4 * w + 1] = v.y; u.vw[cn][4 * w + 2] = v.z; u.vw[cn][4 * w + 3] = v.w;
+      }
     }
   }
   // bounds: K in kbound order (this lane's dims at j*D/4), V in vbound order
@@ -299,14 +302,14 @@ __device__ __forceinline__ void unit_load(const uint8_t* pg, int tt0, UnitData<T
 // (token, lane%4) and (channel tile, lane) (sk_layout.cuh); P goes from the
 // S^T accumulator to the P^T operand with one movmatrix per 8x8.
 // KIND: 0 raw pages (MMA in T), 1 nibble codes, 2 byte codes (MMA in fp16).
-template <typename T, int KIND, int D, int P>
-__device__ __forceinline__ void unit_compute(const UnitData<T, KIND, D, P>& u, int tt0, int tok_in_page,
+template <typename T, int KIND, int D, int P, int UT>
+__device__ __forceinline__ void unit_compute(const UnitData<T, KIND, D, P, UT>& u, int tt0, int tok_in_page,
                                              uint32_t att_mask, const uint32_t (&qw)[D / 8], float sl2,
                                              float inv_levels, RowState<D>& st) {
   using MT = typename std::conditional<KIND == 0, T, __half>::type;
   constexpr int NKS = D / 16;  // QK k-steps (16 dims)
   constexpr int NCT = D / 16;  // PV M-tiles (16 channels)
-  constexpr int TT = 2;        // 16-token tiles per unit
+  constexpr int TT = UT;       // 16-token tiles per unit
   const int lane = threadIdx.x & 31, g = lane >> 2, j = lane & 3;
   const auto& kw = u.kw;
   const auto& vw = u.vw;
@@ -443,11 +446,11 @@ __device__ __forceinline__ void unit_compute(const UnitData<T, KIND, D, P>& u, i
 #pragma unroll
     for (int i = 0; i < TT; ++i) {
       uint32_t a0, a1, a2, a3;  // (ch g, tok lo) (ch g+8, lo) (ch g, hi) (ch g+8, hi)
-      if constexpr (KIND == 1) {  // the unit's word: slots 2i, 2i+1 are tiles tt0+i
-        a0 = nib2h(vw[2 * ct][0], 2 * i);
-        a1 = nib2h(vw[2 * ct + 1][0], 2 * i);
-        a2 = nib2h(vw[2 * ct][0], 2 * i + 1);
-        a3 = nib2h(vw[2 * ct + 1][0], 2 * i + 1);
+      if constexpr (KIND == 1) {  // word i/2 of the unit, slots 2(i%2), 2(i%2)+1: tile tt0+i
+        a0 = nib2h(vw[2 * ct][i / 2], 2 * (i % 2));
+        a1 = nib2h(vw[2 * ct + 1][i / 2], 2 * (i % 2));
+        a2 = nib2h(vw[2 * ct][i / 2], 2 * (i % 2) + 1);
+        a3 = nib2h(vw[2 * ct + 1][i / 2], 2 * (i % 2) + 1);
       } else if constexpr (KIND == 2) {
         a0 = byte2h(vw[2 * ct][i], 0);
         a1 = byte2h(vw[2 * ct + 1][i], 0);
@@ -491,9 +494,9 @@ __device__ __forceinline__ void finish_out(const DecodeParams& prm, int s, int r
   else reinterpret_cast<__nv_bfloat16*>(prm.out)[oi] = __float2bfloat16_rn(O);
 }
 
-template <typename T, int KIND, int D, int P>
+template <typename T, int KIND, int D, int P, int UT>
 __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_constant__ DecodeParams prm) {
-  constexpr int UPP = P / kUnitTok;  // units per page
+  constexpr int UPP = P / (16 * UT);  // units per page
   __shared__ int s_sel[kMaxSel];
   __shared__ int s_extra[kWarps][kMaxExtra];
   __shared__ float s_m[kWarps][kMaxRows], s_l[kWarps][kMaxRows];
@@ -596,11 +599,11 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   int pg_next = 0;
   uint32_t um_next = 0;
   const uint8_t* slot_next = nullptr;
-  UnitData<T, KIND, D, P> ud;
+  UnitData<T, KIND, D, P, UT> ud;
   if (u < NU) {
     pg_next = unit_page(u, um_next);
     slot_next = pv.slot_ptr(s, pg_next);  // round trip 2 (page table)
-    if (16 * 2 * (u % UPP) < min(P, n_tok - pg_next * P)) unit_load<T, KIND, D, P>(slot_next, 2 * (u % UPP), ud);
+    if (16 * UT * (u % UPP) < min(P, n_tok - pg_next * P)) unit_load<T, KIND, D, P, UT>(slot_next, UT * (u % UPP), ud);
   }
   if (pdl && early_sel) asm volatile("griddepcontrol.wait;" ::: "memory");
   // ---- q and the new token: the previous kernel's outputs in a model --------
@@ -614,16 +617,24 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
       qw[ri] = row_ok ? __ldcg(reinterpret_cast<const uint32_t*>(qrow + d)) : 0u;
     }
   }
-  // scores of the new token (raw K, in-register; merged last, engine.py:276-277)
+  // the new token's raw K and warp w's q row (w < G): loaded now, scored after
+  // the units (engine.py:276-277 merges the new token last)
+  T qs_self[D / 32], ks_self[D / 32];
+  const T* vn = reinterpret_cast<const T*>(prm.v_new) + s * prm.new_ss;
+  float v_own[(kMaxRows * D + kDecThreads - 1) / kDecThreads];  // v_new of this thread's output elements
+#pragma unroll
+  for (int k = 0; k < (kMaxRows * D + kDecThreads - 1) / kDecThreads; ++k) {  // element tid + k * kDecThreads
+    const int i = tid + k * kDecThreads;
+    v_own[k] = i < G * D ? DT<T>::to_f(__ldcg(vn + i % D)) : 0.f;
+  }
   if (warp < G) {
     const T* qrow = reinterpret_cast<const T*>(prm.q) + s * prm.q_ss + (int64_t)warp * prm.q_rs;
     const T* kn = reinterpret_cast<const T*>(prm.k_new) + s * prm.new_ss;
-    float dot = 0.f;
 #pragma unroll
-    for (int c = lane; c < D; c += 32) dot = fmaf(DT<T>::to_f(__ldcg(qrow + c)), DT<T>::to_f(__ldcg(kn + c)), dot);
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
-    if (lane == 0) s_self[warp] = dot * prm.scale_log2;
+    for (int i = 0; i < D / 32; ++i) {
+      qs_self[i] = __ldcg(qrow + lane + 32 * i);
+      ks_self[i] = __ldcg(kn + lane + 32 * i);
+    }
   }
   bool first = true;
   for (; u < NU; u += ustride) {
@@ -638,14 +649,22 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
       for (int off = lane * 128; off < kSlotUsed; off += 32 * 128)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(slot_next + off));
     }
-    const int tok_in_page = min(P, n_tok - pg * P), tt0 = 2 * (u % UPP);
+    const int tok_in_page = min(P, n_tok - pg * P), tt0 = UT * (u % UPP);
     if (16 * tt0 < tok_in_page) {  // a unit past the open page's last token holds nothing
-      if (!first) unit_load<T, KIND, D, P>(slot, tt0, ud);
+      if (!first) unit_load<T, KIND, D, P, UT>(slot, tt0, ud);
       WSTAMP(0);
-      unit_compute<T, KIND, D, P>(ud, tt0, tok_in_page, um & gmask, qw, sl2, inv_levels, st);
+      unit_compute<T, KIND, D, P, UT>(ud, tt0, tok_in_page, um & gmask, qw, sl2, inv_levels, st);
       WSTAMP(1);
     }
     first = false;
+  }
+  if (warp < G) {
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < D / 32; ++i) dot = fmaf(DT<T>::to_f(qs_self[i]), DT<T>::to_f(ks_self[i]), dot);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+    if (lane == 0) s_self[warp] = dot * prm.scale_log2;
   }
   DSTAMP(2);
 
@@ -671,10 +690,13 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   DSTAMP(3);
   // every thread merges the warps for its own output elements (no serial
   // per-row step, one barrier): M = max_w m_w, O = sum_w 2^(m_w - M) O_w
-  const T* vn = reinterpret_cast<const T*>(prm.v_new) + s * prm.new_ss;
   const int64_t PF = part_floats(G, D);
   float* mine = prm.part + ((int64_t)s * prm.cps + blockIdx.x) * PF;
-  for (int i = tid; i < G * D; i += kDecThreads) {
+  constexpr int kEl = (kMaxRows * D + kDecThreads - 1) / kDecThreads;  // output elements per thread
+#pragma unroll
+  for (int k = 0; k < kEl; ++k) {
+    const int i = tid + k * kDecThreads;
+    if (i >= G * D) break;
     const int rr = i / D, c = i % D;
     float M = -INFINITY;
 #pragma unroll
@@ -689,7 +711,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     if (prm.cps == 1) {  // the CTA holds the whole stream: finish with the new token
       const float s_new = s_self[rr], Mt = fmaxf(M, s_new);
       const float f = M == -INFINITY ? 0.f : fast_exp2(M - Mt), fs = fast_exp2(s_new - Mt);
-      finish_out<T>(prm, s, rr, c, Mt, fmaf(f, L, fs), fmaf(f, O, fs * DT<T>::to_f(__ldcg(vn + c))));
+      finish_out<T>(prm, s, rr, c, Mt, fmaf(f, L, fs), fmaf(f, O, fs * v_own[k]));
     } else {
       mine[2 * G + i] = O;
       if (c == 0) {
@@ -728,33 +750,50 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   if (!s_last) return;
   mbar_wait(&s_bar, 0);
   DSTAMP(5);
-  for (int i = tid; i < G * D; i += kDecThreads) {
-    const int rr = i / D, c = i % D;
+  // per-(row, partial) merge factors 2^(m_b - M) once, the new token's at b = cps
+  const int cps = prm.cps;
+  float* s_f = &s_o[0][0][0];  // [G][cps + 1] (s_o is free now)
+  for (int i = tid; i < G * (cps + 1); i += kDecThreads) {
+    const int rr = i / (cps + 1), b = i % (cps + 1);
     const float s_new = s_self[rr];
     float M = s_new;
-    for (int b = 0; b < prm.cps; ++b) M = fmaxf(M, s_part[b * PF + rr]);
-    const float fs = fast_exp2(s_new - M);
-    float L = fs, O = fs * DT<T>::to_f(__ldcg(vn + c));
-#pragma unroll 4
-    for (int b = 0; b < prm.cps; ++b) {
-      const float pm = s_part[b * PF + rr];
-      const float f = pm == -INFINITY ? 0.f : fast_exp2(pm - M);
-      L = fmaf(f, s_part[b * PF + G + rr], L);
-      O = fmaf(f, s_part[b * PF + 2 * G + i], O);
+    for (int b2 = 0; b2 < cps; ++b2) M = fmaxf(M, s_part[b2 * PF + rr]);
+    const float pm = b < cps ? s_part[b * PF + rr] : s_new;
+    s_f[i] = pm == -INFINITY ? 0.f : fast_exp2(pm - M);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kEl; ++k) {
+    const int i = tid + k * kDecThreads;
+    if (i >= G * D) break;
+    const int rr = i / D, c = i % D;
+    const float* f = s_f + rr * (cps + 1);
+    const float fs = f[cps];
+    float L0 = fs, L1 = 0.f, O0 = fs * v_own[k], O1 = 0.f;
+    int b = 0;
+    for (; b + 1 < cps; b += 2) {  // two independent chains
+      L0 = fmaf(f[b], s_part[b * PF + G + rr], L0);
+      O0 = fmaf(f[b], s_part[b * PF + 2 * G + i], O0);
+      L1 = fmaf(f[b + 1], s_part[(b + 1) * PF + G + rr], L1);
+      O1 = fmaf(f[b + 1], s_part[(b + 1) * PF + 2 * G + i], O1);
     }
-    finish_out<T>(prm, s, rr, c, M, L, O);
+    if (b < cps) {
+      L0 = fmaf(f[b], s_part[b * PF + G + rr], L0);
+      O0 = fmaf(f[b], s_part[b * PF + 2 * G + i], O0);
+    }
+    finish_out<T>(prm, s, rr, c, 0.f, L0 + L1, O0 + O1);
   }
   DSTAMP(6);
 }
 
-template <typename T, int KIND, int D, int P>
-int launch_one(const DecodeParams& prm, int n_streams, cudaStream_t st) {
+template <typename T, int KIND, int D, int P, int UT>
+int launch_ut(const DecodeParams& prm, int n_streams, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(prm.cps, n_streams, 1);
   cfg.blockDim = dim3(kDecThreads, 1, 1);
   cfg.dynamicSmemBytes = prm.cps > 1 ? (size_t)prm.cps * part_floats(prm.G, D) * 4 : 0;
   if (cfg.dynamicSmemBytes > 0)  // static + dynamic exceeds the 48 KB default
-    cudaFuncSetAttribute(decode_kernel<T, KIND, D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(decode_kernel<T, KIND, D, P, UT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)cfg.dynamicSmemBytes);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -762,13 +801,23 @@ int launch_one(const DecodeParams& prm, int n_streams, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (prm.flags & SK_LAUNCH_PDL) ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, KIND, D, P>, prm);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, KIND, D, P, UT>, prm);
   if (e != cudaSuccess) {
     set_error(std::string("decode_kernel: ") + cudaGetErrorString(e));
     return SK_ECUDA;
   }
   SK_CHECK_LAUNCH("decode_kernel");
   return SK_OK;
+}
+
+// Unit size: 32 tokens when a stream's units are spread over several CTAs
+// (latency); whole 64-token pages when one CTA holds the stream (many units
+// per warp: the per-unit bounds, q' and sum setup is paid once per page).
+template <typename T, int KIND, int D, int P>
+int launch_one(const DecodeParams& prm, int n_streams, cudaStream_t st) {
+  constexpr int UT_BIG = (P >= 64 && KIND == 1) ? 4 : 2;  // raw / byte codes: registers only fit 2 tiles
+  if (prm.cps == 1 && UT_BIG != 2) return launch_ut<T, KIND, D, P, UT_BIG>(prm, n_streams, st);
+  return launch_ut<T, KIND, D, P, 2>(prm, n_streams, st);
 }
 
 template <typename T, int KIND>

@@ -205,46 +205,82 @@ __device__ double exact_page_score(const PoolView& pv, int s, int page, int n_lo
 }
 
 // ---- phase A: approximate scores + bounds of this warp's tiles ----------------
-// Tile = 16 logical pages.  Thread (g = lane/4, t = lane%4) loads logical
+// Tile = 16 logical pages.  Thread (g = lane/4, t = lane%4) holds logical
 // pages g and g+8 of the tile, bytes [64i + 16t, +16) of each 2D-channel row
-// for i < 2D/32 (each load instruction covers 8 x 64 contiguous bytes), and
+// for i < 2D/32 (a load instruction covers 8 x 64 contiguous bytes), and
 // k-step ks uses words 2(ks&1), 2(ks&1)+1 of chunk ks/2 -- i.e. the channel
 // permutation ch(ks, k) = (ks/2)*32 + t*8 + 4(ks&1) + {0,1 | 2,3}; bfrag holds
-// q' = [q- | q+] in the same permutation (built in select_kernel).
+// q' = [q- | q+] of every group row in the same permutation.  A warp's first
+// tile is loaded straight into registers, the following ones arrive by 1-D
+// bulk copies into the warp's shared-memory slot; every address is clamped
+// to the stream's allocated stats rows (not its token count), so the first
+// loads issue before the kernel has read anything.
 template <typename T, int D>
-__device__ __forceinline__ void load_tile(const SelParams& p, int s, int n_log, int ti, uint4 (&a)[2][D / 16]) {
+__device__ __forceinline__ void load_tile(const SelParams& p, int s, int rows_alloc, int ti, uint4 (&a)[2][D / 16]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int l0 = ti * 16 + g, l1 = l0 + 8;
-  const T* r0 = reinterpret_cast<const T*>(p.pv.stats_ptr(s, min(l0, n_log - 1))) + t * 8;
-  const T* r1 = reinterpret_cast<const T*>(p.pv.stats_ptr(s, min(l1, n_log - 1))) + t * 8;
+  const T* r0 = reinterpret_cast<const T*>(p.pv.stats_ptr(s, min(l0, rows_alloc - 1))) + t * 8;
+  const T* r1 = reinterpret_cast<const T*>(p.pv.stats_ptr(s, min(l1, rows_alloc - 1))) + t * 8;
 #pragma unroll
   for (int i = 0; i < D / 16; ++i) {
     a[0][i] = ldg_stream(r0 + i * 32);
     a[1][i] = ldg_stream(r1 + i * 32);
   }
 }
+template <int D>
+__device__ __forceinline__ void lds_tile(const uint8_t* tile, uint4 (&a)[2][D / 16]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const uint8_t* r0 = tile + g * (4 * D) + t * 16;  // a row: 2D values of 2 bytes
+  const uint8_t* r1 = r0 + 8 * (4 * D);
+#pragma unroll
+  for (int i = 0; i < D / 16; ++i) {
+    a[0][i] = *reinterpret_cast<const uint4*>(r0 + i * 64);
+    a[1][i] = *reinterpret_cast<const uint4*>(r1 + i * 64);
+  }
+}
+__device__ __forceinline__ void bulk_tile(uint8_t* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  mbar_arrive_expect_tx(bar, bytes);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ uint32_t tile_bytes(int ti, int rows_alloc, int D) {
+  return (uint32_t)(min(16, rows_alloc - ti * 16) * 4 * D);
+}
 
-// The warp's first tile arrives in `a` (its loads were issued before the B
-// fragments were built, so that DRAM round trip overlaps the q loads).
 template <typename T, int D, int NT>
-__device__ __forceinline__ void score_tiles(const SelParams& p, int s, int n_log, int n_pages, int rows,
-                                            const uint2* bfrag, float2* approx, uint4 (&a)[2][D / 16]) {
-  constexpr int KS = D / 8;     // k-steps over 2D channels
+__device__ __forceinline__ void score_tiles(const SelParams& p, int s, int n_log, int n_pages, uint32_t rmask,
+                                            int rows_alloc, int tile_hint, const uint2* bfrag, float2* approx,
+                                            uint4 (&a)[2][D / 16], uint8_t* slot, uint64_t* bar) {
+  constexpr int KS = D / 8;  // k-steps over 2D channels
   const int LP = p.pv.P / p.pv.L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   const int n_tiles = (n_log + 15) >> 4;
   const int tile0 = (blockIdx.x * kWarps + warp) * p.tiles_per_warp;
   const int tile1 = min(tile0 + p.tiles_per_warp, n_tiles);
+  const int tile1_hint = min(tile0 + p.tiles_per_warp, tile_hint);  // tiles whose copies were issued
   float run_v = -INFINITY, run_e = 0.f;  // LP = 32: a page spans two tiles of this warp
-  for (int ti = tile0; ti < tile1; ++ti) {
+  int ti = tile0;
+  for (; ti < tile1; ++ti) {
     const int l0 = ti * 16 + g, l1 = l0 + 8;
-    if (ti != tile0) load_tile<T, D>(p, s, n_log, ti, a);
-    // n-tiles innermost: each k-step's |A| words are formed once and die with it
-    float c[NT][4], m[NT][4];
+    if (ti != tile0) {  // tile ti sits in the slot; refill it with ti + 1 once every lane holds ti
+      mbar_wait(bar, (ti - tile0 - 1) & 1);
+      lds_tile<D>(slot, a);
+      __syncwarp();
+      if (lane == 0 && ti + 1 < tile1_hint)
+        bulk_tile(slot, p.pv.stats_ptr(s, (ti + 1) * 16), tile_bytes(ti + 1, rows_alloc, D), bar);
+    }
+    // n-tiles innermost: each k-step's |A| words are formed once and die with
+    // it; two accumulator chains (even / odd k-steps) halve the MMA latency chain
+    constexpr int CH = NT <= 2 ? 2 : 1;  // accumulator chains (registers allowing)
+    float c[NT][2][4], m[NT][2][4];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) c[nt][e] = m[nt][e] = 0.f;
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[nt][h][e] = m[nt][h][e] = 0.f;
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int i = ks >> 1, w = (ks & 1) * 2;
@@ -254,22 +290,26 @@ __device__ __forceinline__ void score_tiles(const SelParams& p, int s, int n_log
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const uint2 b = bfrag[(nt * KS + ks) * 32 + lane];
-        mma_f32<T>(c[nt], a0, a1, a2, a3, b.x, b.y);
-        mma_f32<T>(m[nt], m0, m1, m2, m3, abs2(b.x), abs2(b.y));
+        mma_f32<T>(c[nt][ks % CH], a0, a1, a2, a3, b.x, b.y);
+        mma_f32<T>(m[nt][ks % CH], m0, m1, m2, m3, abs2(b.x), abs2(b.y));
       }
     }
-    // accumulator: c0/c1 = (page g, rows 2t, 2t+1), c2/c3 = (page g+8, ...)
+    // accumulator: c0/c1 = (page g, group rows 2t, 2t+1), c2/c3 = (page g+8, ...);
+    // only the retrieval rows (bits of rmask) count
     float v0 = -INFINITY, v1 = -INFINITY, e0 = 0.f, e1 = 0.f;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        if (nt * 8 + 2 * t + e >= rows) continue;
-        const bool f0 = isfinite(m[nt][e]), f1 = isfinite(m[nt][2 + e]);
-        v0 = fmaxf(v0, f0 ? c[nt][e] : 0.f);
-        e0 = fmaxf(e0, f0 ? fmaf(m[nt][e], kErrRel, kErrAbs) : INFINITY);
-        v1 = fmaxf(v1, f1 ? c[nt][2 + e] : 0.f);
-        e1 = fmaxf(e1, f1 ? fmaf(m[nt][2 + e], kErrRel, kErrAbs) : INFINITY);
+        const int col = nt * 8 + 2 * t + e;
+        if (col >= 32 || !((rmask >> col) & 1u)) continue;
+        const float c0 = c[nt][0][e] + c[nt][1][e], c2 = c[nt][0][2 + e] + c[nt][1][2 + e];
+        const float ma = m[nt][0][e] + m[nt][1][e], mb = m[nt][0][2 + e] + m[nt][1][2 + e];
+        const bool f0 = isfinite(ma), f1 = isfinite(mb);
+        v0 = fmaxf(v0, f0 ? c0 : 0.f);
+        e0 = fmaxf(e0, f0 ? fmaf(ma, kErrRel, kErrAbs) : INFINITY);
+        v1 = fmaxf(v1, f1 ? c2 : 0.f);
+        e1 = fmaxf(e1, f1 ? fmaf(mb, kErrRel, kErrAbs) : INFINITY);
       }
     if (l0 >= n_log) { v0 = -INFINITY; e0 = 0.f; }
     if (l1 >= n_log) { v1 = -INFINITY; e1 = 0.f; }
@@ -313,6 +353,9 @@ __device__ __forceinline__ void score_tiles(const SelParams& p, int s, int n_log
       }
     }
   }
+  // a copy issued for a tile past the token count must land before the CTA exits
+  if (lane == 0 && ti < tile1_hint && ti > tile0) mbar_wait(bar, (ti - tile0 - 1) & 1);
+  else if (lane == 0 && ti == tile0 && tile0 + 1 < tile1_hint) mbar_wait(bar, 0);
 }
 
 // Block-wide exclusive scan of one value per thread in thread order; returns
@@ -497,9 +540,21 @@ __device__ void topk_exact(int n, int K, const double* scores, uint64_t* s_keys,
       reinterpret_cast<uint64_t*>(p.exact)[(int64_t)s * p.ws_pages + (i)] = t_;                   \
     }                                                                                             \
   } while (0)
+// CTA-level phase-A stamps: [stream][8 + 3 * blockIdx.x + i] of the same scratch
+#define SK_CSTAMP(i)                                                                                        \
+  do {                                                                                                      \
+    if (threadIdx.x == 0) {                                                                                 \
+      uint64_t t_;                                                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                                \
+      reinterpret_cast<uint64_t*>(p.exact)[(int64_t)s * p.ws_pages + 8 + 3 * blockIdx.x + (i)] = t_;        \
+    }                                                                                                       \
+  } while (0)
 #else
 #define SK_STAMP(i) \
   do {              \
+  } while (0)
+#define SK_CSTAMP(i) \
+  do {               \
   } while (0)
 #endif
 
@@ -687,27 +742,81 @@ __device__ bool topk_filtered(const SelParams& p, int s, int n, int n_log, const
   return true;
 }
 
+// Dynamic shared memory: [per-warp tile slots | B fragments]; phase B reuses
+// the slots for its radix histograms.
+template <int D>
+__host__ __device__ constexpr int sel_slot_bytes() { return 16 * 4 * D; }  // one tile
+template <int D>
+__host__ __device__ constexpr int sel_smem_bytes() {
+  return kWarps * sel_slot_bytes<D>() + 4 * (D / 8) * 32 * 8 > 2 * kNB * 4
+             ? kWarps * sel_slot_bytes<D>() + 4 * (D / 8) * 32 * 8
+             : 2 * kNB * 4;
+}
+
 template <typename T, int D>
 __global__ void __launch_bounds__(kThreads, 2) select_kernel(const __grid_constant__ SelParams p) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int row_idx[kMaxRows];
   __shared__ uint32_t is_last;
+  __shared__ uint64_t tile_bar[kWarps];
+  constexpr int KS = D / 8;
   const int s = blockIdx.y;
-  if (p.flags & SK_LAUNCH_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (p.invoke != nullptr && p.invoke[s] == 0) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool pdl = p.flags & SK_LAUNCH_PDL;
+  if (pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  SK_CSTAMP(0);
+  // ---- issued before anything is read: the warp's first tile (registers) and
+  //      its second (bulk copy into the warp's slot), addressed by the stream's
+  //      allocated stats rows; then the header -------------------------------
+  const int LP = p.pv.P / p.pv.L;
+  const int rows_alloc = p.pv.max_pages * LP;
+  const int tile_hint = (min(p.ws_pages * LP, rows_alloc) + 15) >> 4;
+  const int tile0 = (blockIdx.x * kWarps + warp) * p.tiles_per_warp;
+  const int tile1_hint = min(tile0 + p.tiles_per_warp, tile_hint);
+  uint8_t* slot = smem + warp * sel_slot_bytes<D>();
+  uint4 a0[2][D / 16];
+  if (tile0 < tile1_hint) load_tile<T, D>(p, s, rows_alloc, tile0, a0);
+  const bool copy1 = tile0 + 1 < tile1_hint;
+  if (lane == 0) {
+    mbar_init(&tile_bar[warp], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the init, before the async proxy uses it
+    if (copy1) bulk_tile(slot, p.pv.stats_ptr(s, (tile0 + 1) * 16), tile_bytes(tile0 + 1, rows_alloc, D), &tile_bar[warp]);
+  }
+  auto drain = [&]() {  // a CTA leaving early still owns its in-flight copy
+    if (lane == 0 && copy1) mbar_wait(&tile_bar[warp], 0);
+  };
+  const uint8_t inv = p.invoke != nullptr ? p.invoke[s] : 1;
   const uint32_t gmask = p.group_rows >= 32 ? 0xffffffffu : ((1u << p.group_rows) - 1u);
   const uint32_t rmask = p.row_mask[s] & gmask;
-  if (rmask == 0) return;
   const int n_tok = p.tokens[s];
+  // ---- q of every group row (the previous kernel's output in a model: after
+  //      the dependency wait), this thread's B-fragment entries --------------
+  if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  const T* qs = reinterpret_cast<const T*>(p.q) + s * p.q_ss;
+  const int NT = (p.group_rows + 7) >> 3;
+  // entry e = (nt, ks, lane) of the B fragments: 4 consecutive channels of group row nt*8 + lane/4
+  auto q_entry = [&](int e) -> uint2 {
+    const int nt = e / (KS * 32), ks = (e / 32) % KS, ln = e & 31;
+    const int r = nt * 8 + (ln >> 2), tt = ln & 3;
+    const int ch = (ks >> 1) * 32 + tt * 8 + (ks & 1) * 4;  // in [0, 2D); 4 channels of one half
+    return r < p.group_rows ? __ldcg(reinterpret_cast<const uint2*>(qs + (int64_t)r * p.q_rs + (ch % D)))
+                            : make_uint2(0u, 0u);
+  };
+  constexpr int kEnt = (KS * 32 + kThreads - 1) / kThreads;  // the first n-tile's entries, loaded now
+  uint2 qraw[kEnt];
+#pragma unroll
+  for (int k = 0; k < kEnt; ++k) qraw[k] = tid + k * kThreads < KS * 32 ? q_entry(tid + k * kThreads) : make_uint2(0u, 0u);
+  if (inv == 0 || rmask == 0) {
+    drain();
+    return;
+  }
   const int P = p.pv.P, L = p.pv.L;
   const int n_pages = min((n_tok + P - 1) / P, p.ws_pages);
-  const int n_log = min((n_tok + L - 1) / L, n_pages * (P / L));
-  const int tid = threadIdx.x;
+  const int n_log = min((n_tok + L - 1) / L, n_pages * LP);
   int32_t* sel_out = p.sel_out + (int64_t)s * p.sel_stride;
   const int npins = n_pins(n_pages);
-  if (n_pages <= 0) return;
-  if (p.K >= n_pages || p.K <= npins) {  // selector.py:98-103: no scoring
-    if (blockIdx.x == 0) {
+  if (n_pages <= 0 || p.K >= n_pages || p.K <= npins) {  // selector.py:98-103: no scoring
+    if (n_pages > 0 && blockIdx.x == 0) {
       if (p.K >= n_pages) {
         for (int i = tid; i < n_pages; i += kThreads) sel_out[i] = i;
       } else if (tid == 0) {  // pins {0, n-2, n-1}, ascending and deduplicated
@@ -717,63 +826,54 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(const __grid_consta
       }
       if (tid == 0) p.sel_count[s] = p.K >= n_pages ? n_pages : npins;
     }
+    drain();
     return;
   }
   const int rows = __popc(rmask);
-  if (tid == 0) {
+  if (tid == 0) {  // retrieval rows, for phase B's exact rescoring
     uint32_t m = rmask;
     for (int r = 0; r < rows; ++r) {
       row_idx[r] = __ffs(m) - 1;
       m &= m - 1;
     }
   }
-  __syncthreads();
-  const T* qs = reinterpret_cast<const T*>(p.q) + s * p.q_ss;
-  uint4 a0[2][D / 16];  // the warp's first tile, in flight while the B fragments are built
-  {
-    const int first = (blockIdx.x * kWarps + (tid >> 5)) * p.tiles_per_warp;
-    if (first < ((n_log + 15) >> 4)) load_tile<T, D>(p, s, n_log, first, a0);
-  }
-  // programmatic dependent launch: the stats, tokens and masks above were read
-  // before the dependency wait; q (the previous kernel's output in a model) after
-  if (p.flags & SK_LAUNCH_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
-  // ---- B fragments: q' = [q- | q+] of the retrieval rows, A's channel permutation
-  constexpr int KS = D / 8;
-  const int NT = (rows + 7) >> 3;
-  uint2* bfrag = reinterpret_cast<uint2*>(smem);
+  // ---- B fragments: q' = [q- | q+] of every group row, A's channel permutation
+  uint2* bfrag = reinterpret_cast<uint2*>(smem + kWarps * sel_slot_bytes<D>());
   for (int e = tid; e < NT * KS * 32; e += kThreads) {
-    const int nt = e / (KS * 32), ks = (e / 32) % KS, ln = e & 31;
-    const int r = nt * 8 + (ln >> 2), tt = ln & 3;
-    uint32_t w[2] = {0u, 0u};
-    if (r < rows) {
-      const int ch = (ks >> 1) * 32 + tt * 8 + (ks & 1) * 4;  // in [0, 2D); 4 channels, one half
-      const uint16_t* qr = reinterpret_cast<const uint16_t*>(qs + (int64_t)row_idx[r] * p.q_rs) + (ch % D);
-      const bool neg_half = ch < D;  // kmin channels take q-, kmax channels q+
+    const int k = e / kThreads;
+    const int ks = (e / 32) % KS, tt = e & 3;
+    const bool neg_half = ((ks >> 1) * 32 + tt * 8) < D;  // kmin channels take q-, kmax channels q+
+    const uint2 raw = k < kEnt ? qraw[k < kEnt ? k : 0] : q_entry(e);
+    uint32_t w[2] = {raw.x, raw.y};
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint16_t x = __ldcg(qr + c);
-        const bool neg = x & 0x8000u;
-        const uint32_t v = (neg == neg_half) ? x : 0u;
-        w[c >> 1] |= v << (16 * (c & 1));
+    for (int h = 0; h < 2; ++h) {
+      uint32_t o = 0;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const uint32_t x = (w[h] >> (16 * c)) & 0xFFFFu;
+        if (((x & 0x8000u) != 0) == neg_half) o |= x << (16 * c);
       }
+      w[h] = o;
     }
     bfrag[e] = make_uint2(w[0], w[1]);
   }
   __syncthreads();
+  SK_CSTAMP(1);
   // ---- phase A
   float2* approx = p.approx;
   switch (NT) {
-    case 1: score_tiles<T, D, 1>(p, s, n_log, n_pages, rows, bfrag, approx, a0); break;
-    case 2: score_tiles<T, D, 2>(p, s, n_log, n_pages, rows, bfrag, approx, a0); break;
-    case 3: score_tiles<T, D, 3>(p, s, n_log, n_pages, rows, bfrag, approx, a0); break;
-    default: score_tiles<T, D, 4>(p, s, n_log, n_pages, rows, bfrag, approx, a0); break;
+    case 1: score_tiles<T, D, 1>(p, s, n_log, n_pages, rmask, rows_alloc, tile_hint, bfrag, approx, a0, slot, &tile_bar[warp]); break;
+    case 2: score_tiles<T, D, 2>(p, s, n_log, n_pages, rmask, rows_alloc, tile_hint, bfrag, approx, a0, slot, &tile_bar[warp]); break;
+    case 3: score_tiles<T, D, 3>(p, s, n_log, n_pages, rmask, rows_alloc, tile_hint, bfrag, approx, a0, slot, &tile_bar[warp]); break;
+    default: score_tiles<T, D, 4>(p, s, n_log, n_pages, rmask, rows_alloc, tile_hint, bfrag, approx, a0, slot, &tile_bar[warp]); break;
   }
   // ---- CTA ticket: the stream's last CTA runs phase B
 #ifndef SK_SEL_ABLATE  // timing builds only (tools/ab_variant.sh): 1 = phase A only, 2 = no phase B
 #define SK_SEL_ABLATE 0
 #endif
-  if (SK_SEL_ABLATE == 1) return;
   __syncthreads();
+  SK_CSTAMP(2);
+  if (SK_SEL_ABLATE == 1) return;
   if (tid == 0) {  // bar.sync + a gpu-scope acq_rel RMW: releases the CTA's slots, acquires the others'
     uint32_t t;
     asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(p.ticket + s) : "memory");
@@ -785,6 +885,12 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(const __grid_consta
   uint32_t* hist2 = reinterpret_cast<uint32_t*>(smem);
   SK_STAMP(0);
   bool ok = false;
+#ifdef SK_SEL_TWICE  // timing experiment: a second identical phase B (warm instruction cache), stamped
+  if (n_pages <= 8 * kThreads) {
+    topk_filtered<T, D, 8>(p, s, n_pages, n_log, qs, row_idx, rows, hist2);
+    __syncthreads();
+  }
+#endif
   if (n_pages <= 8 * kThreads) ok = topk_filtered<T, D, 8>(p, s, n_pages, n_log, qs, row_idx, rows, hist2);
   else if (n_pages <= 16 * kThreads) ok = topk_filtered<T, D, 16>(p, s, n_pages, n_log, qs, row_idx, rows, hist2);
   else if (n_pages <= 32 * kThreads) ok = topk_filtered<T, D, 32>(p, s, n_pages, n_log, qs, row_idx, rows, hist2);
@@ -793,7 +899,6 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(const __grid_consta
   // ---- slow path: exact fp64 score of every non-pinned page, exact radix select
   __syncthreads();
   double* exact = p.exact + (int64_t)s * p.ws_pages;
-  const int warp = tid >> 5, lane = tid & 31;
   for (int i = warp; i < n_pages; i += kWarps) {
     if (is_pin(i, n_pages)) continue;
     const double sc = exact_page_score<T, D>(p.pv, s, i, n_log, qs, p.q_rs, row_idx, rows);
@@ -831,8 +936,6 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const __grid_constant__
   }
 }
 
-constexpr int kSmemBytes = 2 * kNB * 4;  // phase B histograms (>= the B fragments: 4 x 16 x 32 x 8 B)
-static_assert(kSmemBytes >= 4 * 16 * 32 * 8, "B fragments must fit the dynamic shared memory");
 
 template <typename T, int D>
 int select_launch(const SelParams& p0, int n_streams, int max_pages, cudaStream_t st) {
@@ -845,6 +948,7 @@ int select_launch(const SelParams& p0, int n_streams, int max_pages, cudaStream_
   tpw = tpw < 1 ? 1 : tpw;
   if (LP > 16) tpw = (tpw + LP / 16 - 1) / (LP / 16) * (LP / 16);  // a page's tiles stay in one warp
   p.tiles_per_warp = tpw;
+  constexpr int kSmemBytes = sel_smem_bytes<D>();
   p.smem_bytes = kSmemBytes;
   cudaFuncSetAttribute(select_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   cudaLaunchConfig_t cfg = {};

@@ -5,7 +5,10 @@ on reuse-window starts) and K3 split-KV decode with the fused append.  At
 128k context one layer's kernels take a few microseconds, so Python launch
 overhead would dominate; this runner captures the whole multi-layer step
 into two CUDA graphs (selection step / reuse step) over static buffers and
-replays them.  Token counters, page tables and workspaces are device
+replays them.  Inside a graph the kernels chain by programmatic dependent
+launch, and the one-token appends of every `append_group` layers run as one
+launch on a side stream, overlapping the following layers' attention.
+Token counters, page tables and workspaces are device
 resident, so replays need no host->device traffic besides the new q/k/v
 rows.  Per-engine host bookkeeping (token mirrors, step counters, ledger)
 is advanced exactly like Engine.decode_step would.
@@ -30,7 +33,8 @@ from .selector import _Workspace, selection_size
 
 
 class DecodeGraph:
-    def __init__(self, engines: list, max_steps: int, head_dim: int, record_ledger: bool = True, group=None):
+    def __init__(self, engines: list, max_steps: int, head_dim: int, record_ledger: bool = True, group=None,
+                 append_group: int = 8):
         if not engines:
             raise ValueError("need at least one engine")
         if record_ledger and any(not hasattr(e, "_plans") for e in engines):
@@ -41,6 +45,7 @@ class DecodeGraph:
         self.dev = e0.device
         self.head_dim = head_dim
         self.record_ledger = record_ledger
+        self.append_group = max(1, int(append_group))  # layers per K1 append launch
         pools = [e.cache.pool for e in engines]
         # streams may hold different token counts (a ragged batch: per-sequence
         # page tables); every layer must hold the same counts stream by stream
@@ -121,17 +126,27 @@ class DecodeGraph:
         if self.group is not None:  # layer boundary: head outputs of every rank
             import torch.distributed as dist
             dist.all_gather_into_tensor(self.gathered[li], self.out[li], group=self.group)
-        # K1 one-token append on a side stream: overlaps the next layer's attention
-        side.wait_stream(main)
-        rc = lib.sk_append_pages(C.byref(abi), self.h_kv, self.k[li].data_ptr(), self.v[li].data_ptr(), self.dp, 0,
-                                 pool.tokens.data_ptr(), 1, 1, side.cuda_stream)
+
+    def _launch_appends(self, l0: int, l1: int, side) -> None:
+        """K1 one-token appends of layers [l0, l1) in one launch on the side
+        stream, behind those layers' attention: it overlaps the next layers'."""
+        n = l1 - l0
+        pools = (_lib.SkPool * n)(*[self.pools[li].abi() for li in range(l0, l1)])
+        toks = (C.c_void_p * n)(*[self.pools[li].tokens.data_ptr() for li in range(l0, l1)])
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        rc = _lib.load().sk_append_token_layers(pools, n, self.h_kv, self.k[l0].data_ptr(), self.v[l0].data_ptr(),
+                                                self.h_kv * self.dp, self.dp, toks, side.cuda_stream)
         _lib.check(rc)
 
     def _launch_step(self, select: bool) -> None:
         main = torch.cuda.current_stream(self.dev)
         side = self._side
-        for li in range(len(self.engines)):
+        L, l0 = len(self.engines), 0
+        for li in range(L):
             self._launch_layer(li, select, side)
+            if li + 1 - l0 == self.append_group or li == L - 1:
+                self._launch_appends(l0, li + 1, side)
+                l0 = li + 1
         main.wait_stream(side)
 
     def _capture(self) -> None:

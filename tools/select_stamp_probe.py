@@ -41,3 +41,15 @@ for it in range(3):
     for s in range(HKV):
         t = st[s].tolist()
         print(it, s, [t[i + 1] - t[i] for i in range(5)], "total", t[5] - t[0])
+    import numpy as np
+    ph = ws[off:off + 8 * HKV * n_pages].view(torch.int64).view(HKV, n_pages)[:, 8:8 + 3 * 64].cpu().numpy()
+    ph = ph.reshape(HKV, -1, 3)
+    ph = ph[ph[:, :, 0] > 0]
+    t0 = ph[:, 0].min()
+    print(it, "phase A over %d CTAs: start spread %.2f us, prologue %.2f us, tiles %.2f us (max end %.2f us)" % (
+        len(ph), (ph[:, 0].max() - t0) / 1e3, np.mean(ph[:, 1] - ph[:, 0]) / 1e3, np.mean(ph[:, 2] - ph[:, 1]) / 1e3,
+        (ph[:, 2].max() - t0) / 1e3))
+    b0 = st[:, 0].numpy()
+    b5 = st[:, 5].numpy()
+    print(it, "phase B (last CTAs): start %.2f..%.2f us, end %.2f us after the first CTA's start" % (
+        (b0.min() - t0) / 1e3, (b0.max() - t0) / 1e3, (b5.max() - t0) / 1e3))
