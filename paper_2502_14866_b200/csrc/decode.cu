@@ -51,7 +51,7 @@ constexpr int kWarps = kDecThreads / 32;
 constexpr int kMaxRows = 8;    // group rows (query heads per KV head)
 constexpr int kMaxExtra = 64;  // sink + local pages
 constexpr int kMaxSel = 2048;  // selection entries staged in smem
-constexpr int kMaxCps = 32;    // CTAs per stream
+constexpr int kMaxCps = 31;    // CTAs per stream (the finish gives each a lane, plus the new token)
 constexpr int kUnitTok = 32;   // tokens per work unit when a stream spans several CTAs (two 16-token tiles)
 
 // CTAs per stream: fill the SMs when the streams are few, never more CTAs
@@ -750,16 +750,24 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   if (!s_last) return;
   mbar_wait(&s_bar, 0);
   DSTAMP(5);
-  // per-(row, partial) merge factors 2^(m_b - M) once, the new token's at b = cps
+  // per-(row, partial) merge factors 2^(m_b - M) once -- warp rr, lane b (the new
+  // token's at b = cps) -- and the reciprocal of each row's normaliser L
   const int cps = prm.cps;
   float* s_f = &s_o[0][0][0];  // [G][cps + 1] (s_o is free now)
-  for (int i = tid; i < G * (cps + 1); i += kDecThreads) {
-    const int rr = i / (cps + 1), b = i % (cps + 1);
+  float* s_rl = s_f + G * (kMaxCps + 1);
+  if (warp < G) {
+    const int rr = warp;
     const float s_new = s_self[rr];
-    float M = s_new;
-    for (int b2 = 0; b2 < cps; ++b2) M = fmaxf(M, s_part[b2 * PF + rr]);
-    const float pm = b < cps ? s_part[b * PF + rr] : s_new;
-    s_f[i] = pm == -INFINITY ? 0.f : fast_exp2(pm - M);
+    const float pm = lane < cps ? s_part[lane * PF + rr] : (lane == cps ? s_new : -INFINITY);
+    float M = pm;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    const float f = pm == -INFINITY ? 0.f : fast_exp2(pm - M);
+    float L = lane < cps ? f * s_part[lane * PF + G + rr] : (lane == cps ? f : 0.f);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+    if (lane <= cps) s_f[rr * (kMaxCps + 1) + lane] = f;
+    if (lane == 0) s_rl[rr] = 1.f / L;
   }
   __syncthreads();
 #pragma unroll
@@ -767,21 +775,12 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     const int i = tid + k * kDecThreads;
     if (i >= G * D) break;
     const int rr = i / D, c = i % D;
-    const float* f = s_f + rr * (cps + 1);
-    const float fs = f[cps];
-    float L0 = fs, L1 = 0.f, O0 = fs * v_own[k], O1 = 0.f;
-    int b = 0;
-    for (; b + 1 < cps; b += 2) {  // two independent chains
-      L0 = fmaf(f[b], s_part[b * PF + G + rr], L0);
-      O0 = fmaf(f[b], s_part[b * PF + 2 * G + i], O0);
-      L1 = fmaf(f[b + 1], s_part[(b + 1) * PF + G + rr], L1);
-      O1 = fmaf(f[b + 1], s_part[(b + 1) * PF + 2 * G + i], O1);
-    }
-    if (b < cps) {
-      L0 = fmaf(f[b], s_part[b * PF + G + rr], L0);
-      O0 = fmaf(f[b], s_part[b * PF + 2 * G + i], O0);
-    }
-    finish_out<T>(prm, s, rr, c, 0.f, L0 + L1, O0 + O1);
+    const float* f = s_f + rr * (kMaxCps + 1);
+    float O[4] = {f[cps] * v_own[k], 0.f, 0.f, 0.f};  // four independent chains
+#pragma unroll
+    for (int b = 0; b < kMaxCps; ++b)
+      if (b < cps) O[b & 3] = fmaf(f[b], s_part[b * PF + 2 * G + i], O[b & 3]);
+    finish_out<T>(prm, s, rr, c, 0.f, 1.f / s_rl[rr], (O[0] + O[1]) + (O[2] + O[3]));
   }
   DSTAMP(6);
 }
