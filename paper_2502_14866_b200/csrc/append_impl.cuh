@@ -7,7 +7,7 @@
 namespace sk {
 
 __host__ __device__ inline size_t append_smem_bytes(int D, int P) {
-  return (size_t)2 * P * D * 2 + 6 * D * sizeof(double);
+  return (size_t)2 * P * D * 2 + 6 * D * sizeof(double) + 4 * D * sizeof(float);
 }
 
 // code = clip(round_half_even((x - lo) / scale), 0, levels), computed so the
@@ -21,6 +21,17 @@ __device__ __forceinline__ uint32_t quant_code(double x, double lo, double scale
   if (fabs(fabs(t - r) - 0.5) < 1e-9) r = rint(__ddiv_rn(d, scale));
   r = fmin(fmax(r, 0.0), double(levels));
   return uint32_t(r);
+}
+// The same code from an fp32 quotient: t32 = (x - lo) * (1/scale) in fp32 is
+// within |t| * 2^-22 < 2^-14 of the fp64 quotient (t <= 255), so its rounding
+// agrees with numpy's whenever t32 is farther than 2^-10 from a .5 tie; the
+// (rare) near-tie quotients take the fp64 path above.
+__device__ __forceinline__ uint32_t quant_code32(float x, float lo32, float inv32, double lo, double scale,
+                                                 double inv, int levels) {
+  const float t = (x - lo32) * inv32;
+  const float r = rintf(t);
+  if (fabsf(fabsf(t - r) - 0.5f) < 0x1p-10f) return quant_code((double)x, lo, scale, inv, levels);
+  return (uint32_t)fminf(fmaxf(r, 0.f), (float)levels);
 }
 
 // Rebuild page p of stream s after tokens [n0, n1) were appended: raw page
@@ -65,6 +76,8 @@ __device__ void append_page(const PoolView& pv, int s, int p, int n0, int n1, co
   double* s_lo = reinterpret_cast<double*>(rv + P * D);  // [2][D]
   double* s_sc = s_lo + 2 * D;                           // [2][D]
   double* s_inv = s_sc + 2 * D;                          // [2][D]
+  float* s_lo32 = reinterpret_cast<float*>(s_inv + 2 * D);  // [2][D]
+  float* s_inv32 = s_lo32 + 2 * D;                           // [2][D]
 
   // 1. raw page -> smem (staging for positions < n0, new tokens otherwise)
   const T* stg_k = reinterpret_cast<const T*>(pv.staging_ptr(s, 0));
@@ -95,23 +108,42 @@ __device__ void append_page(const PoolView& pv, int s, int p, int n0, int n1, co
     // 2. per-channel bounds for K (which=0) and V (which=1)
     T* bnd = reinterpret_cast<T*>(pv.bounds(slot));
     const int levels = (1 << bits) - 1;
-    for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) {
-      int which = i / D, c = i % D;
+    // channel pair (2q, 2q+1) of K (q < D/2) or V: 256/D threads split its
+    // tokens, 32-bit loads, then a shuffle across those adjacent lanes
+    {
+      const int tpp = blockDim.x / D;  // threads per channel pair (2 at D = 128)
+      const int pair = threadIdx.x / tpp, sp = threadIdx.x % tpp;
+      const int which = pair / (D / 2), c = 2 * (pair % (D / 2));
       const T* raw = which ? rv : rk;
-      float lo = DT<T>::to_f(raw[c]), hi = lo;
-      for (int t = 1; t < ntok; ++t) {
-        float x = DT<T>::to_f(raw[t * D + c]);
-        lo = fminf(lo, x);
-        hi = fmaxf(hi, x);
+      float lo0 = INFINITY, hi0 = -INFINITY, lo1 = INFINITY, hi1 = -INFINITY;
+      for (int t = sp; t < ntok; t += tpp) {
+        const float2 x = DT<T>::to_f2(*reinterpret_cast<const uint32_t*>(raw + t * D + c));
+        lo0 = fminf(lo0, x.x);
+        hi0 = fmaxf(hi0, x.x);
+        lo1 = fminf(lo1, x.y);
+        hi1 = fmaxf(hi1, x.y);
       }
-      int pos = which ? vbound_pos(c, D) : kbound_pos(c, D);
-      bnd[(2 * which) * D + pos] = DT<T>::from_f(lo);  // exact: lo/hi are T values
-      bnd[(2 * which + 1) * D + pos] = DT<T>::from_f(hi);
-      double sc = ((double)hi - (double)lo) / levels;
-      if (!(sc > 0.0)) sc = 1.0;
-      s_lo[i] = lo;
-      s_sc[i] = sc;
-      s_inv[i] = 1.0 / sc;
+      for (int off = 1; off < tpp; off <<= 1) {
+        lo0 = fminf(lo0, __shfl_xor_sync(0xffffffffu, lo0, off));
+        hi0 = fmaxf(hi0, __shfl_xor_sync(0xffffffffu, hi0, off));
+        lo1 = fminf(lo1, __shfl_xor_sync(0xffffffffu, lo1, off));
+        hi1 = fmaxf(hi1, __shfl_xor_sync(0xffffffffu, hi1, off));
+      }
+      if (sp < 2) {
+        const int ch = c + sp;
+        const float lo = sp ? lo1 : lo0, hi = sp ? hi1 : hi0;
+        const int i = which * D + ch;
+        const int pos = which ? vbound_pos(ch, D) : kbound_pos(ch, D);
+        bnd[(2 * which) * D + pos] = DT<T>::from_f(lo);  // exact: lo/hi are T values
+        bnd[(2 * which + 1) * D + pos] = DT<T>::from_f(hi);
+        double sc = ((double)hi - (double)lo) / levels;
+        if (!(sc > 0.0)) sc = 1.0;
+        s_lo[i] = lo;
+        s_sc[i] = sc;
+        s_inv[i] = 1.0 / sc;
+        s_lo32[i] = lo;
+        s_inv32[i] = (float)(1.0 / sc);
+      }
     }
     __syncthreads();
     // 3. codes, written one 32-bit word at a time in the fragment-native
@@ -120,37 +152,65 @@ __device__ void append_page(const PoolView& pv, int s, int p, int n0, int n1, co
       if (t >= ntok) return 0u;
       const T* raw = which ? rv : rk;
       int i = which * D + c;
-      return quant_code((double)DT<T>::to_f(raw[t * D + c]), s_lo[i], s_sc[i], s_inv[i], levels);
+      return quant_code32(DT<T>::to_f(raw[t * D + c]), s_lo32[i], s_inv32[i], s_lo[i], s_sc[i], s_inv[i], levels);
     };
     uint32_t* kw = reinterpret_cast<uint32_t*>(kc);
     uint32_t* vw = reinterpret_cast<uint32_t*>(vc);
     if (bits <= 4) {
+      // K: blockDim is a multiple of the D/8 words of a token, so a thread keeps
+      // one (j, w) -- the same 8 dims (4 adjacent pairs) -- for every token it
+      // codes: their (lo, 1/scale) stay in registers, raw values load as pairs
       const int kwords = P * D / 8, wpc = D / 32;  // words per (token, j) chunk
-      for (int wi = threadIdx.x; wi < kwords; wi += blockDim.x) {
-        int t = wi / (D / 8), rem = wi % (D / 8), j = rem / wpc, w = rem % wpc;
-        uint32_t word = 0;
+      {
+        const int rem = threadIdx.x % (D / 8), j = rem / wpc, w = rem % wpc;
+        int dp[4];
+        float lo32[8], inv32[8];
 #pragma unroll
-        for (int slot = 0; slot < 4; ++slot)
+        for (int slot = 0; slot < 4; ++slot) {
+          const int ri = 4 * w + slot;
+          dp[slot] = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j;
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            int ri = 4 * w + slot, d = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j + e;
-            word |= code_at(0, t, d) << (4 * slot + 16 * e);
+            lo32[2 * slot + e] = s_lo32[dp[slot] + e];
+            inv32[2 * slot + e] = s_inv32[dp[slot] + e];
           }
-        kw[wi] = word;
+        }
+        for (int wi = threadIdx.x; wi < kwords; wi += blockDim.x) {
+          const int t = wi / (D / 8);
+          uint32_t word = 0;
+          if (t < ntok) {
+#pragma unroll
+            for (int slot = 0; slot < 4; ++slot) {
+              const float2 x = DT<T>::to_f2(*reinterpret_cast<const uint32_t*>(rk + t * D + dp[slot]));
+              const uint32_t c0 = quant_code32(x.x, lo32[2 * slot], inv32[2 * slot], s_lo[dp[slot]], s_sc[dp[slot]],
+                                               s_inv[dp[slot]], levels);
+              const uint32_t c1 = quant_code32(x.y, lo32[2 * slot + 1], inv32[2 * slot + 1], s_lo[dp[slot] + 1],
+                                               s_sc[dp[slot] + 1], s_inv[dp[slot] + 1], levels);
+              word |= (c0 << (4 * slot)) | (c1 << (4 * slot + 16));
+            }
+          }
+          kw[wi] = word;
+        }
       }
+      // V: a thread codes whole (channel tile, lane) chunks -- one channel each
       const int vwpl = P / 32;  // words per (cn, lane)
-      for (int wi = threadIdx.x; wi < kwords; wi += blockDim.x) {
-        int cn = wi / (32 * vwpl), rem = wi % (32 * vwpl), lane = rem / vwpl, w = rem % vwpl;
-        int c = 8 * cn + lane / 4, j = lane % 4;
-        uint32_t word = 0;
+      for (int cl = threadIdx.x; cl < (D / 8) * 32; cl += blockDim.x) {
+        const int cn = cl / 32, lane = cl % 32;
+        const int c = 8 * cn + lane / 4, j = lane % 4, i = D + c;
+        const float lo = s_lo32[i], inv = s_inv32[i];
+        for (int w = 0; w < vwpl; ++w) {
+          uint32_t word = 0;
 #pragma unroll
-        for (int slot = 0; slot < 4; ++slot)
+          for (int slot = 0; slot < 4; ++slot)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            int ri = 4 * w + slot, t = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j + e;
-            word |= code_at(1, t, c) << (4 * slot + 16 * e);
-          }
-        vw[wi] = word;
+            for (int e = 0; e < 2; ++e) {
+              const int ri = 4 * w + slot, t = 16 * (ri / 2) + 8 * (ri % 2) + 2 * j + e;
+              if (t < ntok)
+                word |= quant_code32(DT<T>::to_f(rv[t * D + c]), lo, inv, s_lo[i], s_sc[i], s_inv[i], levels)
+                        << (4 * slot + 16 * e);
+            }
+          vw[cl * vwpl + w] = word;
+        }
       }
     } else {
       const int kwords = P * D / 4, wpc = D / 16;
