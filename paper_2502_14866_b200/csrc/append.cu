@@ -52,29 +52,36 @@ __global__ void __launch_bounds__(256) append_one_kernel(const __grid_constant__
   const int n0 = tokens[s];
   const T* kn = reinterpret_cast<const T*>(a.k) + l * a.layer_stride + s * a.stream_stride;
   const T* vn = reinterpret_cast<const T*>(a.v) + l * a.layer_stride + s * a.stream_stride;
-  if (n0 % pv.P == 0 || pv.bits == 0) {
+  if (n0 % pv.P == 0 || pv.bits == 0 || gridDim.x == 1) {  // fresh page / raw pool / one CTA per stream
     if (part == 0) append_page<T>(pv, s, n0 / pv.P, n0, n0 + 1, kn, vn, 0, smem);
   } else {
     append_one_part<T>(pv, s, part, n0, kn, vn, smem);
   }
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (gridDim.x > 1)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  else
+    __syncthreads();
   if (part == 0 && threadIdx.x == 0) tokens[s] = n0 + 1;
 }
 
+// Parts per (layer, stream): a cluster of kAppendParts when the appends are
+// few (latency), one CTA rebuilding the page (append_page) once they alone
+// fill the GPU several times over (cfg4's 128 streams x 8 layers).
 template <typename T>
 int append_one_launch(const AppendLayers& a, int n_layers, int n_streams, size_t smem, cudaStream_t st) {
+  const int parts = (int64_t)n_layers * n_streams > 2 * device_sm_count() ? 1 : kAppendParts;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kAppendParts, n_streams, n_layers);
+  cfg.gridDim = dim3(parts, n_streams, n_layers);
   cfg.blockDim = dim3(256, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kAppendParts;
+  attr[0].val.clusterDim.x = parts;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = parts > 1 ? 1 : 0;
   cudaFuncSetAttribute(append_one_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaError_t e = cudaLaunchKernelEx(&cfg, append_one_kernel<T>, a);
   if (e != cudaSuccess) {

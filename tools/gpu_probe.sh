@@ -1,2 +1,3 @@
-SK_CTX=32768 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"append_kernel" -c 1 -o gpurun_out/ncu_k1b python tools/profile_workload.py > /dev/null 2>&1
-ls gpurun_out/ncu_k1b.ncu-rep
+timeout 1500 python -m pytest tests -m gpu -q -x -k "decode or batch or graph or append or window or parity" 2>&1 | tail -2
+timeout 600 python tools/batched_probe.py 2>&1 | tail -1
+SK_LAYERS=32 timeout 600 python tools/graph_probe.py 2>&1 | tail -1
