@@ -175,6 +175,35 @@ def test_prefill_8k_against_oracle_sampled_tiles():
     assert led.total(sk.PREFILL) == 264_192
 
 
+def test_prefill_256k_against_oracle_sampled_tiles():
+    """cfg3 geometry for one layer (32/8/128 at 256k, balanced heads): the
+    device prefill's sampled query tiles -- first, middle, last -- against the
+    oracle on the same inputs, and the visited-tile ledger."""
+    n = s = 262144
+    h, h_kv, d = 32, 8, 128
+    gates = [0.9 - 0.001 * i if i % 4 < 2 else 0.1 + 0.001 * i for i in range(h)]
+    cfg = sk.EngineConfig(quant_bits=4, local_blocks=4)
+    prof = sk.classify_heads(gates, 0.5, 1, 4)
+    g = torch.Generator(device="cuda").manual_seed(256)
+    q = torch.randn(n, h, d, device="cuda", dtype=torch.float16, generator=g)
+    k = torch.randn(s, h_kv, d, device="cuda", dtype=torch.float16, generator=g)
+    v = torch.randn(s, h_kv, d, device="cuda", dtype=torch.float16, generator=g)
+    eng = sk.Engine(cfg, prof, device="cuda:0", capacity_tokens=s)
+    out = eng.prefill_device(q, k, v, d)
+    roles = O.assign_roles(gates, 0.5, 1, 4)
+    n_tiles = s // 64
+    for qt in (0, 2049, n_tiles - 1):
+        r0, r1 = qt * 64, qt * 64 + 64
+        sched = {(hh, 0): list(range(qt + 1)) if roles[hh].role == O.RETRIEVAL else O.lambda_tiles(n_tiles, 1, 4, qt)
+                 for hh in range(h)}
+        qh, kh, vh = (t.float().cpu().numpy() for t in (q[r0:r1], k[:r1], v[:r1]))
+        ref, _ = O.tiled_attention(qh, kh, vh, sched, 64, 64)
+        assert_close_attn(out[r0:r1].float().cpu().numpy(), ref)
+    exp_vis = sum(qt + 1 if roles[hh].role == O.RETRIEVAL else len(O.lambda_tiles(n_tiles, 1, 4, qt))
+                  for hh in range(h) for qt in range(n_tiles))
+    assert eng.ledger.visited(sk.PREFILL) == exp_vis == 134_578_016  # DESIGN 9: cfg3 visited tiles
+
+
 def test_decode_long_context_selection_matches_oracle():
     """16k-token context, budget 1024, reuse 4: 12 decode steps; selections,
     index tables and outputs against the oracle driven on the same data."""

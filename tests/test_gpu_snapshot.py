@@ -5,6 +5,8 @@ counts) equal the originals, and a restored partial page refuses appends
 with the reference's error."""
 
 import io
+import os
+import sys
 
 import numpy as np
 import pytest
@@ -37,3 +39,37 @@ def test_snapshot_round_trip(bits):
     assert sorted(restored.streaming_pool) == sorted(eng.cache.streaming_pool)
     with pytest.raises(ValueError, match="partial page restored|restored from a snapshot"):
         restored.append_tokens(0, k[:1, 0], v[:1, 0])
+
+
+# ---- interop with snapshots the reference itself wrote (tests/golden/make_snapshot.py) ----------
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.mark.parametrize("bits,name", [(4, "snapshot_ref_kv4.jsonl"), (None, "snapshot_ref_fp16.jsonl")])
+def test_reference_snapshot_loads_and_dumps_back_identically(bits, name):
+    """A JSONL snapshot written by the reference (cache.py:333-345) loads into
+    the device pools and dumps back byte for byte."""
+    text = open(f"{GOLDEN}/{name}").read()
+    restored = sk.TwoWayCache.load_jsonl(io.StringIO(text), device="cuda:0")
+    buf = io.StringIO()
+    restored.dump_jsonl(buf)
+    assert buf.getvalue() == text
+
+
+@pytest.mark.parametrize("bits,name", [(4, "snapshot_ref_kv4.jsonl"), (None, "snapshot_ref_fp16.jsonl")])
+def test_same_appends_dump_what_the_reference_dumps(bits, name):
+    """The same appends (uneven chunks: an open partial page, streaming
+    evictions) through the device pools dump the reference's bytes."""
+    sys.path.insert(0, GOLDEN)
+    from snapshot_inputs import CHUNKS as chunks, inputs
+    k, v = inputs()
+    c = sk.TwoWayCache(64, 16, bits, dense_heads=[0, 2], streaming_heads=[1], sink_blocks=1, local_blocks=2,
+                       device="cuda:0", capacity_tokens=k.shape[0])
+    t = 0
+    for m in chunks:
+        for h in range(3):
+            c.append_tokens(h, k[t:t + m, h], v[t:t + m, h])
+        t += m
+    buf = io.StringIO()
+    c.dump_jsonl(buf)
+    assert buf.getvalue() == open(f"{GOLDEN}/{name}").read()
