@@ -247,6 +247,23 @@ int sk_prefill_attn(int32_t dtype, const void* q, const void* k, const void* v, 
                     const sk_prefill_item* items, int32_t n_items, const uint32_t* segs,
                     const uint64_t* row_masks, void* stream);
 
+/*
+ * K4 over the page pool (chunked prefill): the same attention
+ * as sk_prefill_attn on an (n_q, hist_tokens + n_q) plan, with keys
+ * [0, hist_tokens) read from the pool's KV4 pages through its page table
+ * (stream = KV head), dequantised by producer warps straight into the
+ * kernel's shared-memory K/V tiles -- code * scale + lo in fp32 rounded to
+ * the pool dtype, the values PhysicalPage.dequantize casts to the attention
+ * dtype (cache.py:97-102, engine.py:250-262) -- and keys [hist_tokens, +n_q)
+ * from the chunk's raw k_chunk / v_chunk [n_q][n_kv_heads][head_dim].  No
+ * history buffer is materialised.  q / out [n_q][n_heads][head_dim] in the
+ * pool dtype.  Pools with <= 4-bit codes and page size 32 or 64.
+ */
+int sk_prefill_attn_paged(const sk_pool* pool, int32_t n_kv_heads, int32_t hist_tokens, const void* q,
+                          const void* k_chunk, const void* v_chunk, void* out, int32_t n_q, int32_t n_heads,
+                          float softmax_scale, const sk_prefill_item* items, int32_t n_items,
+                          const uint32_t* segs, const uint64_t* row_masks, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,7 @@ LIB_PATH = os.environ.get("SK_LIB_PATH") or os.path.join(os.path.dirname(os.path
 EXPORTS = ("sk_version", "sk_last_error", "sk_device_supported", "sk_slot_bytes", "sk_append_pages",
            "sk_append_token_layers",
            "sk_gather_pages", "sk_select_workspace", "sk_select_scores_offset", "sk_select_pages", "sk_score_pages",
-           "sk_decode_workspace", "sk_decode_attn", "sk_prefill_attn")
+           "sk_decode_workspace", "sk_decode_attn", "sk_prefill_attn", "sk_prefill_attn_paged")
 
 
 class SkPool(C.Structure):
@@ -64,6 +64,9 @@ _SIGS = {
                                  C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_int32, C.c_void_p, C.c_float, C.c_void_p, C.c_int64, C.c_int64,
                                  C.c_int32, C.c_uint32, C.c_void_p, C.c_int64, C.c_void_p]),
+    "sk_prefill_attn_paged": (C.c_int, [C.POINTER(SkPool), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float, C.c_void_p,
+                                        C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sk_prefill_attn": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                   C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_void_p, C.c_int32,
                                   C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -339,6 +339,23 @@ def run_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: Prefill
     return out
 
 
+def run_prefill_paged(pool, hist: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: PrefillPlan,
+                      scale: float) -> torch.Tensor:
+    """K4 over a page pool (chunked prefill): keys [0, hist) from the pool's KV4
+    pages, [hist, hist + n) from the chunk's k/v [n, Hkv, Dp]; q [n, H, Dp]."""
+    lib = _lib.load()
+    n, h, dp = q.shape
+    out = torch.empty_like(q)
+    items, segs, masks = plan.device_arrays(q.device)
+    abi = pool.abi()
+    rc = lib.sk_prefill_attn_paged(C.byref(abi), k.shape[1], hist, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                   out.data_ptr(), n, h, C.c_float(scale), items.data_ptr(), plan.n_items,
+                                   segs.data_ptr(), masks.data_ptr() if masks is not None else None,
+                                   _device.stream_ptr(q.device))
+    _lib.check(rc)
+    return out
+
+
 def blockwise_attention(w: Workload, schedules: Mapping[tuple, Sequence[int]], tile_q: int, tile_k: int,
                         stage: str = "attention", *, dtype: torch.dtype | None = None, device=None):
     """attn.py:245-324 on the B200: causal attention over the scheduled KV

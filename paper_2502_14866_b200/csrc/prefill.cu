@@ -31,6 +31,7 @@
 #include <mutex>
 
 #include "sk_common.cuh"
+#include "sk_layout.cuh"
 #include "sk_sm100.cuh"
 
 namespace sk {
@@ -50,15 +51,23 @@ constexpr uint32_t kFlagCausal = 1u << 4, kFlagMasks = 1u << 5;
 #endif
 constexpr int kPolyFrom = SK_POLY_FROM;
 
-template <int D>
+// K/V stages when K/V are dequantised from the page pool (PAGED): one
+// fewer, the room holds the producer's page-bounds tables
+constexpr int kNSPaged = 4;
+
+template <int D, int NS = kNS, bool PAGED = false>
 struct PfSmem {
   static constexpr int NC = D / 64;  // 128-byte column chunks
   alignas(1024) uint8_t q[2][NC][128 * 128];
-  alignas(1024) uint8_t kv[kNS][2][NC][64 * 128];
+  alignas(1024) uint8_t kv[NS][2][NC][64 * 128];
   alignas(kTmemP ? 16 : 1024) uint8_t p[kTmemP ? 1 : 2][kTmemP ? 1 : 2][kTmemP ? 16 : 128 * 128];
+  alignas(16) uint8_t bnd[PAGED ? 4 : 1][PAGED ? 4 * D * 2 : 16];  // raw page bounds / (scale, lo) tables
+  // PAGED, 64-token pages: bulk-copied KV4 page slots, two blocks ahead of the dequantiser
+  alignas(128) uint8_t stage[PAGED ? 3 : 1][PAGED ? 64 * D + 8 * D : 16];
+  uint64_t stage_full[PAGED ? 3 : 1];
   uint64_t q_full;
-  uint64_t kv_full[kNS];
-  uint64_t kv_empty[kNS];
+  uint64_t kv_full[NS];
+  uint64_t kv_empty[NS];
   uint64_t s_full[2][2];
   uint64_t p_full[2][2];
   uint64_t p_empty[2][2];
@@ -73,6 +82,13 @@ struct PfParams {
   const sk_prefill_item* items;
   const uint32_t* segs;
   const uint64_t* row_masks;
+  // PAGED (chunked prefill over the page pool): keys [0, hist) are the pool's
+  // KV4 pages (stream = KV head), keys [hist, n_kv) the chunk's raw k / v
+  // [n_kv - hist][n_kv_heads][D]
+  PoolView pv;
+  int hist;
+  const void* kc;
+  const void* vc;
 };
 
 // Walks an item's segments block by block.
@@ -167,11 +183,339 @@ __device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t* r) {
       : "memory");
 }
 
-template <typename T, int D>
-__global__ void __launch_bounds__(kPfThreads, 1)
+// A 4-bit code as an exact float without I2F (a conversion would share the
+// XU pipe with the softmax's MUFU.EX2): 2^23 + n, less 2^23.
+__device__ __forceinline__ float nib_f(uint32_t w, int shift) {
+  return __uint_as_float(0x4B000000u | ((w >> shift) & 0xFu)) - 8388608.f;
+}
+
+// Producer warps 10-13 of the PAGED kernel: K/V block j of the item is built in
+// the stage's smem tiles in the layouts the MMAs read -- K row-major
+// [key][D] (SWIZZLE_128B, as TMA writes it), V K-major [D][64 keys] (its rows
+// are the pool's channel-major code runs) -- from the KV4 pages (dequantised:
+// code * scale + lo in fp32, rounded to T: the values PhysicalPage.dequantize
+// casts to the attention dtype, identical to K1b and K3) or from the chunk's
+// raw k / v; keys past n_kv are zero.  Thread i: K token i/2, dims
+// [(i%2) D/2, +D/2); V channel i % D, keys [(i/D) 64D/128, +64D/128).
+template <typename T, int D, int P, int NS>
+__device__ __forceinline__ void paged_block(PfSmem<D, NS, true>& sm, const PfParams& prm, int kvh, int st, int key0,
+                                            int tid) {
+  constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+  constexpr int UPT = D / 16;                // K units (8 dims) per thread
+  constexpr int VKEYS = D == 128 ? 64 : 32;  // V keys per thread
+  constexpr int PPB = 64 / P;                // pages per block
+  constexpr int BCH = 4 * D * 2 / 16;        // 16-byte chunks of one page's bounds
+  constexpr int RW = P / 8;                  // words of a channel's code run in a page (4 lanes x P/32)
+  const PoolView& pv = prm.pv;
+  const int hist = prm.hist;
+  const int page0 = key0 / P;
+  // ---- issue every load first: bounds -> smem, K codes / raw row and the
+  //      channel's V code runs -> registers
+  for (int x = tid; x < PPB * BCH; x += 128) {
+    const int pg = x / BCH;
+    if ((page0 + pg) * P < hist) {
+      const uint8_t* bsrc = pv.bounds(pv.slot_ptr(kvh, page0 + pg));
+      *reinterpret_cast<uint4*>(&sm.bnd[pg][(x % BCH) * 16]) = *reinterpret_cast<const uint4*>(bsrc + (x % BCH) * 16);
+    }
+  }
+  const int t = tid >> 1, hd = tid & 1, kpos = key0 + t;
+  uint32_t kwv[4][UPT / 4];
+  uint4 kraw[UPT];
+  if (kpos < hist) {
+    const uint8_t* kc = pv.slot_ptr(kvh, kpos / P) + (kpos % P) * (D / 2);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int w = 0; w < UPT / 4; ++w)
+        kwv[j][w] = *reinterpret_cast<const uint32_t*>(kc + j * (D / 8) + (hd * (UPT / 4) + w) * 4);
+  } else if (kpos < prm.n_kv) {
+    const T* src = reinterpret_cast<const T*>(prm.kc) + ((int64_t)(kpos - hist) * prm.n_kv_heads + kvh) * D + hd * (D / 2);
+#pragma unroll
+    for (int u = 0; u < UPT; ++u) kraw[u] = *reinterpret_cast<const uint4*>(src + 8 * u);
+  }
+  const int c = tid % D, kh = tid / D, kb0 = key0 + kh * VKEYS;
+  uint32_t vrun[PPB][RW];
+#pragma unroll
+  for (int pg = 0; pg < PPB; ++pg) {
+    if ((page0 + pg) * P < hist) {
+      const uint8_t* run = pv.v_codes(pv.slot_ptr(kvh, page0 + pg)) + (32 * (c / 8) + 4 * (c % 8)) * (P / 8);
+#pragma unroll
+      for (int q = 0; q < RW / 4; ++q) {
+        const uint4 v4 = *reinterpret_cast<const uint4*>(run + 16 * q);
+        vrun[pg][4 * q] = v4.x; vrun[pg][4 * q + 1] = v4.y; vrun[pg][4 * q + 2] = v4.z; vrun[pg][4 * q + 3] = v4.w;
+      }
+    }
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");  // bounds staged
+  // ---- K: dequantise (or copy) the thread's 8-dim units into the swizzled row
+  uint8_t* kt = &sm.kv[st][0][0][0];
+  const int kpg = kpos / P - page0;
+#pragma unroll
+  for (int u = 0; u < UPT; ++u) {
+    const int m = hd * UPT + u;  // 8-dim unit of the row
+    uint4 outv = make_uint4(0u, 0u, 0u, 0u);
+    if (kpos < hist) {
+      const T* bt = reinterpret_cast<const T*>(&sm.bnd[kpg][0]);
+      uint32_t pk[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t wd = kwv[j][u / 4];
+        const int bp = j * (D / 4) + 2 * m;  // kbound_pos of dims 8m+2j, 8m+2j+1
+        float x2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float lo = DT<T>::to_f(bt[bp + e]), hi = DT<T>::to_f(bt[D + bp + e]);
+          float sc = (hi - lo) / 15.f;
+          sc = sc > 0.f ? sc : 1.f;
+          x2[e] = fmaf(nib_f(wd, 4 * (m % 4) + 16 * e), sc, lo);
+        }
+        pk[j] = kBF16 ? pack_bf162(x2[0], x2[1]) : pack_half2(x2[0], x2[1]);
+      }
+      outv = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    } else if (kpos < prm.n_kv) {
+      outv = kraw[u];
+    }
+    const int d0 = 8 * m, chk = d0 / 64, un = (d0 % 64) / 8;
+    *reinterpret_cast<uint4*>(kt + chk * (64 * 128) + t * 128 + ((un ^ (t & 7)) << 4)) = outv;
+  }
+  // ---- V: the channel's keys, K-major row c (64 keys x 2 B, swizzled 16 B units)
+  uint8_t* vr = &sm.kv[st][1][0][0] + c * 128;
+  const int vbp = ((c % 8) / 2) * (D / 4) + (c / 8) * 2 + (c % 2);  // vbound_pos(c)
+#pragma unroll
+  for (int q8 = 0; q8 < VKEYS / 8; ++q8) {
+    uint32_t pk[4];
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      float x2[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int key = kb0 + 8 * q8 + 2 * e2 + e;
+        float val = 0.f;
+        if (key < hist) {
+          const int pg = key / P - page0, tin = key % P;
+          const T* bt = reinterpret_cast<const T*>(&sm.bnd[pg][0]);
+          const float lo = DT<T>::to_f(bt[2 * D + vbp]), hi = DT<T>::to_f(bt[3 * D + vbp]);
+          float sc = (hi - lo) / 15.f;
+          sc = sc > 0.f ? sc : 1.f;
+          const uint32_t wd = vrun[pg][((tin % 8) / 2) * (P / 32) + tin / 32];
+          val = fmaf(nib_f(wd, 4 * ((tin / 8) % 4) + 16 * (tin % 2)), sc, lo);
+        } else if (key < prm.n_kv) {
+          val = DT<T>::to_f(reinterpret_cast<const T*>(prm.vc)[((int64_t)(key - hist) * prm.n_kv_heads + kvh) * D + c]);
+        }
+        x2[e] = val;
+      }
+      pk[e2] = kBF16 ? pack_bf162(x2[0], x2[1]) : pack_half2(x2[0], x2[1]);
+    }
+    const int un = (kh * VKEYS) / 8 + q8;
+    *reinterpret_cast<uint4*>(vr + ((un ^ (c & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+  fence_proxy_async_smem();  // generic-proxy smem writes -> the tensor core's async proxy
+  asm volatile("bar.sync 1, 128;" ::: "memory");  // every thread's tile writes (and bounds reads) done
+}
+
+// Fast path of the paged producer for blocks lying wholly in the history:
+// the loads of block j+1 (bound values of this thread's dim / channel, K codes,
+// V code runs) are issued before block j is dequantised; per-page (scale, lo)
+// tables in smem are formed once per block (one fp32 division per dim, the
+// formula of K1b), so a code costs an extract, a conversion and an FMA.
+template <typename T, int D, int P>
+struct PagedRegs {
+  static constexpr int UPT = D / 16, RW = P / 8, PPB = 64 / P;
+  uint32_t kw[4][UPT / 4];   // K codes of the thread's token, its dim half
+  uint32_t vrun[PPB][RW];    // V code runs of the thread's channel
+  uint32_t kb[PPB][2];       // K lo / hi (raw T bits) of dim tid (D = 128) or tid % D
+  uint32_t vb[PPB][2];       // V lo / hi of channel tid % D
+};
+template <typename T, int D, int P>
+__device__ __forceinline__ void paged_prefetch(const PfParams& prm, int kvh, int key0, int tid, PagedRegs<T, D, P>& r) {
+  using R = PagedRegs<T, D, P>;
+  const PoolView& pv = prm.pv;
+  const int page0 = key0 / P;
+  const int t = tid >> 1, hd = tid & 1, kpos = key0 + t;
+  const uint8_t* kc = pv.slot_ptr(kvh, kpos / P) + (kpos % P) * (D / 2);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int w = 0; w < R::UPT / 4; ++w)
+      r.kw[j][w] = __ldg(reinterpret_cast<const uint32_t*>(kc + j * (D / 8) + (hd * (R::UPT / 4) + w) * 4));
+  const int c = tid % D;
+  const int kbp = kbound_pos(c, D), vbp = vbound_pos(c, D);
+#pragma unroll
+  for (int pg = 0; pg < R::PPB; ++pg) {
+    const uint8_t* slot = pv.slot_ptr(kvh, page0 + pg);
+    const uint8_t* run = pv.v_codes(const_cast<uint8_t*>(slot)) + (32 * (c / 8) + 4 * (c % 8)) * (P / 8);
+#pragma unroll
+    for (int q = 0; q < R::RW / 4; ++q) {
+      const uint4 v4 = __ldg(reinterpret_cast<const uint4*>(run + 16 * q));
+      r.vrun[pg][4 * q] = v4.x; r.vrun[pg][4 * q + 1] = v4.y; r.vrun[pg][4 * q + 2] = v4.z; r.vrun[pg][4 * q + 3] = v4.w;
+    }
+    const uint16_t* b = reinterpret_cast<const uint16_t*>(pv.bounds(const_cast<uint8_t*>(slot)));
+    r.kb[pg][0] = __ldg(b + kbp);
+    r.kb[pg][1] = __ldg(b + D + kbp);
+    r.vb[pg][0] = __ldg(b + 2 * D + vbp);
+    r.vb[pg][1] = __ldg(b + 3 * D + vbp);
+  }
+}
+template <typename T>
+__device__ __forceinline__ float2 scale_lo(uint32_t lo_bits, uint32_t hi_bits) {  // K1b's (scale, lo)
+  const uint16_t l16 = (uint16_t)lo_bits, h16 = (uint16_t)hi_bits;
+  const float lo = DT<T>::to_f(*reinterpret_cast<const T*>(&l16)), hi = DT<T>::to_f(*reinterpret_cast<const T*>(&h16));
+  const float sc = (hi - lo) / 15.f;
+  return make_float2(sc > 0.f ? sc : 1.f, lo);
+}
+template <typename T, int D, int P, int NS>
+__device__ __forceinline__ void paged_fast(PfSmem<D, NS, true>& sm, int st, int tid, const PagedRegs<T, D, P>& r,
+                                           const float2* ktab /* [PPB][D] (scale, lo) */) {
+  using R = PagedRegs<T, D, P>;
+  constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+  constexpr int VKEYS = D == 128 ? 64 : 32;
+  const int t = tid >> 1, hd = tid & 1;
+  const int kpg = t / P;
+  uint8_t* kt = &sm.kv[st][0][0][0];
+#pragma unroll
+  for (int u = 0; u < R::UPT; ++u) {
+    const int m = hd * R::UPT + u;
+    uint32_t pk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t wd = r.kw[j][u / 4];
+      const float4 sl = *reinterpret_cast<const float4*>(&ktab[kpg * D + 8 * m + 2 * j]);  // dims 8m+2j, +1
+      const float x0 = fmaf(nib_f(wd, 4 * (u % 4)), sl.x, sl.y);  // m % 4 == u % 4
+      const float x1 = fmaf(nib_f(wd, 4 * (u % 4) + 16), sl.z, sl.w);
+      pk[j] = kBF16 ? pack_bf162(x0, x1) : pack_half2(x0, x1);
+    }
+    const int d0 = 8 * m, chk = d0 / 64, un = (d0 % 64) / 8;
+    *reinterpret_cast<uint4*>(kt + chk * (64 * 128) + t * 128 + ((un ^ (t & 7)) << 4)) =
+        make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+  const int c = tid % D, kh = tid / D;
+  uint8_t* vr = &sm.kv[st][1][0][0] + c * 128;
+  float2 vsl[R::PPB];
+#pragma unroll
+  for (int pg = 0; pg < R::PPB; ++pg) vsl[pg] = scale_lo<T>(r.vb[pg][0], r.vb[pg][1]);
+#pragma unroll
+  for (int q8 = 0; q8 < VKEYS / 8; ++q8) {
+    uint32_t pk[4];
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      float x2[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int kr = 8 * q8 + 2 * e2 + e;  // key within the thread's VKEYS (compile-time)
+        // D = 128: kh == 0 and every index below is a compile-time register index;
+        // D = 64: kh selects the page (P = 32) or the word (P = 64)
+        const int kb = (D == 128 ? 0 : VKEYS) + kr;
+        const int pg1 = kb / P, tin1 = kb % P, pg0 = kr / P, tin0 = kr % P;
+        const uint32_t w0 = r.vrun[pg0][((tin0 % 8) / 2) * (P / 32) + tin0 / 32];
+        const uint32_t w1 = r.vrun[pg1][((tin1 % 8) / 2) * (P / 32) + tin1 / 32];
+        const bool hi = D != 128 && kh == 1;
+        const uint32_t wd = hi ? w1 : w0;
+        const int tin = hi ? tin1 : tin0;
+        const float2 sl = hi ? vsl[pg1] : vsl[pg0];
+        x2[e] = fmaf(nib_f(wd, 4 * ((tin / 8) % 4) + 16 * (tin % 2)), sl.x, sl.y);
+      }
+      pk[e2] = kBF16 ? pack_bf162(x2[0], x2[1]) : pack_half2(x2[0], x2[1]);
+    }
+    const int un = (kh * VKEYS) / 8 + q8;
+    *reinterpret_cast<uint4*>(vr + ((un ^ (c & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+}
+
+// Fast path for 64-token pages: the block's page slot (codes + bounds, one
+// contiguous 64 D + 8 D bytes) arrives by one 1-D bulk copy issued two blocks
+// ahead; the dequantiser reads everything from shared memory.
+template <typename T, int D, int NS>
+__device__ __forceinline__ void paged_staged(PfSmem<D, NS, true>& sm, int st, int tid, const uint8_t* slot,
+                                             float2* ktab) {
+  constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+  constexpr int P = 64, UPT = D / 16, VKEYS = D == 128 ? 64 : 32;
+  const uint16_t* b = reinterpret_cast<const uint16_t*>(slot + 2 * P * (D / 2));
+  if (tid < D) ktab[tid] = scale_lo<T>(b[kbound_pos(tid, D)], b[D + kbound_pos(tid, D)]);
+  const int c = tid % D, kh = tid / D;
+  const float2 vsl = scale_lo<T>(b[2 * D + vbound_pos(c, D)], b[3 * D + vbound_pos(c, D)]);
+  const int t = tid >> 1, hd = tid & 1;
+  uint32_t kw[4][UPT / 4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int w = 0; w < UPT / 4; ++w)
+      kw[j][w] = *reinterpret_cast<const uint32_t*>(slot + t * (D / 2) + j * (D / 8) + (hd * (UPT / 4) + w) * 4);
+  uint32_t vrun[8];
+  {
+    const uint8_t* run = slot + P * (D / 2) + (32 * (c / 8) + 4 * (c % 8)) * (P / 8);
+    const uint4 a = *reinterpret_cast<const uint4*>(run), bb = *reinterpret_cast<const uint4*>(run + 16);
+    vrun[0] = a.x; vrun[1] = a.y; vrun[2] = a.z; vrun[3] = a.w; vrun[4] = bb.x; vrun[5] = bb.y; vrun[6] = bb.z; vrun[7] = bb.w;
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");  // K (scale, lo) table complete
+  uint8_t* kt = &sm.kv[st][0][0][0];
+#pragma unroll
+  for (int u = 0; u < UPT; ++u) {
+    const int m = hd * UPT + u;
+    uint32_t pk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t wd = kw[j][u / 4];
+      const float4 sl = *reinterpret_cast<const float4*>(&ktab[8 * m + 2 * j]);  // dims 8m+2j, +1
+      const float x0 = fmaf(nib_f(wd, 4 * (u % 4)), sl.x, sl.y);  // m % 4 == u % 4
+      const float x1 = fmaf(nib_f(wd, 4 * (u % 4) + 16), sl.z, sl.w);
+      pk[j] = kBF16 ? pack_bf162(x0, x1) : pack_half2(x0, x1);
+    }
+    const int d0 = 8 * m, chk = d0 / 64, un = (d0 % 64) / 8;
+    *reinterpret_cast<uint4*>(kt + chk * (64 * 128) + t * 128 + ((un ^ (t & 7)) << 4)) =
+        make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+  uint8_t* vr = &sm.kv[st][1][0][0] + c * 128;
+#pragma unroll
+  for (int q8 = 0; q8 < VKEYS / 8; ++q8) {
+    uint32_t pk[4];
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      float x2[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        // key tin = kh*VKEYS + tr of the page: word ((tin%8)/2)*2 + tin/32 -- a register index
+        // fixed at compile time (kh only picks between two words when D = 64)
+        const int tr = 8 * q8 + 2 * e2 + e;
+        const int wi = ((tr % 8) / 2) * 2 + (D == 128 ? tr / 32 : 0);
+        const uint32_t wd = (D == 128 || kh == 0) ? vrun[wi] : vrun[wi + 1];
+        x2[e] = fmaf(nib_f(wd, 4 * ((tr / 8) % 4) + 16 * (tr % 2)), vsl.x, vsl.y);
+      }
+      pk[e2] = kBF16 ? pack_bf162(x2[0], x2[1]) : pack_half2(x2[0], x2[1]);
+    }
+    const int un = (kh * VKEYS) / 8 + q8;
+    *reinterpret_cast<uint4*>(vr + ((un ^ (c & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+}
+
+// A block wholly inside the chunk: its raw K and V rows, copied 16 bytes at a
+// time into the same row-major SWIZZLE_128B tiles TMA would write (the MMA
+// reads this block's V as MN-major); keys past n_kv are zero.
+template <typename T, int D, int NS>
+__device__ __forceinline__ void chunk_rows(PfSmem<D, NS, true>& sm, const PfParams& prm, int kvh, int st, int key0,
+                                           int tid) {
+  constexpr int UPR = D / 8;  // 16-byte units per row
+  for (int x = tid; x < 2 * 64 * UPR; x += 128) {
+    const int which = x / (64 * UPR), t = (x / UPR) % 64, u = x % UPR;
+    const int key = key0 + t;
+    uint4 val = make_uint4(0u, 0u, 0u, 0u);
+    if (key < prm.n_kv) {
+      const T* src = reinterpret_cast<const T*>(which ? prm.vc : prm.kc) +
+                     ((int64_t)(key - prm.hist) * prm.n_kv_heads + kvh) * D + 8 * u;
+      val = *reinterpret_cast<const uint4*>(src);
+    }
+    const int chk = u / 8, un = u % 8;
+    *reinterpret_cast<uint4*>(&sm.kv[st][which][chk][0] + t * 128 + ((un ^ (t & 7)) << 4)) = val;
+  }
+  fence_proxy_async_smem();
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+template <typename T, int D, bool PAGED = false, int PP = 64>
+__global__ void __launch_bounds__(PAGED ? kPfThreads + 128 : kPfThreads, 1)
     prefill_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-                   const __grid_constant__ CUtensorMap tv, const PfParams prm) {
-  using Sm = PfSmem<D>;
+                   const __grid_constant__ CUtensorMap tv, const __grid_constant__ PfParams prm) {
+  constexpr int NS = PAGED ? kNSPaged : kNS;
+  using Sm = PfSmem<D, NS, PAGED>;
   constexpr int NC = Sm::NC;
   constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
   constexpr uint32_t kTmemCols = 512;
@@ -187,7 +531,9 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&sm.q_full, 1);
-    for (int i = 0; i < kNS; ++i) {
+    if (PAGED)
+      for (int i = 0; i < 3; ++i) mbar_init(&sm.stage_full[i], 1);
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&sm.kv_full[i], 1);
       mbar_init(&sm.kv_empty[i], 1);
     }
@@ -217,9 +563,9 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       for (int t = 0; t < 2; ++t)
         for (int c = 0; c < NC; ++c) tma_load_3d(sm.q[t][c], &tq, &sm.q_full, 64 * c, item.head, item.row0 + 128 * t);
       int j = 0;
-      for (SegWalk w(prm.segs, item.seg_begin, item.seg_count); !w.done(); w.next(), ++j) {
-        const int st = j % kNS;
-        if (j >= kNS) mbar_wait(&sm.kv_empty[st], ((j / kNS) - 1) & 1);
+      for (SegWalk w(prm.segs, item.seg_begin, item.seg_count); !PAGED && !w.done(); w.next(), ++j) {
+        const int st = j % NS;
+        if (j >= NS) mbar_wait(&sm.kv_empty[st], ((j / NS) - 1) & 1);
         mbar_arrive_expect_tx(&sm.kv_full[st], 2 * NC * 64 * 128);
         const int key0 = w.block() * 64;
         for (int c = 0; c < NC; ++c) {
@@ -232,11 +578,15 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   } else if (warp == 1) {
     // ------------------------------ MMA issuer --------------------------------
     constexpr uint32_t idesc_s = make_idesc_f16(128, 64, kBF16, false, false);
-    constexpr uint32_t idesc_o = make_idesc_f16(128, D, kBF16, false, true);
+    constexpr uint32_t idesc_o = make_idesc_f16(128, D, kBF16, false, true);     // V MN-major (TMA)
+    constexpr uint32_t idesc_o_km = make_idesc_f16(128, D, kBF16, false, false); // V K-major (paged producer)
+    // PAGED: which stage holds a K-major V (a block built by the producer warps)
+    uint32_t kmaj = 0;  // bit st: stage st holds a K-major V
+    SegWalk mw(prm.segs, item.seg_begin, item.seg_count);
     mbar_wait(&sm.q_full, 0);
     tc_fence_after();
     auto issue_s = [&](int t, int jj) {  // S_t,jj = Q_t K_jj^T into TMEM buffer jj&1
-      const int st = jj % kNS;
+      const int st = jj % NS;
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -249,15 +599,18 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       __syncwarp();
     };
     auto issue_pv = [&](int t, int jj) {  // O_t += P_t,jj V_jj
-      const int st = jj % kNS;
+      const int st = jj % NS;
       mbar_wait(&sm.p_full[t][jj & 1], (jj >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          uint64_t b = make_sdesc_sw128(smem_u32(sm.kv[st][1][0]) + kk * 2048, 64 * 128, 1024);
+          // V: MN-major [key][D] as TMA writes it, or K-major [D][key] from the paged producer
+          const bool km = PAGED && ((kmaj >> st) & 1u);
+          uint64_t b = km ? make_sdesc_sw128(smem_u32(sm.kv[st][1][0]) + kk * 32, 16, 1024)
+                          : make_sdesc_sw128(smem_u32(sm.kv[st][1][0]) + kk * 2048, 64 * 128, 1024);
           if (kTmemP) {
-            mma_f16_ts(tmem + kOCol + t * 128, tmem + t * 128 + (jj & 1) * 64 + kk * 8, b, idesc_o,
+            mma_f16_ts(tmem + kOCol + t * 128, tmem + t * 128 + (jj & 1) * 64 + kk * 8, b, km ? idesc_o_km : idesc_o,
                        (jj > 0 || kk > 0) ? 1u : 0u);
           } else {
             uint64_t a = make_sdesc_sw128(smem_u32(sm.p[kTmemP ? 0 : t][jj & 1]) + kk * 32, 16, 1024);
@@ -270,8 +623,13 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       }
       __syncwarp();
     };
-    auto wait_kv = [&](int jj) {
-      mbar_wait(&sm.kv_full[jj % kNS], (jj / kNS) & 1);
+    auto wait_kv = [&](int jj) {  // blocks are waited in order: record block jj's V layout for its PV
+      if (PAGED) {
+        const uint32_t bit = 1u << (jj % NS);
+        kmaj = (mw.block() * 64 < prm.hist) ? (kmaj | bit) : (kmaj & ~bit);
+        mw.next();
+      }
+      mbar_wait(&sm.kv_full[jj % NS], (jj / NS) & 1);
       tc_fence_after();
     };
     // S_t,j reuses the TMEM buffer of S_t,j-2, whose softmax finished before
@@ -308,6 +666,101 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         issue_pv(0, j);
         if (more) issue_s(1, j + 1);
         issue_pv(1, j);
+      }
+    }
+  } else if (PAGED && warp >= 10) {
+    // ------------------------- paged K/V producer (PAGED) -------------------------
+    if constexpr (PAGED && PP == 64) {
+      // 64-token pages: page j's slot is bulk-copied two blocks ahead (one
+      // thread issues, page-table entry loaded one block before that)
+      const int tid = threadIdx.x - 320;
+      float2* ktab = reinterpret_cast<float2*>(&sm.bnd[0][0]);  // [2][D] (scale, lo) of K
+      const uint32_t slot_bytes = 64 * D + 8 * D;
+      auto whole = [&](int block) { return (block + 1) * 64 <= prm.hist; };
+      SegWalk w(prm.segs, item.seg_begin, item.seg_count);
+      SegWalk wi = w;  // issue cursor, two blocks ahead
+      const uint8_t* nxt_slot = nullptr;
+      auto issue = [&](int jj) {  // bulk copy of block jj (cursor wi) if it is a history block
+        if (!wi.done() && whole(wi.block())) {
+          mbar_arrive_expect_tx(&sm.stage_full[jj % 3], slot_bytes);
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           smem_u32(sm.stage[jj % 3])),
+                       "l"(prm.pv.slot_ptr(kvh, wi.block())), "r"(slot_bytes), "r"(smem_u32(&sm.stage_full[jj % 3]))
+                       : "memory");
+        }
+        if (!wi.done()) wi.next();
+      };
+      if (tid == 0) {
+        issue(0);
+        issue(1);
+      }
+      for (int j = 0; !w.done(); ++j) {
+        const int st = j % NS, block = w.block();
+        if (tid == 0) issue(j + 2);  // the slot j + 2 - 3 = j - 1 was released by block j-1's last barrier
+        if (j >= NS) mbar_wait(&sm.kv_empty[st], ((j / NS) - 1) & 1);
+        if (block * 64 >= prm.hist) {  // wholly in the chunk: raw rows, row-major K and V
+          chunk_rows<T, D, NS>(sm, prm, kvh, st, block * 64, tid);
+          if (tid == 0) mbar_arrive(&sm.kv_full[st]);
+          w.next();
+          continue;
+        }
+#ifndef SK_PAGED_NOOP  // timing experiment only: 1 = the producer writes nothing
+#define SK_PAGED_NOOP 0
+#endif
+        if (SK_PAGED_NOOP) {
+          if (whole(block)) mbar_wait(&sm.stage_full[j % 3], (j / 3) & 1);
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        } else if (whole(block)) {
+          mbar_wait(&sm.stage_full[j % 3], (j / 3) & 1);
+          paged_staged<T, D, NS>(sm, st, tid, sm.stage[j % 3], ktab + (j & 1) * D);
+          fence_proxy_async_smem();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        } else {
+          paged_block<T, D, PP, NS>(sm, prm, kvh, st, block * 64, tid);
+        }
+        if (tid == 0) mbar_arrive(&sm.kv_full[st]);
+        w.next();
+      }
+      (void)nxt_slot;
+    } else if constexpr (PAGED) {
+      const int tid = threadIdx.x - 320;
+      float2* ktab = reinterpret_cast<float2*>(&sm.bnd[0][0]);  // [2 buffers][PPB][D] (scale, lo) of K
+      constexpr int PPB = 64 / PP;
+      PagedRegs<T, D, PP> cur, nxt;
+      SegWalk w(prm.segs, item.seg_begin, item.seg_count);
+      auto whole = [&](int block) { return (block + 1) * 64 <= prm.hist; };
+      if (!w.done() && whole(w.block())) paged_prefetch<T, D, PP>(prm, kvh, w.block() * 64, tid, cur);
+      for (int j = 0; !w.done(); ++j) {
+        const int st = j % NS, block = w.block();
+        SegWalk wn = w;
+        wn.next();
+        if (block * 64 >= prm.hist) {  // wholly in the chunk: raw rows, row-major K and V
+          if (j >= NS) mbar_wait(&sm.kv_empty[st], ((j / NS) - 1) & 1);
+          chunk_rows<T, D, NS>(sm, prm, kvh, st, block * 64, tid);
+          if (tid == 0) mbar_arrive(&sm.kv_full[st]);
+          w = wn;
+          continue;
+        }
+        if (whole(block)) {
+          // K (scale, lo) of this block's page(s) -> table j&1 (dim tid % D)
+          if (tid < D)
+#pragma unroll
+            for (int pg = 0; pg < PPB; ++pg)
+              ktab[((j & 1) * PPB + pg) * D + tid] = scale_lo<T>(cur.kb[pg][0], cur.kb[pg][1]);
+        }
+        if (!wn.done() && whole(wn.block())) paged_prefetch<T, D, PP>(prm, kvh, wn.block() * 64, tid, nxt);
+        if (j >= NS) mbar_wait(&sm.kv_empty[st], ((j / NS) - 1) & 1);
+        if (whole(block)) {
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // table j&1 complete
+          paged_fast<T, D, PP, NS>(sm, st, tid, cur, ktab + (j & 1) * PPB * D);
+          fence_proxy_async_smem();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        } else {
+          paged_block<T, D, PP, NS>(sm, prm, kvh, st, block * 64, tid);
+        }
+        if (tid == 0) mbar_arrive(&sm.kv_full[st]);
+        cur = nxt;
+        w = wn;
       }
     }
   } else {
@@ -502,13 +955,13 @@ int make_map(CUtensorMap* m, const void* base, int dtype, int D, int heads, int 
   return SK_OK;
 }
 
-template <typename T, int D>
+template <typename T, int D, bool PAGED = false, int PP = 64>
 int launch_prefill(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const PfParams& prm,
                    int n_items, cudaStream_t st) {
-  size_t smem = sizeof(PfSmem<D>) + 1024;
-  auto kern = prefill_kernel<T, D>;
+  size_t smem = sizeof(PfSmem<D, PAGED ? kNSPaged : kNS, PAGED>) + 1024;
+  auto kern = prefill_kernel<T, D, PAGED, PP>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<n_items, kPfThreads, smem, st>>>(tq, tk, tv, prm);
+  kern<<<n_items, PAGED ? kPfThreads + 128 : kPfThreads, smem, st>>>(tq, tk, tv, prm);
   SK_CHECK_LAUNCH("prefill_kernel");
   return SK_OK;
 }
@@ -536,7 +989,7 @@ extern "C" int sk_prefill_attn(int32_t dtype, const void* q, const void* k, cons
   if ((rc = make_map(&tq, q, dtype, head_dim, n_heads, n_q, 128))) return rc;
   if ((rc = make_map(&tk, k, dtype, head_dim, n_kv_heads, n_kv, 64))) return rc;
   if ((rc = make_map(&tv, v, dtype, head_dim, n_kv_heads, n_kv, 64))) return rc;
-  PfParams prm;
+  PfParams prm = {};
   prm.out = out;
   prm.n_q = n_q;
   prm.n_kv = n_kv;
@@ -553,4 +1006,57 @@ extern "C" int sk_prefill_attn(int32_t dtype, const void* q, const void* k, cons
                            : launch_prefill<__half, 64>(tq, tk, tv, prm, n_items, st);
   return head_dim == 128 ? launch_prefill<__nv_bfloat16, 128>(tq, tk, tv, prm, n_items, st)
                          : launch_prefill<__nv_bfloat16, 64>(tq, tk, tv, prm, n_items, st);
+}
+
+extern "C" int sk_prefill_attn_paged(const sk_pool* pool, int32_t n_kv_heads, int32_t hist_tokens, const void* q,
+                                     const void* k_chunk, const void* v_chunk, void* out, int32_t n_q,
+                                     int32_t n_heads, float softmax_scale, const sk_prefill_item* items,
+                                     int32_t n_items, const uint32_t* segs, const uint64_t* row_masks,
+                                     void* stream) {
+  using namespace sk;
+  int rc = check_pool(pool);
+  if (rc) return rc;
+  SK_CHECK_ARG(pool->bits >= 1 && pool->bits <= 4, "prefill paged: the pool must hold <= 4-bit codes (KV4)");
+  SK_CHECK_ARG(pool->page_size == 32 || pool->page_size == 64, "prefill paged: page size must be 32 or 64");
+  SK_CHECK_ARG(hist_tokens >= 1 && n_q >= 1, "prefill paged: empty history or chunk");
+  SK_CHECK_ARG((int64_t)(hist_tokens + pool->page_size - 1) / pool->page_size <= pool->max_pages,
+               "prefill paged: more history than the pool holds");
+  SK_CHECK_ARG(n_heads >= 1 && n_kv_heads >= 1 && n_heads % n_kv_heads == 0,
+               "prefill paged: query head count is not a multiple of KV head count");
+  SK_CHECK_ARG(q && k_chunk && v_chunk && out && items && segs, "prefill paged: NULL pointer");
+  SK_CHECK_ARG((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k_chunk) |
+                reinterpret_cast<uintptr_t>(v_chunk) | reinterpret_cast<uintptr_t>(pool->arena)) % 16 == 0,
+               "prefill paged: q/k/v/arena must be 16-byte aligned");
+  if (n_items == 0) return SK_OK;
+  const int D = pool->head_dim, dtype = pool->dtype;
+  CUtensorMap tq, tk, tv;  // K/V maps are not read by the paged kernel (the producer warps are)
+  if ((rc = make_map(&tq, q, dtype, D, n_heads, n_q, 128))) return rc;
+  if ((rc = make_map(&tk, k_chunk, dtype, D, n_kv_heads, n_q, 64))) return rc;
+  if ((rc = make_map(&tv, v_chunk, dtype, D, n_kv_heads, n_q, 64))) return rc;
+  PfParams prm = {};
+  prm.out = out;
+  prm.n_q = n_q;
+  prm.n_kv = hist_tokens + n_q;
+  prm.n_heads = n_heads;
+  prm.n_kv_heads = n_kv_heads;
+  prm.group = n_heads / n_kv_heads;
+  prm.scale_log2 = softmax_scale * 1.4426950408889634f;
+  prm.items = items;
+  prm.segs = segs;
+  prm.row_masks = row_masks;
+  prm.pv = make_view(*pool);
+  prm.hist = hist_tokens;
+  prm.kc = k_chunk;
+  prm.vc = v_chunk;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+#define SK_PG(TT, DD)                                                                             \
+  return pool->page_size == 64 ? launch_prefill<TT, DD, true, 64>(tq, tk, tv, prm, n_items, st) \
+                               : launch_prefill<TT, DD, true, 32>(tq, tk, tv, prm, n_items, st)
+  if (dtype == SK_F16) {
+    if (D == 128) SK_PG(__half, 128);
+    SK_PG(__half, 64);
+  }
+  if (D == 128) SK_PG(__nv_bfloat16, 128);
+  SK_PG(__nv_bfloat16, 64);
+#undef SK_PG
 }

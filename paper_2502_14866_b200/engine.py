@@ -30,8 +30,8 @@ import numpy as np
 import torch
 
 from . import _device, _lib
-from .attn import Workload, check_finite_device, diagonal_tile, kv_tile_count, plan_from_segments, plan_generic, query_tile_count, \
-    run_prefill
+from .attn import (Workload, check_finite_device, diagonal_tile, kv_tile_count, plan_from_segments, plan_generic,
+                   query_tile_count, run_prefill, run_prefill_paged)
 from .cache import TwoWayCache
 from .heads import RETRIEVAL, HeadProfile, lambda_segments
 from .ledger import CostLedger
@@ -352,14 +352,18 @@ class Engine:
                                  f"streaming pool's ({cfg.sink_blocks}, {cfg.local_blocks}); evicted pages "
                                  "cannot be attended")
         s0 = self.cache.num_tokens
-        kh, vh = pool.gather(extra_tokens=n)
-        kh[s0:] = k
-        vh[s0:] = v
         plan = self._plan(n, s0 + n)
-        out = run_prefill(q, kh, vh, plan, 1.0 / math.sqrt(head_dim))
+        if 1 <= pool.bits <= 4 and pool.P in (32, 64):
+            # K4 reads the KV4 history through the page table (no history buffer)
+            out = run_prefill_paged(pool, s0, q, k.contiguous(), v.contiguous(), plan, 1.0 / math.sqrt(head_dim))
+        else:  # KV8 / raw pages: K1b expands the history once, K4 streams it with TMA
+            kh, vh = pool.gather(extra_tokens=n)
+            kh[s0:] = k
+            vh[s0:] = v
+            out = run_prefill(q, kh, vh, plan, 1.0 / math.sqrt(head_dim))
+            del kh, vh
         for hh in range(h):
             self.ledger.record_tiles(PREFILL, hh, int(plan.visited[hh]), int(plan.total[hh]))
-        del kh, vh
         self.cache.append_all(k, v)
         return out
 

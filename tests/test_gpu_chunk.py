@@ -104,3 +104,33 @@ def test_chunked_prefill_32k_matches_one_shot():
                                                 one.float().transpose(0, 1).reshape(h, -1), dim=1).min().item()
     assert err <= 2e-2 and cos >= 0.9999, (err, cos)
     assert eng.cache.num_tokens == s
+
+
+@pytest.mark.parametrize("page,hist,chunk,dtype", [(64, 4096 + 17, 333, torch.float16), (32, 2048 + 40, 100, torch.float16),
+                                                   (64, 3000, 600, torch.bfloat16)])
+def test_paged_k4_equals_gathered_history(page, hist, chunk, dtype):
+    """K4 reading the KV4 history through the page table (sk_prefill_attn_paged)
+    gives the outputs of K4 over the K1b-expanded history, to fp rounding of
+    the accumulation order (same dequantised values, same schedules)."""
+    import math
+
+    from paper_2502_14866_b200.attn import run_prefill, run_prefill_paged
+    h, h_kv, d = 8, 2, 128
+    gates = [0.9, 0.1, 0.8, 0.2, 0.05, 0.15, 0.7, 0.6]
+    cfg = sk.EngineConfig(physical_page=page, logical_page=16, quant_bits=4, sink_blocks=1, local_blocks=2)
+    eng = sk.Engine(cfg, sk.classify_heads(gates, 0.5, 1, 2), device="cuda:0", dtype=dtype,
+                    capacity_tokens=hist + chunk)
+    g = torch.Generator(device="cuda").manual_seed(page + hist)
+    eng.load_context(torch.randn((hist, h_kv, d), generator=g, device="cuda").to(dtype),
+                     torch.randn((hist, h_kv, d), generator=g, device="cuda").to(dtype))
+    q = torch.randn((chunk, h, d), generator=g, device="cuda").to(dtype)
+    k = torch.randn((chunk, h_kv, d), generator=g, device="cuda").to(dtype)
+    v = torch.randn((chunk, h_kv, d), generator=g, device="cuda").to(dtype)
+    pool = eng.cache.pool
+    plan = eng._plan(chunk, hist + chunk)
+    kf, vf = pool.gather(extra_tokens=chunk)
+    kf[hist:], vf[hist:] = k, v
+    ref = run_prefill(q, kf, vf, plan, 1 / math.sqrt(d)).float()
+    out = run_prefill_paged(pool, hist, q, k, v, plan, 1 / math.sqrt(d)).float()
+    assert torch.isfinite(out).all()
+    assert (out - ref).abs().max().item() <= (2e-3 if dtype == torch.float16 else 1.6e-2)
