@@ -188,6 +188,18 @@ __device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t* r) {
 __device__ __forceinline__ float nib_f(uint32_t w, int shift) {
   return __uint_as_float(0x4B000000u | ((w >> shift) & 0xFu)) - 8388608.f;
 }
+// The two codes at bits [shift, +4) and [shift + 16, +4) of w, dequantised as
+// a pair with packed fp32 ops: PRMT builds 2^23 + n for both, one FADD2
+// removes 2^23 (exact), one FFMA2 applies (scale, lo) -- the same single
+// fp32 fma per value as K1b -- and the pair is rounded to T.
+template <typename T>
+__device__ __forceinline__ uint32_t nib_pair(uint32_t w, int shift, uint64_t sc2, uint64_t lo2) {
+  const uint32_t x = (w >> shift) & 0x000F000Fu;
+  const uint64_t f = f2_pack(__uint_as_float(__byte_perm(x, 0x4B000000u, 0x7540)),
+                             __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7542)));
+  const float2 v = f2_unpack(f2_fma(f2_add(f, f2_pack(-8388608.f, -8388608.f)), sc2, lo2));
+  return std::is_same<T, __nv_bfloat16>::value ? pack_bf162(v.x, v.y) : pack_half2(v.x, v.y);
+}
 
 // Producer warps 10-13 of the PAGED kernel: K/V block j of the item is built in
 // the stage's smem tiles in the layouts the MMAs read -- K row-major
@@ -454,33 +466,27 @@ __device__ __forceinline__ void paged_staged(PfSmem<D, NS, true>& sm, int st, in
     uint32_t pk[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const uint32_t wd = kw[j][u / 4];
       const float4 sl = *reinterpret_cast<const float4*>(&ktab[8 * m + 2 * j]);  // dims 8m+2j, +1
-      const float x0 = fmaf(nib_f(wd, 4 * (u % 4)), sl.x, sl.y);  // m % 4 == u % 4
-      const float x1 = fmaf(nib_f(wd, 4 * (u % 4) + 16), sl.z, sl.w);
-      pk[j] = kBF16 ? pack_bf162(x0, x1) : pack_half2(x0, x1);
+      pk[j] = nib_pair<T>(kw[j][u / 4], 4 * (u % 4), f2_pack(sl.x, sl.z), f2_pack(sl.y, sl.w));  // m%4 == u%4
     }
     const int d0 = 8 * m, chk = d0 / 64, un = (d0 % 64) / 8;
     *reinterpret_cast<uint4*>(kt + chk * (64 * 128) + t * 128 + ((un ^ (t & 7)) << 4)) =
         make_uint4(pk[0], pk[1], pk[2], pk[3]);
   }
   uint8_t* vr = &sm.kv[st][1][0][0] + c * 128;
+  const uint64_t vsc2 = f2_pack(vsl.x, vsl.x), vlo2 = f2_pack(vsl.y, vsl.y);
 #pragma unroll
   for (int q8 = 0; q8 < VKEYS / 8; ++q8) {
     uint32_t pk[4];
 #pragma unroll
     for (int e2 = 0; e2 < 4; ++e2) {
-      float x2[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        // key tin = kh*VKEYS + tr of the page: word ((tin%8)/2)*2 + tin/32 -- a register index
-        // fixed at compile time (kh only picks between two words when D = 64)
-        const int tr = 8 * q8 + 2 * e2 + e;
-        const int wi = ((tr % 8) / 2) * 2 + (D == 128 ? tr / 32 : 0);
-        const uint32_t wd = (D == 128 || kh == 0) ? vrun[wi] : vrun[wi + 1];
-        x2[e] = fmaf(nib_f(wd, 4 * ((tr / 8) % 4) + 16 * (tr % 2)), vsl.x, vsl.y);
-      }
-      pk[e2] = kBF16 ? pack_bf162(x2[0], x2[1]) : pack_half2(x2[0], x2[1]);
+      // keys tin = kh*VKEYS + tr, tr + 1 of the page share word ((tin%8)/2)*2 + tin/32 -- a
+      // register index fixed at compile time (kh only picks between two words when D = 64) --
+      // at bit offsets 4((tin/8)%4) and +16
+      const int tr = 8 * q8 + 2 * e2;
+      const int wi = ((tr % 8) / 2) * 2 + (D == 128 ? tr / 32 : 0);
+      const uint32_t wd = (D == 128 || kh == 0) ? vrun[wi] : vrun[wi + 1];
+      pk[e2] = nib_pair<T>(wd, 4 * ((tr / 8) % 4), vsc2, vlo2);
     }
     const int un = (kh * VKEYS) / 8 + q8;
     *reinterpret_cast<uint4*>(vr + ((un ^ (c & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);

@@ -166,8 +166,12 @@ class Engine:
     """engine.py:108-286 -- one layer of one sequence, device resident."""
 
     def __init__(self, config: EngineConfig, profiles: list, *, dtype: torch.dtype = _device.DEFAULT_DTYPE,
-                 device=None, capacity_tokens: int = 0):
+                 device=None, capacity_tokens: int = 0, paged_history: bool | None = None):
         self.config = config
+        # chunked prefill over KV4 history: True = K4 reads pages through the page table,
+        # False = K1b gathers the history into a dense buffer first (faster, see DESIGN.md §4),
+        # None = gather unless the dense buffer would not fit in half the free HBM
+        self.paged_history = paged_history
         self.profiles = profiles
         self.cache: TwoWayCache | None = None
         self.ledger = CostLedger()
@@ -353,7 +357,7 @@ class Engine:
                                  "cannot be attended")
         s0 = self.cache.num_tokens
         plan = self._plan(n, s0 + n)
-        if 1 <= pool.bits <= 4 and pool.P in (32, 64):
+        if 1 <= pool.bits <= 4 and pool.P in (32, 64) and self._use_paged(pool, s0 + n, dp):
             # K4 reads the KV4 history through the page table (no history buffer)
             out = run_prefill_paged(pool, s0, q, k.contiguous(), v.contiguous(), plan, 1.0 / math.sqrt(head_dim))
         else:  # KV8 / raw pages: K1b expands the history once, K4 streams it with TMA
@@ -366,6 +370,13 @@ class Engine:
             self.ledger.record_tiles(PREFILL, hh, int(plan.visited[hh]), int(plan.total[hh]))
         self.cache.append_all(k, v)
         return out
+
+    def _use_paged(self, pool, tokens: int, dp: int) -> bool:
+        if self.paged_history is not None:
+            return bool(self.paged_history)
+        need = 2 * tokens * pool.n_streams * dp * torch.empty((), dtype=self._dtype).element_size()
+        free, _ = torch.cuda.mem_get_info(self.device)
+        return need > free // 2
 
     def load_context(self, k_history, v_history) -> None:
         """engine.py:175-204: K1 bulk append, no attention."""

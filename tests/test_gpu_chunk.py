@@ -49,15 +49,16 @@ CHUNK_CASES = [
 ]
 
 
+@pytest.mark.parametrize("paged", [False, True], ids=["gather", "paged"])
 @pytest.mark.parametrize("case", CHUNK_CASES)
-def test_chunked_prefill_against_oracle(case):
+def test_chunked_prefill_against_oracle(case, paged):
     splits, total, h, h_kv, bits, sp = case
     rng = np.random.default_rng(sum(splits) + total)
     d = 128
     gates = list(rng.uniform(0, 1, h))
     q, k, v = fp16_vals(rng, total, h, d), fp16_vals(rng, total, h_kv, d), fp16_vals(rng, total, h_kv, d)
     cfg = sk.EngineConfig(quant_bits=bits, budget_tokens=256, reuse_interval=2, local_blocks=2, target_sparsity=sp)
-    eng = sk.Engine(cfg, sk.classify_heads(gates, sp, 1, 2), device="cuda:0")
+    eng = sk.Engine(cfg, sk.classify_heads(gates, sp, 1, 2), device="cuda:0", paged_history=paged)
     ref = O.OracleEngine(O.Config(quant_bits=bits, budget_tokens=256, reuse_interval=2, local_blocks=2,
                                   target_sparsity=sp), O.assign_roles(gates, sp, 1, 2))
     a = 0

@@ -36,7 +36,7 @@ def main():
     gates = [0.9 - 0.001 * i if i % 4 < 2 else 0.1 + 0.001 * i for i in range(H)]
     prof = sk.classify_heads(gates, 0.5, 1, 4)
     cfg = sk.EngineConfig(quant_bits=4, local_blocks=4)
-    for s0, c in ((131072, 8192), (131072, 2048), (32768, 4096)):
+    for s0, c in ((131072, 8192), (131072, 2048), (131072, 512), (131072, 256), (32768, 4096)):
         eng = sk.Engine(cfg, prof, device="cuda:0", capacity_tokens=s0 + c)
         g = torch.Generator(device="cuda").manual_seed(s0 + c)
         kh = torch.randn((s0, HKV, D), generator=g, device="cuda", dtype=torch.float16)
