@@ -122,6 +122,18 @@ __device__ uint64_t g_dec_stamps[4096][8];
   } while (0)
 #endif
 
+// timing builds only (tools/ab_variant.sh): 2 = no ticket / merge of the
+// partials, 3 = the last CTA skips the final merge, 4 = units only
+#ifndef SK_DEC_ABLATE
+#define SK_DEC_ABLATE 0
+#endif
+#ifndef SK_DEC_STAGE  // 0: the one-CTA-per-stream path loads pages straight into registers
+#define SK_DEC_STAGE 1
+#endif
+#ifndef SK_DEC_MINB
+#define SK_DEC_MINB 1
+#endif
+
 // m16n8k16 MMA, fp32 accumulate.
 template <typename MT>
 __device__ __forceinline__ void mma16816_full(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
@@ -185,6 +197,38 @@ __device__ __forceinline__ uint32_t byte2h(uint32_t w, int r2) {
 
 __device__ __forceinline__ uint4 ldg16(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 __device__ __forceinline__ uint2 ldg8(const void* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
+// unit loads from global memory (SM = false) or from a page staged in shared
+// memory by a bulk copy (SM = true)
+template <bool SM>
+__device__ __forceinline__ uint4 ldu16(const void* p) {
+  if constexpr (SM) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(smem_u32(p)));
+    return v;
+  } else {
+    return ldg16(p);
+  }
+}
+template <bool SM>
+__device__ __forceinline__ uint2 ldu8(const void* p) {
+  if constexpr (SM) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(smem_u32(p)));
+    return v;
+  } else {
+    return ldg8(p);
+  }
+}
+template <bool SM>
+__device__ __forceinline__ uint32_t ldu4(const void* p) {
+  if constexpr (SM) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)));
+    return v;
+  } else {
+    return __ldg(reinterpret_cast<const uint32_t*>(p));
+  }
+}
 
 // Binary search in an ascending int list.
 __device__ __forceinline__ bool contains(const int32_t* a, int n, int x) {
@@ -235,7 +279,7 @@ struct UnitData {
 // Every load of one 32-token unit (tiles tt0, tt0+1 of the page in slot pg),
 // straight into registers -- issued before any math (one round trip), and
 // for the first unit before the kernel's dependency wait (PDL prologue).
-template <typename T, int KIND, int D, int P, int UT>
+template <typename T, int KIND, int D, int P, int UT, bool SM = false>
 __device__ __forceinline__ void unit_load(const uint8_t* pg, int tt0, UnitData<T, KIND, D, P, UT>& u) {
   using U = UnitData<T, KIND, D, P, UT>;
   constexpr int NCT = D / 16;
@@ -251,12 +295,12 @@ __device__ __forceinline__ void unit_load(const uint8_t* pg, int tt0, UnitData<T
     for (int h = 0; h < 2; ++h) {
       const uint8_t* src = kc + (16 * (tt0 + i) + 8 * h + g) * RB + j * (RB / 4);
       if constexpr (KW == 2) {
-        const uint2 v = ldg8(src);
+        const uint2 v = ldu8<SM>(src);
         u.kw[i][h][0] = v.x; u.kw[i][h][1] = v.y;
       } else {
 #pragma unroll
         for (int w = 0; w < KW / 4; ++w) {
-          const uint4 v = ldg16(src + 16 * w);
+          const uint4 v = ldu16<SM>(src + 16 * w);
           u.kw[i][h][4 * w] = v.x; u.kw[i][h][4 * w + 1] = v.y; u.kw[i][h][4 * w + 2] = v.z; u.kw[i][h][4 * w + 3] = v.w;
         }
       }
@@ -267,14 +311,14 @@ __device__ __forceinline__ void unit_load(const uint8_t* pg, int tt0, UnitData<T
   for (int cn = 0; cn < 2 * NCT; ++cn) {
     const uint8_t* src = vc + ((32 * cn + lane) * VW + w0) * 4;
     if constexpr (VU == 1) {
-      u.vw[cn][0] = __ldg(reinterpret_cast<const uint32_t*>(src));
+      u.vw[cn][0] = ldu4<SM>(src);
     } else if constexpr (VU == 2) {
-      const uint2 v = ldg8(src);
+      const uint2 v = ldu8<SM>(src);
       u.vw[cn][0] = v.x; u.vw[cn][1] = v.y;
     } else {
 #pragma unroll
       for (int w = 0; w < VU / 4; ++w) {
-        const uint4 v = ldg16(src + 16 * w);
+        const uint4 v = ldu16<SM>(src + 16 * w);
         u.vw[cn][4 * w] = v.x; u.vw[cn][4 * w + 1] = v.y; u.vw[cn][4 * w + 2] = v.z; u.vw[cn][4 * w + 3] = v.w;
       }
     }
@@ -284,9 +328,9 @@ __device__ __forceinline__ void unit_load(const uint8_t* pg, int tt0, UnitData<T
   if constexpr (KIND != 0) {
 #pragma unroll
     for (int i = 0; i < D / 32; ++i) {
-      const uint4 a = ldg16(bnd + j * (D / 4) + 8 * i), b = ldg16(bnd + D + j * (D / 4) + 8 * i);
-      const uint4 c = ldg16(bnd + 2 * D + (g >> 1) * (D / 4) + 8 * i);
-      const uint4 d = ldg16(bnd + 3 * D + (g >> 1) * (D / 4) + 8 * i);
+      const uint4 a = ldu16<SM>(bnd + j * (D / 4) + 8 * i), b = ldu16<SM>(bnd + D + j * (D / 4) + 8 * i);
+      const uint4 c = ldu16<SM>(bnd + 2 * D + (g >> 1) * (D / 4) + 8 * i);
+      const uint4 d = ldu16<SM>(bnd + 3 * D + (g >> 1) * (D / 4) + 8 * i);
       u.kb_lo[4 * i] = a.x; u.kb_lo[4 * i + 1] = a.y; u.kb_lo[4 * i + 2] = a.z; u.kb_lo[4 * i + 3] = a.w;
       u.kb_hi[4 * i] = b.x; u.kb_hi[4 * i + 1] = b.y; u.kb_hi[4 * i + 2] = b.z; u.kb_hi[4 * i + 3] = b.w;
       u.vb_lo[4 * i] = c.x; u.vb_lo[4 * i + 1] = c.y; u.vb_lo[4 * i + 2] = c.z; u.vb_lo[4 * i + 3] = c.w;
@@ -494,9 +538,25 @@ __device__ __forceinline__ void finish_out(const DecodeParams& prm, int s, int r
   else reinterpret_cast<__nv_bfloat16*>(prm.out)[oi] = __float2bfloat16_rn(O);
 }
 
-template <typename T, int KIND, int D, int P, int UT>
-__global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_constant__ DecodeParams prm) {
+// Bytes of a page slot a unit reads: codes of K and V, then the four bound rows.
+template <int KIND, int D, int P>
+__host__ __device__ constexpr int slot_used_bytes() {
+  return (KIND == 0 ? 4 * P * D : (KIND == 1 ? P * D : 2 * P * D)) + (KIND == 0 ? 0 : 8 * D);
+}
+// STAGE (one CTA per stream, whole-page units): each warp streams its pages
+// through two shared-memory buffers filled by bulk copies, the next page in
+// flight while the current one computes.
+template <int KIND, int D, int P, int UT>
+__host__ __device__ constexpr bool stage_fits() {
+  return KIND == 1 && P == 16 * UT && 2 * kWarps * slot_used_bytes<KIND, D, P>() <= 160 * 1024;
+}
+
+template <typename T, int KIND, int D, int P, int UT, bool STAGE = false>
+__global__ void __launch_bounds__(kDecThreads, SK_DEC_MINB) decode_kernel(const __grid_constant__ DecodeParams prm) {
   constexpr int UPP = P / (16 * UT);  // units per page
+  constexpr int kSlotUsed = slot_used_bytes<KIND, D, P>();
+  static_assert(!STAGE || stage_fits<KIND, D, P, UT>(), "staged decode needs whole-page units that fit");
+  __shared__ uint64_t s_sbar[STAGE ? 2 * kWarps : 1];
   __shared__ int s_sel[kMaxSel];
   __shared__ int s_extra[kWarps][kMaxExtra];
   __shared__ float s_m[kWarps][kMaxRows], s_l[kWarps][kMaxRows];
@@ -600,7 +660,31 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   uint32_t um_next = 0;
   const uint8_t* slot_next = nullptr;
   UnitData<T, KIND, D, P, UT> ud;
-  if (u < NU) {
+  uint64_t* sbar = s_sbar + 2 * warp;
+  uint8_t* sbuf = reinterpret_cast<uint8_t*>(s_part) + (size_t)warp * 2 * kSlotUsed;
+  // warp-wide: lane 0 bulk-copies the page slot of unit uu into buffer b
+  auto stage_unit = [&](int uu, int b) {
+    uint32_t um_;
+    const uint8_t* src = pv.slot_ptr(s, unit_page(uu, um_));
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the warp's reads of b precede the copy
+      mbar_arrive_expect_tx(sbar + b, kSlotUsed);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(sbuf + b * kSlotUsed)),
+                   "l"(src), "r"(kSlotUsed), "r"(smem_u32(sbar + b))
+                   : "memory");
+    }
+  };
+  if constexpr (STAGE) {
+    if (lane == 0) {
+      mbar_init(sbar, 1);
+      mbar_init(sbar + 1, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    if (u < NU) stage_unit(u, 0);
+    if (u + ustride < NU) stage_unit(u + ustride, 1);
+  } else if (u < NU) {
     pg_next = unit_page(u, um_next);
     slot_next = pv.slot_ptr(s, pg_next);  // round trip 2 (page table)
     if (16 * UT * (u % UPP) < min(P, n_tok - pg_next * P)) unit_load<T, KIND, D, P, UT>(slot_next, UT * (u % UPP), ud);
@@ -637,7 +721,21 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     }
   }
   bool first = true;
-  for (; u < NU; u += ustride) {
+  if constexpr (STAGE) {
+    for (int it = 0; u < NU; u += ustride, ++it) {
+      uint32_t um;
+      const int pg = unit_page(u, um), b = it & 1;
+      const int tok_in_page = min(P, n_tok - pg * P);
+      mbar_wait(sbar + b, (it >> 1) & 1);
+      unit_load<T, KIND, D, P, UT, true>(sbuf + b * kSlotUsed, 0, ud);
+      unit_compute<T, KIND, D, P, UT>(ud, 0, tok_in_page, um & gmask, qw, sl2, inv_levels, st);
+      if (u + 2 * ustride < NU) {
+        __syncwarp();
+        stage_unit(u + 2 * ustride, b);
+      }
+    }
+  }
+  for (; !STAGE && u < NU; u += ustride) {
     const int pg = pg_next;
     const uint32_t um = um_next;
     const uint8_t* slot = slot_next;
@@ -667,6 +765,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     if (lane == 0) s_self[warp] = dot * prm.scale_log2;
   }
   DSTAMP(2);
+  if (SK_DEC_ABLATE == 4) return;
 
   // ---- merge the CTA's warps ---------------------------------------------------
 #pragma unroll
@@ -724,6 +823,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
     DSTAMP(6);
     return;
   }
+  if (SK_DEC_ABLATE == 2) return;
   // ---- partial -> workspace; the stream's last CTA merges them -----------------
   __syncthreads();
   if (tid == 0) {  // bar.sync + a gpu-scope acq_rel RMW: releases this partial, acquires the others
@@ -750,6 +850,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   if (!s_last) return;
   mbar_wait(&s_bar, 0);
   DSTAMP(5);
+  if (SK_DEC_ABLATE == 3) return;
   // per-(row, partial) merge factors 2^(m_b - M) once -- warp rr, lane b (the new
   // token's at b = cps) -- and the reciprocal of each row's normaliser L
   const int cps = prm.cps;
@@ -785,14 +886,15 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(const __grid_con
   DSTAMP(6);
 }
 
-template <typename T, int KIND, int D, int P, int UT>
+template <typename T, int KIND, int D, int P, int UT, bool STAGE = false>
 int launch_ut(const DecodeParams& prm, int n_streams, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(prm.cps, n_streams, 1);
   cfg.blockDim = dim3(kDecThreads, 1, 1);
-  cfg.dynamicSmemBytes = prm.cps > 1 ? (size_t)prm.cps * part_floats(prm.G, D) * 4 : 0;
+  cfg.dynamicSmemBytes = STAGE ? (size_t)2 * kWarps * slot_used_bytes<KIND, D, P>()
+                               : (prm.cps > 1 ? (size_t)prm.cps * part_floats(prm.G, D) * 4 : 0);
   if (cfg.dynamicSmemBytes > 0)  // static + dynamic exceeds the 48 KB default
-    cudaFuncSetAttribute(decode_kernel<T, KIND, D, P, UT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(decode_kernel<T, KIND, D, P, UT, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)cfg.dynamicSmemBytes);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -800,7 +902,7 @@ int launch_ut(const DecodeParams& prm, int n_streams, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (prm.flags & SK_LAUNCH_PDL) ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, KIND, D, P, UT>, prm);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, KIND, D, P, UT, STAGE>, prm);
   if (e != cudaSuccess) {
     set_error(std::string("decode_kernel: ") + cudaGetErrorString(e));
     return SK_ECUDA;
@@ -815,7 +917,11 @@ int launch_ut(const DecodeParams& prm, int n_streams, cudaStream_t st) {
 template <typename T, int KIND, int D, int P>
 int launch_one(const DecodeParams& prm, int n_streams, cudaStream_t st) {
   constexpr int UT_BIG = (P >= 64 && KIND == 1) ? 4 : 2;  // raw / byte codes: registers only fit 2 tiles
-  if (prm.cps == 1 && UT_BIG != 2) return launch_ut<T, KIND, D, P, UT_BIG>(prm, n_streams, st);
+  if (prm.cps == 1 && UT_BIG != 2) {
+    if constexpr (SK_DEC_STAGE && stage_fits<KIND, D, P, UT_BIG>())
+      return launch_ut<T, KIND, D, P, UT_BIG, true>(prm, n_streams, st);
+    return launch_ut<T, KIND, D, P, UT_BIG>(prm, n_streams, st);
+  }
   return launch_ut<T, KIND, D, P, 2>(prm, n_streams, st);
 }
 

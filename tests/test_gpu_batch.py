@@ -78,7 +78,14 @@ def test_batched_eager_matches_engines_all_cluster_sizes(batch, h, h_kv):
             np.testing.assert_allclose(out[b], res.output, atol=2e-3, rtol=0, err_msg=f"step {t} seq {b}")
 
 
-def test_ragged_cfg4_batch_against_oracle():
+RAGGED = {
+    "cfg4_6seq": [4100, 9000, 12037, 6500, 16384, 5000],       # 48 streams: K3 splits each over CTAs
+    "cfg4_12seq": [4100, 9000, 5037, 6500, 8192, 5000, 4097, 7001, 4300, 6100, 5555, 4444],  # 96: one CTA
+}                                                                # per stream, pages staged in smem
+
+
+@pytest.mark.parametrize("lens", list(RAGGED.values()), ids=list(RAGGED))
+def test_ragged_cfg4_batch_against_oracle(lens):
     """BASELINE cfg4 geometry (32 Q / 8 KV heads, D 128, balanced gates, KV4,
     budget 4096, reuse 4) for a RAGGED batch: every sequence has its own
     context length, page-table rows and token counts in one pool.  Each
@@ -89,7 +96,6 @@ def test_ragged_cfg4_batch_against_oracle():
     from test_gpu_parity import assert_close_attn
     rng = np.random.default_rng(4)
     h, h_kv, d = 32, 8, 128
-    lens = [4100, 9000, 12037, 6500, 16384, 5000]
     B = len(lens)
     gates = [0.9 - 0.001 * i if i % 4 < 2 else 0.1 + 0.001 * i for i in range(h)]
     kw = dict(quant_bits=4, budget_tokens=4096, reuse_interval=4, local_blocks=4)
