@@ -11,20 +11,232 @@
 // HBM-bound: reads the raw page once, writes codes + bounds + stats.
 #include "append_impl.cuh"
 
+#ifndef SK_APPEND_FAST  // 0: every page through the generic rebuild (A/B builds)
+#define SK_APPEND_FAST 1
+#endif
+
 namespace sk {
 
 namespace {
 
+// code of x from the fp32 quotient, rounded to nearest-even by the 1.5 * 2^23
+// magic add (FMA pipe, no F2I / FRND); the near-tie quotients take the fp64
+// path of quant_code (the same decision rule as quant_code32).
+__device__ __forceinline__ uint32_t qcode_magic(float x, float lo32, float inv32, int levels, const double* lo64,
+                                                const double* sc64, const double* inv64, int ci) {
+  const float t = __fmul_rn(__fsub_rn(x, lo32), inv32);
+  const float r = __fadd_rn(t, 12582912.f);
+  const float d = __fsub_rn(t, __fsub_rn(r, 12582912.f));
+  if (fabsf(fabsf(d) - 0.5f) < 0x1p-10f) return quant_code((double)x, lo64[ci], sc64[ci], inv64[ci], levels);
+  return min(__float_as_uint(r) & 0xFFu, (uint32_t)levels);
+}
+
+// Full-page fast path of the bulk append: a KV4 (bits <= 4) page of 64 new
+// tokens, D = 128, logical pages of 16.  The raw page never touches shared
+// memory: warp wq = (w, j) = (wq / 4, wq % 4) and lane (m, e) = (lane % 16,
+// lane / 16) hold tokens t_i = 32w + 8i + 2j + e (i < 4) at dims
+// 32(m/4) + 2(m%4) + 8sl + {0, 1} (sl < 4) of K and V, so a thread owns every
+// nibble of the K word (t_i, j = m%4, w = m/4) and, with its lane^16 partner,
+// the V words (channel, j, w) of its eight channels (sk_layout.cuh).  Only the
+// per-channel min / max reductions go through shared memory.
 template <typename T>
-__global__ void __launch_bounds__(256) append_kernel(PoolView pv, const T* __restrict__ k_src,
-                                                     const T* __restrict__ v_src, int64_t src_ss, int64_t src_ts,
-                                                     const int32_t* __restrict__ tokens, int m) {
+__device__ void append_full_kv4(const PoolView& pv, int s, int p, const T* __restrict__ src_k,
+                                const T* __restrict__ src_v, int64_t src_ts, int tok0, uint8_t* smem) {
+  constexpr int D = 128;
+  using H2 = typename std::conditional<std::is_same<T, __half>::value, __half2, __nv_bfloat162>::type;
+  auto hmin = [](uint32_t a, uint32_t b) {
+    H2 r = __hmin2(*reinterpret_cast<H2*>(&a), *reinterpret_cast<H2*>(&b));
+    return *reinterpret_cast<uint32_t*>(&r);
+  };
+  auto hmax = [](uint32_t a, uint32_t b) {
+    H2 r = __hmax2(*reinterpret_cast<H2*>(&a), *reinterpret_cast<H2*>(&b));
+    return *reinterpret_cast<uint32_t*>(&r);
+  };
+  const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+  const int w = wq >> 2, j = wq & 3, m = lane & 15, e = lane >> 4;
+  const int dbase = 32 * (m >> 2) + 2 * (m & 3);
+  const bool streaming = pv.kind[s] == SK_KIND_STREAMING;
+  const int levels = (1 << pv.bits) - 1;
+  uint4* red_k = reinterpret_cast<uint4*>(smem);         // [w 2][j 4][h 2][mm 2][m 16]
+  uint4* red_v = red_k + 2 * 4 * 2 * 2 * 16;             // [wq 8][mm 2][m 16]
+  uint4* kb = red_v + 8 * 2 * 16;                        // [mm 2][m 16] K page bounds
+  uint4* vb = kb + 2 * 16;                               // [mm 2][m 16] V page bounds
+  float* lo32 = reinterpret_cast<float*>(vb + 2 * 16);  // [which 2][q 128], q = 8m + 2sl + x
+  float* inv32 = lo32 + 256;
+  double* lo64 = reinterpret_cast<double*>(inv32 + 256);
+  double* sc64 = lo64 + 256;
+  double* inv64 = sc64 + 256;
+
+  // 1. raw K / V pairs: 16 x 4 bytes each per thread (a warp instruction reads
+  //    eight 16-byte runs of two token rows; the sl instructions share sectors in L1)
+  uint32_t kr[4][4], vr[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t off = (int64_t)(tok0 + 32 * w + 8 * i + 2 * j + e) * src_ts + dbase;
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl) {
+      kr[i][sl] = __ldg(reinterpret_cast<const uint32_t*>(src_k + off + 8 * sl));
+      vr[i][sl] = __ldg(reinterpret_cast<const uint32_t*>(src_v + off + 8 * sl));
+    }
+  }
+  // 2. per-thread min / max: K per logical page h (tokens i = 2h, 2h+1), V over
+  //    all four tokens; then across e (lane ^ 16)
+  uint32_t kmn[2][4], kmx[2][4], vmn[4], vmx[4];
+#pragma unroll
+  for (int sl = 0; sl < 4; ++sl) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      kmn[h][sl] = hmin(kr[2 * h][sl], kr[2 * h + 1][sl]);
+      kmx[h][sl] = hmax(kr[2 * h][sl], kr[2 * h + 1][sl]);
+      kmn[h][sl] = hmin(kmn[h][sl], __shfl_xor_sync(0xffffffffu, kmn[h][sl], 16));
+      kmx[h][sl] = hmax(kmx[h][sl], __shfl_xor_sync(0xffffffffu, kmx[h][sl], 16));
+    }
+    vmn[sl] = hmin(hmin(vr[0][sl], vr[1][sl]), hmin(vr[2][sl], vr[3][sl]));
+    vmx[sl] = hmax(hmax(vr[0][sl], vr[1][sl]), hmax(vr[2][sl], vr[3][sl]));
+    vmn[sl] = hmin(vmn[sl], __shfl_xor_sync(0xffffffffu, vmn[sl], 16));
+    vmx[sl] = hmax(vmx[sl], __shfl_xor_sync(0xffffffffu, vmx[sl], 16));
+  }
+  // lane e = 0 publishes the minima, e = 1 the maxima
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    red_k[(((w * 4 + j) * 2 + h) * 2 + e) * 16 + m] =
+        e ? make_uint4(kmx[h][0], kmx[h][1], kmx[h][2], kmx[h][3]) : make_uint4(kmn[h][0], kmn[h][1], kmn[h][2], kmn[h][3]);
+  red_v[(wq * 2 + e) * 16 + m] = e ? make_uint4(vmx[0], vmx[1], vmx[2], vmx[3]) : make_uint4(vmn[0], vmn[1], vmn[2], vmn[3]);
+  __syncthreads();
+  // 3. threads 0..127: logical page lp = tid % 4 of (mm, m) = tid / 4 -> key
+  //    stats, then the K bounds across the four lanes; threads 128..159: V bounds
+  if (tid < 128) {
+    const int lp = tid & 3, mm = (tid >> 2) >> 4, mq = (tid >> 2) & 15, ww = lp >> 1, h = lp & 1;
+    uint4 a = red_k[(((ww * 4 + 0) * 2 + h) * 2 + mm) * 16 + mq];
+#pragma unroll
+    for (int jj = 1; jj < 4; ++jj) {
+      const uint4 b = red_k[(((ww * 4 + jj) * 2 + h) * 2 + mm) * 16 + mq];
+      a = mm ? make_uint4(hmax(a.x, b.x), hmax(a.y, b.y), hmax(a.z, b.z), hmax(a.w, b.w))
+             : make_uint4(hmin(a.x, b.x), hmin(a.y, b.y), hmin(a.z, b.z), hmin(a.w, b.w));
+    }
+    if (!streaming && pv.stats != nullptr) {
+      T* st = reinterpret_cast<T*>(pv.stats_ptr(s, p * 4 + lp)) + mm * D + 32 * (mq >> 2) + 2 * (mq & 3);
+      *reinterpret_cast<uint32_t*>(st) = a.x;
+      *reinterpret_cast<uint32_t*>(st + 8) = a.y;
+      *reinterpret_cast<uint32_t*>(st + 16) = a.z;
+      *reinterpret_cast<uint32_t*>(st + 24) = a.w;
+    }
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+      const uint4 b = make_uint4(__shfl_xor_sync(0xffffffffu, a.x, off), __shfl_xor_sync(0xffffffffu, a.y, off),
+                                 __shfl_xor_sync(0xffffffffu, a.z, off), __shfl_xor_sync(0xffffffffu, a.w, off));
+      a = mm ? make_uint4(hmax(a.x, b.x), hmax(a.y, b.y), hmax(a.z, b.z), hmax(a.w, b.w))
+             : make_uint4(hmin(a.x, b.x), hmin(a.y, b.y), hmin(a.z, b.z), hmin(a.w, b.w));
+    }
+    if (lp == 0) kb[mm * 16 + mq] = a;
+  } else if (tid < 160) {
+    const int mm = (tid - 128) >> 4, mq = tid & 15;
+    uint4 a = red_v[mm * 16 + mq];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) {
+      const uint4 b = red_v[(q * 2 + mm) * 16 + mq];
+      a = mm ? make_uint4(hmax(a.x, b.x), hmax(a.y, b.y), hmax(a.z, b.z), hmax(a.w, b.w))
+             : make_uint4(hmin(a.x, b.x), hmin(a.y, b.y), hmin(a.z, b.z), hmin(a.w, b.w));
+    }
+    vb[mm * 16 + mq] = a;
+  }
+  __syncthreads();
+  // 4. one thread per (which, q): bounds -> the page slot, quantiser tables
+  uint8_t* slot = pv.slot_ptr(s, p);
+  {
+    const int which = tid >> 7, q = tid & 127, mq = q >> 3, sl = (q & 7) >> 1, x = q & 1;
+    const uint4* b = which ? vb : kb;
+    const T* lo_h = reinterpret_cast<const T*>(&b[mq]);
+    const T* hi_h = reinterpret_cast<const T*>(&b[16 + mq]);
+    const T lo_t = lo_h[q & 7], hi_t = hi_h[q & 7];
+    const int c = 32 * (mq >> 2) + 2 * (mq & 3) + 8 * sl + x;
+    T* bnd = reinterpret_cast<T*>(pv.bounds(slot));
+    const int pos = which ? vbound_pos(c, D) : kbound_pos(c, D);
+    bnd[(2 * which) * D + pos] = lo_t;
+    bnd[(2 * which + 1) * D + pos] = hi_t;
+    const float lo = DT<T>::to_f(lo_t), hi = DT<T>::to_f(hi_t);
+    double sc = ((double)hi - (double)lo) / levels;
+    if (!(sc > 0.0)) sc = 1.0;
+    lo32[tid] = lo;
+    inv32[tid] = (float)(1.0 / sc);
+    lo64[tid] = lo;
+    sc64[tid] = sc;
+    inv64[tid] = 1.0 / sc;
+  }
+  __syncthreads();
+  // 5. K words: token t_i, (j = m%4, w = m/4), slot sl = the pair's dim / 8
+  uint32_t* kw = reinterpret_cast<uint32_t*>(pv.k_codes(slot));
+  uint32_t* vw = reinterpret_cast<uint32_t*>(pv.v_codes(slot));
+  {
+    float l[8], iv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      l[k] = lo32[8 * m + k];
+      iv[k] = inv32[8 * m + k];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int sl = 0; sl < 4; ++sl) {
+        const float2 x = DT<T>::to_f2(kr[i][sl]);
+        const uint32_t c0 = qcode_magic(x.x, l[2 * sl], iv[2 * sl], levels, lo64, sc64, inv64, 8 * m + 2 * sl);
+        const uint32_t c1 = qcode_magic(x.y, l[2 * sl + 1], iv[2 * sl + 1], levels, lo64, sc64, inv64, 8 * m + 2 * sl + 1);
+        word |= (c0 << (4 * sl)) | (c1 << (16 + 4 * sl));
+      }
+      kw[(32 * w + 8 * i + 2 * j + e) * 16 + (m & 3) * 4 + (m >> 2)] = word;
+    }
+  }
+  // 6. V words: channel (sl, x) of this thread, tokens t_i -> slot i, e; the
+  //    lane^16 partner holds the other e
+  {
+    float l[8], iv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      l[k] = lo32[128 + 8 * m + k];
+      iv[k] = inv32[128 + 8 * m + k];
+    }
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl) {
+      uint32_t pw[2] = {0u, 0u};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 x = DT<T>::to_f2(vr[i][sl]);
+        pw[0] |= qcode_magic(x.x, l[2 * sl], iv[2 * sl], levels, lo64, sc64, inv64, 128 + 8 * m + 2 * sl) << (4 * i + 16 * e);
+        pw[1] |= qcode_magic(x.y, l[2 * sl + 1], iv[2 * sl + 1], levels, lo64, sc64, inv64, 128 + 8 * m + 2 * sl + 1)
+                 << (4 * i + 16 * e);
+      }
+      pw[0] |= __shfl_xor_sync(0xffffffffu, pw[0], 16);
+      pw[1] |= __shfl_xor_sync(0xffffffffu, pw[1], 16);
+      const int c = dbase + 8 * sl + e;  // lane e stores channel x = e
+      vw[((c >> 3) * 32 + 4 * (c & 7) + j) * 2 + w] = pw[e];
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 2) append_kernel(PoolView pv, const T* __restrict__ k_src,
+                                                        const T* __restrict__ v_src, int64_t src_ss, int64_t src_ts,
+                                                        const int32_t* __restrict__ tokens, int m) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int s = blockIdx.y;
   const int n0 = tokens[s];
   const int n1 = n0 + m;
   const int p = n0 / pv.P + blockIdx.x;
   if (p > (n1 - 1) / pv.P) return;
+  const int t0 = p * pv.P;
+  if (SK_APPEND_FAST && pv.bits >= 1 && pv.bits <= 4 && pv.D == 128 && pv.P == 64 && pv.L == 16 && t0 >= n0 &&
+      t0 + 64 <= n1) {
+    const bool streaming = pv.kind[s] == SK_KIND_STREAMING;
+    const int count = (n1 + pv.P - 1) / pv.P;
+    const bool evicted = streaming && p >= pv.sink && p < count - pv.local;
+    // a partial last page's tail is written to staging by the open page's CTA
+    const int p_open = n0 / pv.P, p_last = (n1 - 1) / pv.P;
+    if (p == p_open && p_last != p_open && (n1 % pv.P) != 0)
+      write_tail_from_src<T>(pv, s, n0, n1, k_src + s * src_ss, v_src + s * src_ss, src_ts);
+    if (!evicted) append_full_kv4<T>(pv, s, p, k_src + s * src_ss, v_src + s * src_ss, src_ts, t0 - n0, smem);
+    return;
+  }
   append_page<T>(pv, s, p, n0, n1, k_src + s * src_ss, v_src + s * src_ss, src_ts, smem);
 }
 

@@ -34,6 +34,24 @@ __device__ __forceinline__ uint32_t quant_code32(float x, float lo32, float inv3
   return (uint32_t)fminf(fmaxf(r, 0.f), (float)levels);
 }
 
+// The raw tokens of a partial last page (n1 % P != 0) -> the stream's staging
+// rows, straight from the source (every tail token is new).  Whole CTA.
+template <typename T>
+__device__ void write_tail_from_src(const PoolView& pv, int s, int n0, int n1, const T* __restrict__ src_k,
+                                    const T* __restrict__ src_v, int64_t src_ts) {
+  constexpr int vec = 8;
+  const int D = pv.D, P = pv.P;
+  T* wk = reinterpret_cast<T*>(pv.staging_ptr(s, 0));
+  T* wv = reinterpret_cast<T*>(pv.staging_ptr(s, 1));
+  const int tail0 = (n1 - 1) / P * P;  // > n0
+  for (int i = threadIdx.x; i < (n1 - tail0) * (D / vec); i += blockDim.x) {
+    const int tl = i / (D / vec), c = (i % (D / vec)) * vec;
+    const int64_t off = (int64_t)(tail0 + tl - n0) * src_ts + c;
+    *reinterpret_cast<uint4*>(wk + tl * D + c) = *reinterpret_cast<const uint4*>(src_k + off);
+    *reinterpret_cast<uint4*>(wv + tl * D + c) = *reinterpret_cast<const uint4*>(src_v + off);
+  }
+}
+
 // Rebuild page p of stream s after tokens [n0, n1) were appended: raw page
 // -> smem, bounds, codes (fragment-native layout, sk_layout.cuh), logical
 // stats, staging.  Whole CTA.  src_k/src_v point at the stream's first new
@@ -52,17 +70,7 @@ __device__ void append_page(const PoolView& pv, int s, int p, int n0, int n1, co
   // done -- so no two CTAs of one launch touch staging unordered.
   const int p_open = n0 / P, p_last = (n1 - 1) / P;
   const bool tail_by_open = p == p_open && p_last != p_open && (n1 % P) != 0;
-  auto write_tail_from_src = [&]() {
-    T* wk = reinterpret_cast<T*>(pv.staging_ptr(s, 0));
-    T* wv = reinterpret_cast<T*>(pv.staging_ptr(s, 1));
-    const int tail0 = p_last * P;  // > n0: every tail token is new
-    for (int i = threadIdx.x; i < (n1 - tail0) * (D / vec); i += blockDim.x) {
-      const int tl = i / (D / vec), c = (i % (D / vec)) * vec;
-      const int64_t off = (int64_t)(tail0 + tl - n0) * src_ts + c;
-      *reinterpret_cast<uint4*>(wk + tl * D + c) = *reinterpret_cast<const uint4*>(src_k + off);
-      *reinterpret_cast<uint4*>(wv + tl * D + c) = *reinterpret_cast<const uint4*>(src_v + off);
-    }
-  };
+  auto write_tail_from_src = [&]() { sk::write_tail_from_src<T>(pv, s, n0, n1, src_k, src_v, src_ts); };
   if (streaming && p >= pv.sink && p < count - pv.local) {  // evicted by the end of this append
     if (tail_by_open) write_tail_from_src();
     return;

@@ -662,10 +662,22 @@ __global__ void __launch_bounds__(kDecThreads, SK_DEC_MINB) decode_kernel(const 
   UnitData<T, KIND, D, P, UT> ud;
   uint64_t* sbar = s_sbar + 2 * warp;
   uint8_t* sbuf = reinterpret_cast<uint8_t*>(s_part) + (size_t)warp * 2 * kSlotUsed;
-  // warp-wide: lane 0 bulk-copies the page slot of unit uu into buffer b
-  auto stage_unit = [&](int uu, int b) {
-    uint32_t um_;
-    const uint8_t* src = pv.slot_ptr(s, unit_page(uu, um_));
+  // the slots of the warp's units k0 .. k0+31 (unit u0 + k * ustride), lane k - k0
+  // each: one page-table round trip per 32 units instead of one per unit
+  const int u0 = u;
+  const uint8_t* lane_slot = nullptr;
+  auto fetch_slots = [&](int k0) {
+    const int ul = u0 + (k0 + lane) * ustride;
+    if (ul < NU) {
+      const int pi = ul / UPP;
+      lane_slot = pv.slot_ptr(s, pi < nsel ? s_sel[pi] : w_extra[pi - nsel]);
+    }
+  };
+  // warp-wide: lane 0 bulk-copies the page slot of the warp's k-th unit into buffer b
+  auto stage_unit = [&](int k, int b) {
+    if ((k & 31) == 0) fetch_slots(k);
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(
+        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(lane_slot), k & 31));
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the warp's reads of b precede the copy
       mbar_arrive_expect_tx(sbar + b, kSlotUsed);
@@ -682,8 +694,8 @@ __global__ void __launch_bounds__(kDecThreads, SK_DEC_MINB) decode_kernel(const 
       fence_barrier_init();
     }
     __syncwarp();
-    if (u < NU) stage_unit(u, 0);
-    if (u + ustride < NU) stage_unit(u + ustride, 1);
+    if (u < NU) stage_unit(0, 0);
+    if (u + ustride < NU) stage_unit(1, 1);
   } else if (u < NU) {
     pg_next = unit_page(u, um_next);
     slot_next = pv.slot_ptr(s, pg_next);  // round trip 2 (page table)
@@ -731,7 +743,7 @@ __global__ void __launch_bounds__(kDecThreads, SK_DEC_MINB) decode_kernel(const 
       unit_compute<T, KIND, D, P, UT>(ud, 0, tok_in_page, um & gmask, qw, sl2, inv_levels, st);
       if (u + 2 * ustride < NU) {
         __syncwarp();
-        stage_unit(u + 2 * ustride, b);
+        stage_unit(it + 2, b);
       }
     }
   }
