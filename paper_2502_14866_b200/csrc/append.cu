@@ -19,16 +19,19 @@ namespace sk {
 
 namespace {
 
-// code of x from the fp32 quotient, rounded to nearest-even by the 1.5 * 2^23
-// magic add (FMA pipe, no F2I / FRND); the near-tie quotients take the fp64
-// path of quant_code (the same decision rule as quant_code32).
-__device__ __forceinline__ uint32_t qcode_magic(float x, float lo32, float inv32, int levels, const double* lo64,
-                                                const double* sc64, const double* inv64, int ci) {
+// Code of x from the fp32 quotient t32 = (x - lo) * (1/scale), rounded to
+// nearest-even by the 1.5 * 2^23 magic add (FMA pipe, no F2I / FRND), branch
+// free.  t32 is within |t| * 2^-22.4 <= 2^-18.4 of numpy's fp64 quotient for
+// t <= 15 (bits <= 4), so rint(t32) is numpy's np.round unless t32 lies
+// within 2^-16 of a .5 tie; `tie` flags those (about 1 in 2^15 values) for
+// the exact fp64 path (quant_code).
+__device__ __forceinline__ uint32_t qcode_fast(float x, float lo32, float inv32, uint32_t levels, const double* lo64,
+                                               const double* sc64, const double* inv64, int ci) {
   const float t = __fmul_rn(__fsub_rn(x, lo32), inv32);
   const float r = __fadd_rn(t, 12582912.f);
   const float d = __fsub_rn(t, __fsub_rn(r, 12582912.f));
-  if (fabsf(fabsf(d) - 0.5f) < 0x1p-10f) return quant_code((double)x, lo64[ci], sc64[ci], inv64[ci], levels);
-  return min(__float_as_uint(r) & 0xFFu, (uint32_t)levels);
+  if (fabsf(fabsf(d) - 0.5f) < 0x1p-16f) return quant_code((double)x, lo64[ci], sc64[ci], inv64[ci], (int)levels);
+  return min(__float_as_uint(r) & 0xFFu, levels);
 }
 
 // Full-page fast path of the bulk append: a KV4 (bits <= 4) page of 64 new
@@ -67,6 +70,7 @@ __device__ void append_full_kv4(const PoolView& pv, int s, int p, const T* __res
   double* sc64 = lo64 + 256;
   double* inv64 = sc64 + 256;
 
+  uint8_t* slot = pv.slot_ptr(s, p);  // issued early: read after two barriers
   // 1. raw K / V pairs: 16 x 4 bytes each per thread (a warp instruction reads
   //    eight 16-byte runs of two token rows; the sl instructions share sectors in L1)
   uint32_t kr[4][4], vr[4][4];
@@ -142,7 +146,6 @@ __device__ void append_full_kv4(const PoolView& pv, int s, int p, const T* __res
   }
   __syncthreads();
   // 4. one thread per (which, q): bounds -> the page slot, quantiser tables
-  uint8_t* slot = pv.slot_ptr(s, p);
   {
     const int which = tid >> 7, q = tid & 127, mq = q >> 3, sl = (q & 7) >> 1, x = q & 1;
     const uint4* b = which ? vb : kb;
@@ -164,9 +167,11 @@ __device__ void append_full_kv4(const PoolView& pv, int s, int p, const T* __res
     inv64[tid] = 1.0 / sc;
   }
   __syncthreads();
-  // 5. K words: token t_i, (j = m%4, w = m/4), slot sl = the pair's dim / 8
+  // 5. codes (near-ties through the exact fp64 path, about 1 value in 2^15)
   uint32_t* kw = reinterpret_cast<uint32_t*>(pv.k_codes(slot));
   uint32_t* vw = reinterpret_cast<uint32_t*>(pv.v_codes(slot));
+  const uint32_t lv = (uint32_t)levels;
+  uint32_t kword[4], pw[4][2];
   {
     float l[8], iv[8];
 #pragma unroll
@@ -174,43 +179,45 @@ __device__ void append_full_kv4(const PoolView& pv, int s, int p, const T* __res
       l[k] = lo32[8 * m + k];
       iv[k] = inv32[8 * m + k];
     }
+    int CB = 8 * m;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       uint32_t word = 0;
 #pragma unroll
       for (int sl = 0; sl < 4; ++sl) {
         const float2 x = DT<T>::to_f2(kr[i][sl]);
-        const uint32_t c0 = qcode_magic(x.x, l[2 * sl], iv[2 * sl], levels, lo64, sc64, inv64, 8 * m + 2 * sl);
-        const uint32_t c1 = qcode_magic(x.y, l[2 * sl + 1], iv[2 * sl + 1], levels, lo64, sc64, inv64, 8 * m + 2 * sl + 1);
-        word |= (c0 << (4 * sl)) | (c1 << (16 + 4 * sl));
+        word |= (qcode_fast(x.x, l[2 * sl], iv[2 * sl], lv, lo64, sc64, inv64, CB + 2 * sl) << (4 * sl)) |
+                (qcode_fast(x.y, l[2 * sl + 1], iv[2 * sl + 1], lv, lo64, sc64, inv64, CB + 2 * sl + 1) << (16 + 4 * sl));
       }
-      kw[(32 * w + 8 * i + 2 * j + e) * 16 + (m & 3) * 4 + (m >> 2)] = word;
+      kword[i] = word;
     }
-  }
-  // 6. V words: channel (sl, x) of this thread, tokens t_i -> slot i, e; the
-  //    lane^16 partner holds the other e
-  {
-    float l[8], iv[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       l[k] = lo32[128 + 8 * m + k];
       iv[k] = inv32[128 + 8 * m + k];
     }
+    CB = 128 + 8 * m;
 #pragma unroll
     for (int sl = 0; sl < 4; ++sl) {
-      uint32_t pw[2] = {0u, 0u};
+      pw[sl][0] = pw[sl][1] = 0u;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float2 x = DT<T>::to_f2(vr[i][sl]);
-        pw[0] |= qcode_magic(x.x, l[2 * sl], iv[2 * sl], levels, lo64, sc64, inv64, 128 + 8 * m + 2 * sl) << (4 * i + 16 * e);
-        pw[1] |= qcode_magic(x.y, l[2 * sl + 1], iv[2 * sl + 1], levels, lo64, sc64, inv64, 128 + 8 * m + 2 * sl + 1)
-                 << (4 * i + 16 * e);
+        pw[sl][0] |= qcode_fast(x.x, l[2 * sl], iv[2 * sl], lv, lo64, sc64, inv64, CB + 2 * sl) << (4 * i + 16 * e);
+        pw[sl][1] |= qcode_fast(x.y, l[2 * sl + 1], iv[2 * sl + 1], lv, lo64, sc64, inv64, CB + 2 * sl + 1) << (4 * i + 16 * e);
       }
-      pw[0] |= __shfl_xor_sync(0xffffffffu, pw[0], 16);
-      pw[1] |= __shfl_xor_sync(0xffffffffu, pw[1], 16);
-      const int c = dbase + 8 * sl + e;  // lane e stores channel x = e
-      vw[((c >> 3) * 32 + 4 * (c & 7) + j) * 2 + w] = pw[e];
     }
+  }
+  // K word (t_i, j = m%4, w = m/4); V words: the lane^16 partner holds the other
+  // token parity e, lane e stores channel dbase + 8 sl + e
+#pragma unroll
+  for (int i = 0; i < 4; ++i) kw[(32 * w + 8 * i + 2 * j + e) * 16 + (m & 3) * 4 + (m >> 2)] = kword[i];
+#pragma unroll
+  for (int sl = 0; sl < 4; ++sl) {
+    const uint32_t a = pw[sl][0] | __shfl_xor_sync(0xffffffffu, pw[sl][0], 16);
+    const uint32_t b = pw[sl][1] | __shfl_xor_sync(0xffffffffu, pw[sl][1], 16);
+    const int c = dbase + 8 * sl + e;
+    vw[((c >> 3) * 32 + 4 * (c & 7) + j) * 2 + w] = e ? b : a;
   }
 }
 
