@@ -14,24 +14,72 @@
 #ifndef SK_APPEND_FAST  // 0: every page through the generic rebuild (A/B builds)
 #define SK_APPEND_FAST 1
 #endif
+#ifndef SK_APPEND_MINB  // resident CTAs per SM the bulk kernel is compiled for
+#define SK_APPEND_MINB 3
+#endif
 
 namespace sk {
 
 namespace {
 
 // Code of x from the fp32 quotient t32 = (x - lo) * (1/scale), rounded to
-// nearest-even by the 1.5 * 2^23 magic add (FMA pipe, no F2I / FRND), branch
-// free.  t32 is within |t| * 2^-22.4 <= 2^-18.4 of numpy's fp64 quotient for
+// nearest-even by the 1.5 * 2^23 magic add (FMA pipe, no F2I / FRND).
+// t32 is within |t| * 2^-22.4 <= 2^-18.4 of numpy's fp64 quotient for
 // t <= 15 (bits <= 4), so rint(t32) is numpy's np.round unless t32 lies
-// within 2^-16 of a .5 tie; `tie` flags those (about 1 in 2^15 values) for
-// the exact fp64 path (quant_code).
-__device__ __forceinline__ uint32_t qcode_fast(float x, float lo32, float inv32, uint32_t levels, const double* lo64,
-                                               const double* sc64, const double* inv64, int ci) {
-  const float t = __fmul_rn(__fsub_rn(x, lo32), inv32);
-  const float r = __fadd_rn(t, 12582912.f);
-  const float d = __fsub_rn(t, __fsub_rn(r, 12582912.f));
-  if (fabsf(fabsf(d) - 0.5f) < 0x1p-16f) return quant_code((double)x, lo64[ci], sc64[ci], inv64[ci], (int)levels);
-  return min(__float_as_uint(r) & 0xFFu, levels);
+// within 2^-16 of a .5 tie; those (about 1 in 2^15 values) take the exact
+// fp64 path (quant_code), kept
+// out of line so the compiler cannot if-convert (predicate) its fp64
+// instructions into every value's fast path.
+__device__ __noinline__ uint32_t qcode_exact(float x, double lo, double sc, double inv, int levels) {
+  return quant_code((double)x, lo, sc, inv, levels);
+}
+// packed fp32x2 (FADD2 / FMUL2 / FFMA2 on sm_100)
+__device__ __forceinline__ uint64_t f2p(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2u(uint64_t r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+// Codes of the two values of a T pair (channels ci, ci + 1) as n0 | n1 << 16:
+// t = (x - lo) * inv and the magic add as packed pairs, the two code bytes
+// gathered by one PRMT (byte 1 of 1.5 * 2^23 + n is zero).  A near-tie takes
+// qcode_exact.
+template <typename T>
+__device__ __forceinline__ uint32_t qpair(uint32_t raw, uint64_t nlo2, uint64_t inv2, const double* lo64,
+                                         const double* sc64, const double* inv64, int ci, int levels) {
+  const float2 x = DT<T>::to_f2(raw);
+  const uint64_t t2 = f2mul(f2add(f2p(x.x, x.y), nlo2), inv2);
+  const uint64_t r2 = f2add(t2, f2p(12582912.f, 12582912.f));
+  const float2 d = f2u(f2fma(f2add(r2, f2p(-12582912.f, -12582912.f)), f2p(-1.f, -1.f), t2));
+  const float2 r = f2u(r2);
+  const bool tie0 = fabsf(fabsf(d.x) - 0.5f) < 0x1p-16f, tie1 = fabsf(fabsf(d.y) - 0.5f) < 0x1p-16f;
+  if (tie0 || tie1) {
+    const uint32_t c0 = tie0 ? qcode_exact(x.x, lo64[ci], sc64[ci], inv64[ci], levels) : __float_as_uint(r.x) & 0xFFu;
+    const uint32_t c1 =
+        tie1 ? qcode_exact(x.y, lo64[ci + 1], sc64[ci + 1], inv64[ci + 1], levels) : __float_as_uint(r.y) & 0xFFu;
+    return c0 | (c1 << 16);
+  }
+  return __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x1410);
 }
 
 // Full-page fast path of the bulk append: a KV4 (bits <= 4) page of 64 new
@@ -170,42 +218,36 @@ __device__ void append_full_kv4(const PoolView& pv, int s, int p, const T* __res
   // 5. codes (near-ties through the exact fp64 path, about 1 value in 2^15)
   uint32_t* kw = reinterpret_cast<uint32_t*>(pv.k_codes(slot));
   uint32_t* vw = reinterpret_cast<uint32_t*>(pv.v_codes(slot));
-  const uint32_t lv = (uint32_t)levels;
   uint32_t kword[4], pw[4][2];
   {
-    float l[8], iv[8];
+    uint64_t nl[4], iv[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      l[k] = lo32[8 * m + k];
-      iv[k] = inv32[8 * m + k];
+    for (int sl = 0; sl < 4; ++sl) {
+      nl[sl] = f2p(-lo32[8 * m + 2 * sl], -lo32[8 * m + 2 * sl + 1]);
+      iv[sl] = f2p(inv32[8 * m + 2 * sl], inv32[8 * m + 2 * sl + 1]);
     }
-    int CB = 8 * m;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       uint32_t word = 0;
 #pragma unroll
-      for (int sl = 0; sl < 4; ++sl) {
-        const float2 x = DT<T>::to_f2(kr[i][sl]);
-        word |= (qcode_fast(x.x, l[2 * sl], iv[2 * sl], lv, lo64, sc64, inv64, CB + 2 * sl) << (4 * sl)) |
-                (qcode_fast(x.y, l[2 * sl + 1], iv[2 * sl + 1], lv, lo64, sc64, inv64, CB + 2 * sl + 1) << (16 + 4 * sl));
-      }
+      for (int sl = 0; sl < 4; ++sl)
+        word |= qpair<T>(kr[i][sl], nl[sl], iv[sl], lo64, sc64, inv64, 8 * m + 2 * sl, levels) << (4 * sl);
       kword[i] = word;
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      l[k] = lo32[128 + 8 * m + k];
-      iv[k] = inv32[128 + 8 * m + k];
+    for (int sl = 0; sl < 4; ++sl) {
+      nl[sl] = f2p(-lo32[128 + 8 * m + 2 * sl], -lo32[128 + 8 * m + 2 * sl + 1]);
+      iv[sl] = f2p(inv32[128 + 8 * m + 2 * sl], inv32[128 + 8 * m + 2 * sl + 1]);
     }
-    CB = 128 + 8 * m;
 #pragma unroll
     for (int sl = 0; sl < 4; ++sl) {
-      pw[sl][0] = pw[sl][1] = 0u;
+      uint32_t a = 0;  // channel x = 0 in the low half, x = 1 in the high half, token i at 4i
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 x = DT<T>::to_f2(vr[i][sl]);
-        pw[sl][0] |= qcode_fast(x.x, l[2 * sl], iv[2 * sl], lv, lo64, sc64, inv64, CB + 2 * sl) << (4 * i + 16 * e);
-        pw[sl][1] |= qcode_fast(x.y, l[2 * sl + 1], iv[2 * sl + 1], lv, lo64, sc64, inv64, CB + 2 * sl + 1) << (4 * i + 16 * e);
-      }
+      for (int i = 0; i < 4; ++i)
+        a |= qpair<T>(vr[i][sl], nl[sl], iv[sl], lo64, sc64, inv64, 128 + 8 * m + 2 * sl, levels) << (4 * i);
+      // this thread's token parity e: nibbles at 4i + 16e of each channel's word
+      pw[sl][0] = (a & 0xFFFFu) << (16 * e);
+      pw[sl][1] = (a >> 16) << (16 * e);
     }
   }
   // K word (t_i, j = m%4, w = m/4); V words: the lane^16 partner holds the other
@@ -222,7 +264,7 @@ __device__ void append_full_kv4(const PoolView& pv, int s, int p, const T* __res
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256, 2) append_kernel(PoolView pv, const T* __restrict__ k_src,
+__global__ void __launch_bounds__(256, SK_APPEND_MINB) append_kernel(PoolView pv, const T* __restrict__ k_src,
                                                         const T* __restrict__ v_src, int64_t src_ss, int64_t src_ts,
                                                         const int32_t* __restrict__ tokens, int m) {
   extern __shared__ __align__(16) uint8_t smem[];
