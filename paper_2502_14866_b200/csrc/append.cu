@@ -14,6 +14,9 @@
 #ifndef SK_APPEND_FAST  // 0: every page through the generic rebuild (A/B builds)
 #define SK_APPEND_FAST 1
 #endif
+#ifndef SK_APPEND_SFIRST
+#define SK_APPEND_SFIRST 1
+#endif
 #ifndef SK_APPEND_MINB  // resident CTAs per SM the bulk kernel is compiled for
 #define SK_APPEND_MINB 3
 #endif
@@ -90,9 +93,28 @@ __device__ __forceinline__ uint32_t qpair(uint32_t raw, uint64_t nlo2, uint64_t 
 // nibble of the K word (t_i, j = m%4, w = m/4) and, with its lane^16 partner,
 // the V words (channel, j, w) of its eight channels (sk_layout.cuh).  Only the
 // per-channel min / max reductions go through shared memory.
+// 1. raw K / V pairs, 16 x 4 bytes each per thread (a warp instruction reads
+//    eight 16-byte runs of two token rows; the sl instructions share sectors in L1)
 template <typename T>
-__device__ void append_full_kv4(const PoolView& pv, int s, int p, const T* __restrict__ src_k,
-                                const T* __restrict__ src_v, int64_t src_ts, int tok0, uint8_t* smem) {
+__device__ __forceinline__ void load_full_kv4(const T* __restrict__ src_k, const T* __restrict__ src_v, int64_t src_ts,
+                                              int tok0, uint32_t (&kr)[4][4], uint32_t (&vr)[4][4]) {
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int w = wq >> 2, j = wq & 3, m = lane & 15, e = lane >> 4;
+  const int dbase = 32 * (m >> 2) + 2 * (m & 3);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t off = (int64_t)(tok0 + 32 * w + 8 * i + 2 * j + e) * src_ts + dbase;
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl) {
+      kr[i][sl] = __ldg(reinterpret_cast<const uint32_t*>(src_k + off + 8 * sl));
+      vr[i][sl] = __ldg(reinterpret_cast<const uint32_t*>(src_v + off + 8 * sl));
+    }
+  }
+}
+
+template <typename T>
+__device__ void append_full_kv4(const PoolView& pv, int s, int p, const uint32_t (&kr)[4][4],
+                                const uint32_t (&vr)[4][4], uint8_t* smem) {
   constexpr int D = 128;
   using H2 = typename std::conditional<std::is_same<T, __half>::value, __half2, __nv_bfloat162>::type;
   auto hmin = [](uint32_t a, uint32_t b) {
@@ -119,18 +141,6 @@ __device__ void append_full_kv4(const PoolView& pv, int s, int p, const T* __res
   double* inv64 = sc64 + 256;
 
   uint8_t* slot = pv.slot_ptr(s, p);  // issued early: read after two barriers
-  // 1. raw K / V pairs: 16 x 4 bytes each per thread (a warp instruction reads
-  //    eight 16-byte runs of two token rows; the sl instructions share sectors in L1)
-  uint32_t kr[4][4], vr[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t off = (int64_t)(tok0 + 32 * w + 8 * i + 2 * j + e) * src_ts + dbase;
-#pragma unroll
-    for (int sl = 0; sl < 4; ++sl) {
-      kr[i][sl] = __ldg(reinterpret_cast<const uint32_t*>(src_k + off + 8 * sl));
-      vr[i][sl] = __ldg(reinterpret_cast<const uint32_t*>(src_v + off + 8 * sl));
-    }
-  }
   // 2. per-thread min / max: K per logical page h (tokens i = 2h, 2h+1), V over
   //    all four tokens; then across e (lane ^ 16)
   uint32_t kmn[2][4], kmx[2][4], vmn[4], vmx[4];
@@ -266,27 +276,49 @@ __device__ void append_full_kv4(const PoolView& pv, int s, int p, const T* __res
 template <typename T>
 __global__ void __launch_bounds__(256, SK_APPEND_MINB) append_kernel(PoolView pv, const T* __restrict__ k_src,
                                                         const T* __restrict__ v_src, int64_t src_ss, int64_t src_ts,
-                                                        const int32_t* __restrict__ tokens, int m) {
+                                                        const int32_t* __restrict__ tokens, int m, int sfirst) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int s = blockIdx.y;
+  // sfirst: streams fastest, so the CTAs that run together read the same token
+  // rows of the [token][stream][D] source -- whole DRAM rows at a time
+  const int s = sfirst ? blockIdx.x : blockIdx.y;
+  const int pi = sfirst ? blockIdx.y : blockIdx.x;  // page of this launch
+  const T* sk_ = k_src + s * src_ss;
+  const T* sv_ = v_src + s * src_ss;
+  const bool fast = SK_APPEND_FAST && pv.bits >= 1 && pv.bits <= 4 && pv.D == 128 && pv.P == 64 && pv.L == 16;
+  if (fast && (pi + 1) * 64 <= m) {
+    // a bulk append usually starts on a page boundary: load the page's raw
+    // tokens assuming n0 % 64 == 0 while the token count is still in flight
+    uint32_t kr[4][4], vr[4][4];
+    load_full_kv4<T>(sk_, sv_, src_ts, pi * 64, kr, vr);
+    const int n0 = tokens[s];
+    if (n0 % 64 == 0) {
+      const int n1 = n0 + m, p = n0 / 64 + pi;
+      const int count = (n1 + 63) / 64;
+      const bool evicted = pv.kind[s] == SK_KIND_STREAMING && p >= pv.sink && p < count - pv.local;
+      // a partial last page's tail is written to staging by the open page's CTA
+      if (pi == 0 && (n1 - 1) / 64 != p && (n1 % 64) != 0) write_tail_from_src<T>(pv, s, n0, n1, sk_, sv_, src_ts);
+      if (!evicted) append_full_kv4<T>(pv, s, p, kr, vr, smem);
+      return;
+    }
+  }
   const int n0 = tokens[s];
   const int n1 = n0 + m;
-  const int p = n0 / pv.P + blockIdx.x;
+  const int p = n0 / pv.P + pi;
   if (p > (n1 - 1) / pv.P) return;
   const int t0 = p * pv.P;
-  if (SK_APPEND_FAST && pv.bits >= 1 && pv.bits <= 4 && pv.D == 128 && pv.P == 64 && pv.L == 16 && t0 >= n0 &&
-      t0 + 64 <= n1) {
-    const bool streaming = pv.kind[s] == SK_KIND_STREAMING;
-    const int count = (n1 + pv.P - 1) / pv.P;
-    const bool evicted = streaming && p >= pv.sink && p < count - pv.local;
-    // a partial last page's tail is written to staging by the open page's CTA
-    const int p_open = n0 / pv.P, p_last = (n1 - 1) / pv.P;
-    if (p == p_open && p_last != p_open && (n1 % pv.P) != 0)
-      write_tail_from_src<T>(pv, s, n0, n1, k_src + s * src_ss, v_src + s * src_ss, src_ts);
-    if (!evicted) append_full_kv4<T>(pv, s, p, k_src + s * src_ss, v_src + s * src_ss, src_ts, t0 - n0, smem);
+  if (fast && t0 >= n0 && t0 + 64 <= n1) {  // a full page of new tokens after an unaligned start
+    const int count = (n1 + 63) / 64;
+    const bool evicted = pv.kind[s] == SK_KIND_STREAMING && p >= pv.sink && p < count - pv.local;
+    const int p_open = n0 / 64, p_last = (n1 - 1) / 64;
+    if (p == p_open && p_last != p_open && (n1 % 64) != 0) write_tail_from_src<T>(pv, s, n0, n1, sk_, sv_, src_ts);
+    if (!evicted) {
+      uint32_t kr[4][4], vr[4][4];
+      load_full_kv4<T>(sk_, sv_, src_ts, t0 - n0, kr, vr);
+      append_full_kv4<T>(pv, s, p, kr, vr, smem);
+    }
     return;
   }
-  append_page<T>(pv, s, p, n0, n1, k_src + s * src_ss, v_src + s * src_ss, src_ts, smem);
+  append_page<T>(pv, s, p, n0, n1, sk_, sv_, src_ts, smem);
 }
 
 // One new token per stream (decode), for up to kMaxAppendLayers pools of one
@@ -384,15 +416,16 @@ int append_launch(const sk_pool* pool, int n_streams, const void* k_src, const v
                               : append_one_launch<__nv_bfloat16>(a, 1, n_streams, sm, st);
   }
   size_t smem = append_smem_bytes(pv.D, pv.P);
-  dim3 grid(max_pages_touched, n_streams);
+  const int sfirst = SK_APPEND_SFIRST && max_pages_touched <= 65535;
+  dim3 grid = sfirst ? dim3(n_streams, max_pages_touched) : dim3(max_pages_touched, n_streams);
   if (pv.dtype == SK_F16) {
     cudaFuncSetAttribute(append_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     append_kernel<__half><<<grid, 256, smem, st>>>(pv, (const __half*)k_src, (const __half*)v_src, ss, ts,
-                                                   tokens, m);
+                                                   tokens, m, sfirst);
   } else {
     cudaFuncSetAttribute(append_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     append_kernel<__nv_bfloat16><<<grid, 256, smem, st>>>(pv, (const __nv_bfloat16*)k_src,
-                                                          (const __nv_bfloat16*)v_src, ss, ts, tokens, m);
+                                                          (const __nv_bfloat16*)v_src, ss, ts, tokens, m, sfirst);
   }
   SK_CHECK_LAUNCH("append_kernel");
   advance_tokens_kernel<<<(n_streams + 255) / 256, 256, 0, st>>>(tokens, n_streams, m);
