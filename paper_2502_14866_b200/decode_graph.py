@@ -68,6 +68,8 @@ class DecodeGraph:
         self.start_tokens = tok
         self.start_per_stream = start
         self.steps_done = 0
+        self._valid = None  # cached [lo, hi) of steps the current selections cover
+        self._next_step = -1
         self.max_steps = max_steps
         cfg = self.cfg
         self.k_pages = -(-cfg.budget_tokens // cfg.physical_page)
@@ -172,21 +174,41 @@ class DecodeGraph:
             raise RuntimeError("DecodeGraph capacity exhausted; build a new one")
         cfg = self.cfg
         step = self.engines[0].decode_steps
-        select = any(not (st is not None and st.valid_for(step, cfg.budget_tokens, cfg.reuse_interval))
-                     for e in self.engines for kv, st in [(kv, e.selection_states.get(kv))
-                                                            for kv in e.cache.dense_pool if e._row_mask_host[kv]])
+        if step != self._next_step:  # the engines were stepped outside this runner: rescan their states
+            self._valid = None
+        self._next_step = step + 1
+        if self._valid is None:  # steps [lo, hi) every stream's selection state covers
+            lo, hi = -1, -1
+            states = [e.selection_states.get(kv) for e in self.engines for kv in e.cache.dense_pool
+                      if e._row_mask_host[kv]]
+            if all(st is not None and st.budget_tokens == cfg.budget_tokens and
+                   st.reuse_interval == cfg.reuse_interval for st in states):
+                lo = max((st.chunk_start_step for st in states), default=0)
+                hi = min((st.chunk_start_step + cfg.reuse_interval for st in states), default=1 << 62)
+            self._valid = (lo, hi)
+        select = not (self._valid[0] <= step < self._valid[1])
         self.graphs[select].replay()
+        # host bookkeeping (overlaps the replay): mirrors Engine.decode_step
         n_tok = self.start_tokens + self.steps_done
         n_pages = -(-n_tok // cfg.physical_page)
-        pages_of = [-(-(t + self.steps_done) // cfg.physical_page) for t in self.start_per_stream]
+        if select:
+            from .selector import SelectionState
+            self._valid = (step, step + cfg.reuse_interval)
+            pg = cfg.physical_page
+            sizes = [selection_size(-(-(t + self.steps_done) // pg), self.k_pages) for t in self.start_per_stream]
         for e, pool in zip(self.engines, self.pools):
             if select:
-                from .selector import SelectionState
+                states = e.selection_states
                 for kv in e.cache.dense_pool:
                     if e._row_mask_host[kv]:
-                        size = selection_size(pages_of[kv], self.k_pages)
-                        e.selection_states[kv] = SelectionState(_Sized(size), step, cfg.reuse_interval,
-                                                                cfg.budget_tokens)
+                        st = states.get(kv)
+                        if isinstance(st, SelectionState) and isinstance(st.selected_pages, _Sized):
+                            st.selected_pages._n = sizes[kv]  # this runner's own state: refresh in place
+                            st.chunk_start_step = step
+                            st.reuse_interval, st.budget_tokens = cfg.reuse_interval, cfg.budget_tokens
+                        else:
+                            states[kv] = SelectionState(_Sized(sizes[kv]), step, cfg.reuse_interval,
+                                                        cfg.budget_tokens)
                         e.ledger.record_selector(kv)
             if self.record_ledger:
                 for hh, prof in enumerate(e.profiles):
@@ -197,8 +219,7 @@ class DecodeGraph:
                         vis = sum(b - a for a, b in lambda_segments(n_pages, prof.sink_blocks, prof.local_blocks,
                                                                      n_pages - 1))
                     e.ledger.record_tiles(DECODE, hh, vis, n_pages)
-            for s in range(pool.n_streams):
-                pool.tokens_host[s] += 1
+            pool.tokens_host[:] = [t + 1 for t in pool.tokens_host]
             e.decode_steps += 1
         self.steps_done += 1
         return self.out

@@ -25,7 +25,7 @@ for _ in range(L):
         k = torch.randn((ctx, HKV, D), generator=g, device="cuda", dtype=torch.float16)
         ly.load_context(b, k, k)
     layers.append(ly)
-dg = DecodeGraph(layers, 68, D, record_ledger=False)
+dg = DecodeGraph(layers, 72, D, record_ledger=False)
 dg.q.normal_(generator=g)
 dg.k.normal_(generator=g)
 dg.v.normal_(generator=g)
@@ -33,7 +33,7 @@ for _ in range(4):
     dg.step()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 ts = []
-for _ in range(32):
+for _ in range(28):
     flush.zero_()
     torch.cuda.synchronize()
     a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -43,3 +43,13 @@ for _ in range(32):
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b_) * 1e3)
 print(f"batched decode {B} x {ctx}, {L} layers: {statistics.mean(ts):.1f} us/step ({statistics.mean(ts) / L:.2f} us/layer)")
+# host-side cost of DecodeGraph.step (bookkeeping after the replay is enqueued)
+import time
+hs = []
+for _ in range(16):
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    dg.step()
+    hs.append((time.perf_counter() - t) * 1e6)
+torch.cuda.synchronize()
+print(f"host time per step() call: mean {statistics.mean(hs):.0f} us, max {max(hs):.0f} us")
