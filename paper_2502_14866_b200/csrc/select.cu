@@ -942,9 +942,13 @@ int select_launch(const SelParams& p0, int n_streams, int max_pages, cudaStream_
   SelParams p = p0;
   const int LP = p.pv.P / p.pv.L;
   const int n_tiles = (max_pages * LP + 15) / 16;
-  // ~2 CTAs per SM in total: each warp streams tiles_per_warp tiles (8 KB each)
+  // ~2 CTAs per SM in total, as c equal chunks per stream (c = 2 SMs / streams,
+  // so the grid is one wave: cfg4's 128 streams take 2 chunks each, 256 CTAs,
+  // not 3 uneven ones spilling into a second wave); each warp streams
+  // tiles_per_warp tiles (8 KB each)
   const int sms = device_sm_count();
-  int tpw = (int)(((int64_t)n_streams * n_tiles + (int64_t)kWarps * 2 * sms - 1) / ((int64_t)kWarps * 2 * sms));
+  const int chunks = 2 * sms / n_streams > 1 ? 2 * sms / n_streams : 1;
+  int tpw = (n_tiles + kWarps * chunks - 1) / (kWarps * chunks);
   tpw = tpw < 1 ? 1 : tpw;
   if (LP > 16) tpw = (tpw + LP / 16 - 1) / (LP / 16) * (LP / 16);  // a page's tiles stay in one warp
   p.tiles_per_warp = tpw;
