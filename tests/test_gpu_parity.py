@@ -316,3 +316,61 @@ def test_decode_appends_bit_exact_across_formats(bits):
             np.testing.assert_array_equal(st.k_min, kmin)
             np.testing.assert_array_equal(st.k_max, kmax)
             assert st.covered_tokens == cov
+
+
+def _tie_grid(rng, shape):
+    """Values on a 1/8 grid in [-2, 2] with both ends present per channel:
+    (x - lo) / scale hits exact .5 ties (x = 0 -> 7.5 for 4-bit codes)."""
+    x = rng.integers(-16, 17, shape).astype(np.float32) / 8.0
+    x[0], x[1] = -2.0, 2.0
+    return x
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16], ids=["f16", "bf16"])
+@pytest.mark.parametrize("dist", ["normal", "wide", "ties"])
+@pytest.mark.parametrize("bits", [4, 2])
+def test_bulk_append_pages_bit_exact(dtype, dist, bits):
+    """K1's full-page fast path (KV<=4, D 128, page 64) and the generic
+    rebuild, through load_context (page-aligned start) and a chunk appended
+    at an unaligned start: every page's codes, scale/zero and logical stats
+    equal the oracle's -- including exact .5 ties (round half to even) and
+    wide-range values."""
+    rng = np.random.default_rng(hash((str(dtype), dist, bits)) % 2**32)
+    s, n2, h, h_kv, d = 1000, 300, 8, 2, 128
+
+    def vals(*shape):
+        if dist == "normal":
+            x = rng.standard_normal(shape).astype(np.float32)
+        elif dist == "wide":
+            x = (rng.choice([-1, 1], shape) * np.exp2(rng.uniform(-12, 12, shape))).astype(np.float32)
+        else:
+            x = _tie_grid(rng, shape)
+        return torch.from_numpy(x).to(dtype).float().numpy()
+
+    gates = [0.9, 0.1, 0.8, 0.2, 0.05, 0.15, 0.12, 0.11]  # kv 1 all-streaming -> ring pool
+    kw = dict(quant_bits=bits, budget_tokens=384, reuse_interval=3, local_blocks=2)
+    prof = sk.classify_heads(gates, 0.75, 1, 2)
+    k, v = vals(s, h_kv, d), vals(s, h_kv, d)
+    eng = sk.Engine(sk.EngineConfig(**kw), prof, device="cuda:0", dtype=dtype)
+    eng.load_context(torch.from_numpy(k).to(dtype).cuda(), torch.from_numpy(v).to(dtype).cuda())
+    ref = O.OracleEngine(O.Config(**kw), O.assign_roles(gates, 0.75, 1, 2))
+    ref.load_context(k, v)
+    q2 = torch.from_numpy(rng.standard_normal((n2, h, d)).astype(np.float32)).to(dtype).float().numpy()
+    k2, v2 = vals(n2, h_kv, d), vals(n2, h_kv, d)
+    eng.prefill_chunk(sk.Workload(*(torch.from_numpy(a).to(dtype).cuda() for a in (q2, k2, v2))))
+    ref.prefill_chunk(q2, k2, v2)
+    mine = [(1, kv, pg) for kv in sorted(eng.cache.dense_pool) for pg in eng.cache.dense_pool[kv].live_pages()] + \
+           [(0, kv, pg) for kv in sorted(eng.cache.streaming_pool) for pg in eng.cache.streaming_pool[kv].live_pages()]
+    theirs = _oracle_pages(ref.pools)
+    assert [(a, b, c.page_id, c.token_count) for a, b, c in mine] == \
+        [(a, b, c.index, c.tokens) for a, b, c in theirs]
+    for (_, _, pg), (_, _, rp) in zip(mine, theirs):
+        t = pg.token_count
+        np.testing.assert_array_equal(pg.k_codes[:t], rp.k_codes[:t])
+        np.testing.assert_array_equal(pg.v_codes[:t], rp.v_codes[:t])
+        for name in ("k_scale", "k_zero", "v_scale", "v_zero"):
+            np.testing.assert_array_equal(getattr(pg, name), getattr(rp, name))
+        for st, (kmin, kmax, cov) in zip(pg.stats, rp.bounds):
+            np.testing.assert_array_equal(st.k_min, kmin)
+            np.testing.assert_array_equal(st.k_max, kmax)
+            assert st.covered_tokens == cov
