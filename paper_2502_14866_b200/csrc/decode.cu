@@ -169,30 +169,27 @@ __device__ __forceinline__ float2 unpack2(uint32_t w) {
   else return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w));
 }
 
-// nibble word -> fp16x2 register `slot` (exact integers 0..15)
-// (slot is a compile-time constant after unrolling).  Even slots take the
-// low nibble of each 16-bit half: LOP3 into the 1024 + n fp16 pattern, then
-// subtract 1024.  Odd slots take the high nibble in place -- 1024 + 16 n --
-// and one HFMA2 (x/16 - 64) recovers n, so a word costs 1 shift (shared by
-// slots 2 and 3), 4 LOP3 and 4 half2 ops.  Every value is exact in fp16.
+// Code word -> fp16x2 MMA operand, with NO conversion arithmetic: the codes
+// are used as fp16 SUBNORMALS (the tensor cores multiply subnormal fp16
+// operands exactly; every product and partial sum stays a normal fp32).
+// Nibble slot 0/2 (bits 0-3 / 8-11 of each 16-bit half) masks to n * 2^-24,
+// slot 1/3 (bits 4-7 / 12-15) to 16 n * 2^-24 in place, so a word costs one
+// shift (shared by slots 2 and 3) and four single-immediate LOP3s; the odd
+// slots feed the MMA's second k-half (a2/a3), whose B operand carries the
+// matching 1/16, and the accumulator is scaled back by 2^24 (kCodeUnscale).
+// Round 2 formed exact fp16 integers (LOP3 into 1024 + n, then HSUB2/HFMA2):
+// ptxas splits that LOP3 in two (one immediate per instruction), so a word
+// cost 13 instructions instead of 5 (ncu, cfg4 K3: 27% of all instructions
+// were LOP3, 14% HADD2).
+constexpr float kCodeUnscale = 16777216.f;  // 2^24
+constexpr float kOddSlot = 0.0625f;         // 1/16 on the B operand of the odd nibble slots
 __device__ __forceinline__ uint32_t nib2h(uint32_t w, int slot) {
   const uint32_t x = slot >= 2 ? (w >> 8) : w;
-  uint32_t y;
-  if (slot & 1) {
-    y = (x & 0x00F000F0u) | 0x64006400u;
-    __half2 h = __hfma2(*reinterpret_cast<__half2*>(&y), __half2half2(__ushort_as_half(0x2C00)),   // 1/16
-                        __half2half2(__ushort_as_half(0xD400)));                                     // -64
-    return *reinterpret_cast<uint32_t*>(&h);
-  }
-  y = (x & 0x000F000Fu) | 0x64006400u;
-  __half2 h = __hsub2(*reinterpret_cast<__half2*>(&y), __half2half2(__ushort_as_half(0x6400)));   // -1024
-  return *reinterpret_cast<uint32_t*>(&h);
+  return x & ((slot & 1) ? 0x00F000F0u : 0x000F000Fu);
 }
-// byte pair (r2 = 0: bytes 0,1; r2 = 1: bytes 2,3) -> fp16x2 exact integers 0..255
+// byte pair (r2 = 0: bytes 0,1; r2 = 1: bytes 2,3) -> fp16x2 subnormals b * 2^-24
 __device__ __forceinline__ uint32_t byte2h(uint32_t w, int r2) {
-  uint32_t x = __byte_perm(w, 0x64u, r2 ? 0x4342 : 0x4140);  // {b, 0x64, b', 0x64}
-  __half2 h = __hsub2(*reinterpret_cast<__half2*>(&x), __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400)));
-  return *reinterpret_cast<uint32_t*>(&h);
+  return __byte_perm(w, 0u, r2 ? 0x4342 : 0x4140);  // {b, 0, b', 0}
 }
 
 __device__ __forceinline__ uint4 ldg16(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
@@ -391,16 +388,24 @@ __device__ __forceinline__ void unit_compute(const UnitData<T, KIND, D, P, UT>& 
     qz += __shfl_xor_sync(0xffffffffu, qz, 1);
     qz += __shfl_xor_sync(0xffffffffu, qz, 2);  // qz of row g
     smax = mx;
-    const float inv = 1.f / mx;
+    const float inv = 1.f / mx, inv1 = KIND == 1 ? inv * kOddSlot : inv;  // k-half 1 = odd nibble slots
 #pragma unroll
     for (int ks = 0; ks < NKS; ++ks) {
       const float2 q0 = DT<T>::to_f2(qw[2 * ks]), q1 = DT<T>::to_f2(qw[2 * ks + 1]);
       bq[ks][0] = pack2<MT>(q0.x * (sk[4 * ks] * inv), q0.y * (sk[4 * ks + 1] * inv));
-      bq[ks][1] = pack2<MT>(q1.x * (sk[4 * ks + 2] * inv), q1.y * (sk[4 * ks + 3] * inv));
+      bq[ks][1] = pack2<MT>(q1.x * (sk[4 * ks + 2] * inv1), q1.y * (sk[4 * ks + 3] * inv1));
     }
   }
   // the S^T accumulator holds rows 2j, 2j+1: fetch their qz from lanes 8j, 8j+4
   const float qz0 = __shfl_sync(0xffffffffu, qz, 8 * j), qz1 = __shfl_sync(0xffffffffu, qz, 8 * j + 4);
+
+  // codes enter the MMA as subnormals: undo their 2^-24 with the page scale
+  // (fp16 scales cannot overflow by it; bf16 ones keep a separate exact multiply)
+  float smax_u = smax;
+  if constexpr (KIND != 0) {
+    if constexpr (std::is_same<T, __half>::value) smax_u = smax * kCodeUnscale;
+  }
+  constexpr float kAccU = (KIND != 0 && !std::is_same<T, __half>::value) ? kCodeUnscale : 1.f;
 
   // ---- S^T = K q'^T: tile i gives tokens 16(tt0+i) + g (+8), rows 2j, 2j+1 ---------
   float sc[TT][4];
@@ -429,11 +434,15 @@ __device__ __forceinline__ void unit_compute(const UnitData<T, KIND, D, P, UT>& 
       }
       mma16816_full<MT>(c, a0, a1, a2, a3, bq[ks][0], bq[ks][1]);
     }
+    if constexpr (kAccU != 1.f) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) c[e] *= kAccU;
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const bool ok = 16 * (tt0 + i) + 8 * h + g < tok_in_page;
-      sc[i][2 * h] = ok ? (c[2 * h] * smax + qz0) * sl2 : -INFINITY;
-      sc[i][2 * h + 1] = ok ? (c[2 * h + 1] * smax + qz1) * sl2 : -INFINITY;
+      sc[i][2 * h] = ok ? (c[2 * h] * smax_u + qz0) * sl2 : -INFINITY;
+      sc[i][2 * h + 1] = ok ? (c[2 * h + 1] * smax_u + qz1) * sl2 : -INFINITY;
     }
   }
 
@@ -466,10 +475,12 @@ __device__ __forceinline__ void unit_compute(const UnitData<T, KIND, D, P, UT>& 
     for (int h = 0; h < 2; ++h) {
       const float p0 = att[0] ? fast_exp2(sc[i][2 * h] - m_new[0]) : 0.f;
       const float p1 = att[1] ? fast_exp2(sc[i][2 * h + 1] - m_new[1]) : 0.f;
-      const uint32_t pk = pack2<MT>(p0, p1);  // (token 16tt + 8h + g, rows 2j, 2j+1)
-      const float2 pr = unpack2<MT>(pk);     // the rounded values the MMA sees
-      psum[0] += pr.x;
-      psum[1] += pr.y;
+      // tokens 8..15 of the tile (h = 1) meet the odd nibble slots: P / 16 there
+      const float ps = (KIND == 1 && h == 1) ? kOddSlot : 1.f;
+      const uint32_t pk = pack2<MT>(p0 * ps, p1 * ps);  // (token 16tt + 8h + g, rows 2j, 2j+1)
+      const float2 pr = unpack2<MT>(pk);               // the rounded values the MMA sees
+      psum[0] = fmaf(pr.x, 1.f / ps, psum[0]);
+      psum[1] = fmaf(pr.y, 1.f / ps, psum[1]);
       pb[i][h] = transpose8x8(pk);
     }
   float prow[2];
@@ -518,8 +529,9 @@ __device__ __forceinline__ void unit_compute(const UnitData<T, KIND, D, P, UT>& 
         const float lo_c = (g & 1) ? lo.y : lo.x, hi_c = (g & 1) ? hi.y : hi.x;
         float sc_ = (hi_c - lo_c) * inv_levels;
         sc_ = sc_ > 0.f ? sc_ : 1.f;
-        add0 = fmaf(sc_, c[2 * h], lo_c * prow[0]);
-        add1 = fmaf(sc_, c[2 * h + 1], lo_c * prow[1]);
+        if constexpr (std::is_same<T, __half>::value) sc_ *= kCodeUnscale;  // codes were subnormals
+        add0 = fmaf(sc_, c[2 * h] * kAccU, lo_c * prow[0]);
+        add1 = fmaf(sc_, c[2 * h + 1] * kAccU, lo_c * prow[1]);
       }
       st.o[ct][2 * h] = fmaf(st.o[ct][2 * h], alpha[0], add0);
       st.o[ct][2 * h + 1] = fmaf(st.o[ct][2 * h + 1], alpha[1], add1);
