@@ -192,6 +192,29 @@ __device__ __forceinline__ uint32_t byte2h(uint32_t w, int r2) {
   return __byte_perm(w, 0u, r2 ? 0x4342 : 0x4140);  // {b, 0, b', 0}
 }
 
+// packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2 on sm_100): two lanes of
+// scale / bias work per instruction in the per-page dequantisation algebra
+__device__ __forceinline__ uint64_t x2(float x, float y) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ float2 x2f(uint64_t r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ uint64_t x2mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t x2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 __device__ __forceinline__ uint4 ldg16(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 __device__ __forceinline__ uint2 ldg8(const void* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
 // unit loads from global memory (SM = false) or from a page staged in shared
@@ -369,31 +392,37 @@ __device__ __forceinline__ void unit_compute(const UnitData<T, KIND, D, P, UT>& 
       bq[ks][1] = qw[2 * ks + 1];
     }
   } else {
-    float sk[D / 4];
+    // s_k = (hi - lo) / levels per channel; a constant channel (s_k = 0) has
+    // all-zero codes, so its scale never reaches the score
+    uint64_t qs2[D / 8];  // (q s_k) channel pairs
+    uint64_t qz2 = x2(0.f, 0.f);
     float mx = 0.f;
+    const uint64_t il2 = x2(inv_levels, inv_levels), m12 = x2(-1.f, -1.f);
 #pragma unroll
     for (int i = 0; i < D / 8; ++i) {
-      const float2 lo = DT<T>::to_f2(kb_lo[i]), hi = DT<T>::to_f2(kb_hi[i]);
-      float a = (hi.x - lo.x) * inv_levels, b = (hi.y - lo.y) * inv_levels;
-      a = a > 0.f ? a : 1.f;
-      b = b > 0.f ? b : 1.f;
-      sk[2 * i] = a;
-      sk[2 * i + 1] = b;
-      mx = fmaxf(mx, fmaxf(a, b));
-      const float2 q = DT<T>::to_f2(qw[i]);
-      qz = fmaf(q.x, lo.x, fmaf(q.y, lo.y, qz));
+      const float2 lo = DT<T>::to_f2(kb_lo[i]), hi = DT<T>::to_f2(kb_hi[i]), q = DT<T>::to_f2(qw[i]);
+      const uint64_t lo2 = x2(lo.x, lo.y), q2 = x2(q.x, q.y);
+      const uint64_t s2 = x2mul(x2fma(lo2, m12, x2(hi.x, hi.y)), il2);
+      const float2 sf = x2f(s2);
+      mx = fmax3(mx, sf.x, sf.y);
+      qs2[i] = x2mul(q2, s2);
+      qz2 = x2fma(q2, lo2, qz2);
     }
+    const float2 qzf = x2f(qz2);
+    qz = qzf.x + qzf.y;
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
     qz += __shfl_xor_sync(0xffffffffu, qz, 1);
     qz += __shfl_xor_sync(0xffffffffu, qz, 2);  // qz of row g
+    mx = mx > 0.f ? mx : 1.f;                    // every channel constant
     smax = mx;
     const float inv = 1.f / mx, inv1 = KIND == 1 ? inv * kOddSlot : inv;  // k-half 1 = odd nibble slots
+    const uint64_t i0 = x2(inv, inv), i1 = x2(inv1, inv1);
 #pragma unroll
     for (int ks = 0; ks < NKS; ++ks) {
-      const float2 q0 = DT<T>::to_f2(qw[2 * ks]), q1 = DT<T>::to_f2(qw[2 * ks + 1]);
-      bq[ks][0] = pack2<MT>(q0.x * (sk[4 * ks] * inv), q0.y * (sk[4 * ks + 1] * inv));
-      bq[ks][1] = pack2<MT>(q1.x * (sk[4 * ks + 2] * inv1), q1.y * (sk[4 * ks + 3] * inv1));
+      const float2 a = x2f(x2mul(qs2[2 * ks], i0)), b = x2f(x2mul(qs2[2 * ks + 1], i1));
+      bq[ks][0] = pack2<MT>(a.x, a.y);
+      bq[ks][1] = pack2<MT>(b.x, b.y);
     }
   }
   // the S^T accumulator holds rows 2j, 2j+1: fetch their qz from lanes 8j, 8j+4
@@ -495,6 +524,9 @@ __device__ __forceinline__ void unit_compute(const UnitData<T, KIND, D, P, UT>& 
   }
 
   // ---- O^T = alpha O^T + s_v (V^T P^T) + lo_v sum(P) -----------------------------
+  const uint64_t prow2 = x2(prow[0], prow[1]), alpha2 = x2(alpha[0], alpha[1]);
+  const uint32_t vsel = (g & 1) ? 0x7632u : 0x5410u;  // {lo, hi} halves of this lane's channel
+  const float inv_v = std::is_same<T, __half>::value ? inv_levels * kCodeUnscale : inv_levels;
 #pragma unroll
   for (int ct = 0; ct < NCT; ++ct) {
     float c[4] = {0.f, 0.f, 0.f, 0.f};
@@ -521,20 +553,17 @@ __device__ __forceinline__ void unit_compute(const UnitData<T, KIND, D, P, UT>& 
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      float add0 = c[2 * h], add1 = c[2 * h + 1];
+      uint64_t add = x2(c[2 * h], c[2 * h + 1]);
       if constexpr (KIND != 0) {
-        // channel 16ct + 8h + g: vbound index (g/2)*D/4 + 2*(2ct+h) + g%2
-        const int wi = 2 * ct + h;  // register holding (cn = 2ct+h, e = 0/1)
-        const float2 lo = DT<T>::to_f2(vb_lo[wi]), hi = DT<T>::to_f2(vb_hi[wi]);
-        const float lo_c = (g & 1) ? lo.y : lo.x, hi_c = (g & 1) ? hi.y : hi.x;
-        float sc_ = (hi_c - lo_c) * inv_levels;
-        sc_ = sc_ > 0.f ? sc_ : 1.f;
-        if constexpr (std::is_same<T, __half>::value) sc_ *= kCodeUnscale;  // codes were subnormals
-        add0 = fmaf(sc_, c[2 * h] * kAccU, lo_c * prow[0]);
-        add1 = fmaf(sc_, c[2 * h + 1] * kAccU, lo_c * prow[1]);
+        // channel 16ct + 8h + g: half g%2 of vbound words (g/2)*D/4 + 2*(2ct+h)
+        const float2 b = DT<T>::to_f2(__byte_perm(vb_lo[2 * ct + h], vb_hi[2 * ct + h], vsel));  // (lo_c, hi_c)
+        const float sc_ = (b.y - b.x) * inv_v;  // a constant channel's codes are 0: any scale
+        if constexpr (kAccU != 1.f) add = x2mul(add, x2(kAccU, kAccU));
+        add = x2fma(x2(sc_, sc_), add, x2mul(x2(b.x, b.x), prow2));
       }
-      st.o[ct][2 * h] = fmaf(st.o[ct][2 * h], alpha[0], add0);
-      st.o[ct][2 * h + 1] = fmaf(st.o[ct][2 * h + 1], alpha[1], add1);
+      const float2 o = x2f(x2fma(x2(st.o[ct][2 * h], st.o[ct][2 * h + 1]), alpha2, add));
+      st.o[ct][2 * h] = o.x;
+      st.o[ct][2 * h + 1] = o.y;
     }
   }
 }
