@@ -339,6 +339,9 @@ struct AppendLayers {
 template <typename T>
 __global__ void __launch_bounds__(256) append_one_kernel(const __grid_constant__ AppendLayers a) {
   extern __shared__ __align__(16) uint8_t smem[];
+#ifdef SK_APPEND_ONE_NOOP  // timing builds only (tools/ab_variant.sh): the decode step without its appends
+  return;
+#endif
   const int part = blockIdx.x, s = blockIdx.y, l = blockIdx.z;
   const PoolView& pv = a.pv[l];
   int32_t* tokens = a.tokens[l];
