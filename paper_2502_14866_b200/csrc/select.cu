@@ -624,21 +624,31 @@ __device__ bool topk_filtered(const SelParams& p, int s, int n, int n_log, const
   const double w2 = 2.0 * (double)emax * (1.0 + 0x1p-20);  // 2E, widened for the threshold roundings
   uint32_t kk = p.K - n_pins(n);                            // K' >= 1 here
   const uint32_t kq = kk;
-  int hi = kmax == kmin ? 0 : 32 - __clz(kmax ^ kmin);
-  uint32_t mask = hi >= 32 ? 0u : (~0u << hi);
-  uint32_t prefix = kmax & mask;
+  // Value-linear passes: bin b of [vlo, vhi] holds x with
+  // floor((x - vlo) * kNB / (vhi - vlo)) = b (double arithmetic, monotone in x),
+  // so keys spread over the bins by value -- few share a histogram counter,
+  // where the top bits of the order keys put most pages in a handful of bins.
+  // A pass finds the bin of the K'-th largest remaining candidate; the next
+  // pass splits that bin.  It stops once the bin is narrower than 2E or holds
+  // few candidates (or after 3 passes): the band [lo - 2E, hi + 2E] around it
+  // is rescored exactly whatever its width.
+  double vlo = (double)key32_value(kmin), vhi = (double)key32_value(kmax);
+  uint32_t cand = 0;  // bit j: key j still inside the current bin
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) cand |= key[j] ? (1u << j) : 0u;
+  __shared__ uint32_t sh_cnt;
+  bool done = !(vhi - vlo > w2) || !isfinite(vhi - vlo);
   int cur = 0;
-  // the bin's value range, clamped to the candidates' (no NaN/inf encodings)
-  auto bin_hi = [&]() { return (double)key32_value(min(prefix | ~mask, kmax)); };
-  auto bin_lo = [&]() { return (double)key32_value(max(prefix, kmin)); };
-  while (hi > 0 && bin_hi() - bin_lo() > w2) {
-    const int w = hi < kRadixBits ? hi : kRadixBits;
-    const int shift = hi - w;
-    const uint32_t dm = (1u << w) - 1u;
+  for (int pass = 0; pass < 3 && !done; ++pass) {
+    const double scale = (double)kNB / (vhi - vlo);
+    auto bin_of = [&](uint32_t k) -> int {
+      const int b = (int)(((double)key32_value(k) - vlo) * scale);
+      return b < 0 ? 0 : (b > kNB - 1 ? kNB - 1 : b);
+    };
     uint32_t* h = hist2 + cur * kNB;
 #pragma unroll
     for (int j = 0; j < KPT; ++j)
-      if (key[j] && (key[j] & mask) == prefix) atomicAdd(&h[(key[j] >> shift) & dm], 1u);
+      if ((cand >> j) & 1u) atomicAdd(&h[bin_of(key[j])], 1u);
     uint32_t* hn = hist2 + (cur ^ 1) * kNB;
     for (int b = tid; b < kNB; b += kThreads) hn[b] = 0;
     __syncthreads();  // A: histogram complete
@@ -666,19 +676,27 @@ __device__ bool topk_filtered(const SelParams& p, int s, int n, int n_log, const
         if (cum + loc[e] >= kk && cum < kk) {
           sh_bin = kNB - 1 - BPT * tid - e;
           sh_kk = kk - cum;
+          sh_cnt = loc[e];
         }
         cum += loc[e];
       }
     }
     __syncthreads();  // C: boundary bin published
-    prefix |= sh_bin << shift;
-    mask |= dm << shift;
+    const int bs = (int)sh_bin;
     kk = sh_kk;
-    hi = shift;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j)
+      if (((cand >> j) & 1u) && bin_of(key[j]) != bs) cand &= ~(1u << j);
+    // the bin's value range, widened by the rounding of the bin formula
+    const double w = 1.0 / scale, delta = (vhi - vlo) * 0x1p-40;
+    const double nlo = vlo + bs * w - delta, nhi = vlo + (bs + 1) * w + delta;
+    vlo = nlo;
+    vhi = nhi;
     cur ^= 1;
+    done = !(vhi - vlo > w2) || sh_cnt <= 16u;
   }
   SK_STAMP(2);
-  const double hiT = bin_hi() + w2, loT = bin_lo() - w2;
+  const double hiT = vhi + w2, loT = vlo - w2;
   uint64_t inb = 0, bnd = 0;
   uint32_t c_in = 0;
 #pragma unroll
