@@ -26,8 +26,9 @@
 //   score / max bound over its logical pages and rows: (score, err) -> ws.
 //
 // Phase B (the stream's last CTA, found with an acq_rel ticket).  With T =
-//   the K'-th largest approximate score (K' = K - |pins|, radix select on the
-//   order-preserving 32-bit image) and E = the largest bound:
+//   the K'-th largest approximate score (K' = K - |pins|, located by
+//   value-linear histogram passes over [min, max] of the approximate scores)
+//   and E = the largest bound:
 //     approx > T + 2E  -> certainly among the top K' (true score > true K'-th)
 //     approx < T - 2E  -> certainly not
 //     otherwise        -> the band: rescored EXACTLY in fp64 (the round-1
