@@ -25,8 +25,13 @@ def test_reference_suite_against_this_package():
     env = dict(os.environ)
     env["PYTHONPATH"] = os.pathsep.join([os.path.join(ROOT, "tests", "refsuite"), ROOT])
     env["PYTHONDONTWRITEBYTECODE"] = "1"
+    # A fixed hypothesis seed: the reference's own property test
+    # test_partition_is_invariant_under_monotone_transforms (test_heads.py:45)
+    # fails for the unmodified reference too on some random draws -- x / (1 + x)
+    # maps gates 0.9989999999999999 and 0.999 to one float, and the tie then
+    # goes to the lower head index -- so unseeded runs are flaky for both.
     cmd = [sys.executable, "-m", "pytest", "-q", "-p", "sparsekv_shim", "-p", "no:cacheprovider", "-rxf",
-           "--rootdir", SUITE, "-o", "addopts=", *[os.path.join(SUITE, f) for f in FILES]]
+           "--hypothesis-seed=0", "--rootdir", SUITE, "-o", "addopts=", *[os.path.join(SUITE, f) for f in FILES]]
     res = subprocess.run(cmd, cwd=SUITE, env=env, capture_output=True, text=True, timeout=1800)
     out = res.stdout + res.stderr
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
