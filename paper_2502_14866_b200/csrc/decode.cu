@@ -703,23 +703,12 @@ __global__ void __launch_bounds__(kDecThreads, SK_DEC_MINB) decode_kernel(const 
   UnitData<T, KIND, D, P, UT> ud;
   uint64_t* sbar = s_sbar + 2 * warp;
   uint8_t* sbuf = reinterpret_cast<uint8_t*>(s_part) + (size_t)warp * 2 * kSlotUsed;
-  // Staged path (one CTA per stream, whole-page units, ustride = kWarps): the
-  // warp's k-th unit is page u0 + k * kWarps for the n_full full rounds; the
-  // R = NU - kWarps * n_full tail pages would give R warps one page more than
-  // the rest (cfg4: 66 pages -> 9 vs 8), so when 2R <= kWarps they are split
-  // in halves (two 16-token tiles each), one half per warp: 8.5 pages instead of 9.
+  // the slots of the warp's units k0 .. k0+31 (unit u0 + k * ustride), lane k - k0
+  // each: one page-table round trip per 32 units instead of one per unit
   const int u0 = u;
-  const int n_full = STAGE ? NU / kWarps : 0, n_tail = STAGE ? NU - kWarps * n_full : 0;
-  const bool tail_split = 2 * n_tail <= kWarps && UPP == 1 && UT == 4;
-  const int n_it = STAGE ? n_full + (warp < (tail_split ? 2 * n_tail : n_tail) ? 1 : 0) : 0;
-  auto unit_of = [&](int k) -> int {  // staged path: union index of the warp's k-th unit
-    return k < n_full ? u0 + k * ustride : kWarps * n_full + (tail_split ? (warp >> 1) : warp);
-  };
-  // the slots of the warp's units k0 .. k0+31, lane k - k0 each: one
-  // page-table round trip per 32 units instead of one per unit
   const uint8_t* lane_slot = nullptr;
   auto fetch_slots = [&](int k0) {
-    const int ul = STAGE ? (k0 + lane < n_it ? unit_of(k0 + lane) : NU) : u0 + (k0 + lane) * ustride;
+    const int ul = u0 + (k0 + lane) * ustride;
     if (ul < NU) {
       const int pi = ul / UPP;
       lane_slot = pv.slot_ptr(s, pi < nsel ? s_sel[pi] : w_extra[pi - nsel]);
@@ -746,8 +735,8 @@ __global__ void __launch_bounds__(kDecThreads, SK_DEC_MINB) decode_kernel(const 
       fence_barrier_init();
     }
     __syncwarp();
-    if (0 < n_it) stage_unit(0, 0);
-    if (1 < n_it) stage_unit(1, 1);
+    if (u < NU) stage_unit(0, 0);
+    if (u + ustride < NU) stage_unit(1, 1);
   } else if (u < NU) {
     pg_next = unit_page(u, um_next);
     slot_next = pv.slot_ptr(s, pg_next);  // round trip 2 (page table)
@@ -786,23 +775,14 @@ __global__ void __launch_bounds__(kDecThreads, SK_DEC_MINB) decode_kernel(const 
   }
   bool first = true;
   if constexpr (STAGE) {
-    for (int it = 0; it < n_it; ++it) {
+    for (int it = 0; u < NU; u += ustride, ++it) {
       uint32_t um;
-      const int pg = unit_page(unit_of(it), um), b = it & 1;
+      const int pg = unit_page(u, um), b = it & 1;
       const int tok_in_page = min(P, n_tok - pg * P);
       mbar_wait(sbar + b, (it >> 1) & 1);
-      if (it < n_full || !tail_split) {
-        unit_load<T, KIND, D, P, UT, true>(sbuf + b * kSlotUsed, 0, ud);
-        unit_compute<T, KIND, D, P, UT>(ud, 0, tok_in_page, um & gmask, qw, sl2, inv_levels, st);
-      } else if constexpr (UT == 4) {  // half a tail page: tiles tt0, tt0 + 1
-        const int tt0 = 2 * (warp & 1);
-        if (16 * tt0 < tok_in_page) {
-          UnitData<T, KIND, D, P, 2> uh;
-          unit_load<T, KIND, D, P, 2, true>(sbuf + b * kSlotUsed, tt0, uh);
-          unit_compute<T, KIND, D, P, 2>(uh, tt0, tok_in_page, um & gmask, qw, sl2, inv_levels, st);
-        }
-      }
-      if (it + 2 < n_it) {
+      unit_load<T, KIND, D, P, UT, true>(sbuf + b * kSlotUsed, 0, ud);
+      unit_compute<T, KIND, D, P, UT>(ud, 0, tok_in_page, um & gmask, qw, sl2, inv_levels, st);
+      if (u + 2 * ustride < NU) {
         __syncwarp();
         stage_unit(it + 2, b);
       }
