@@ -389,6 +389,26 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t x, uint32_t* warp_tot, u
   return res;
 }
 
+// Exclusive scan of one value per thread in thread order with ONE barrier:
+// warp-inclusive shuffles, warp totals through shared memory, and each thread
+// adds the totals of the warps before its own.  warp_tot must not be read
+// again by the caller (no trailing barrier).
+__device__ __forceinline__ uint32_t block_scan1(uint32_t x, uint32_t* warp_tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = x;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  uint32_t base = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) base += w < warp ? warp_tot[w] : 0u;
+  return base + incl - x;
+}
+
 // ---- exact top-k (slow path): every non-pinned page scored in fp64 ------------
 // Pins, then the best K-|pins| others by (score desc, index asc), ascending.
 // Keys staged in shared memory when they fit, else re-read from the slots.
@@ -751,8 +771,7 @@ __device__ bool topk_filtered(const SelParams& p, int s, int n, int n_log, const
   uint32_t n_take = 0;
 #pragma unroll
   for (int j = 0; j < KPT; ++j) n_take += taken(j);
-  uint32_t tot;
-  uint32_t pos = block_scan(n_take, wtot, tot);
+  uint32_t pos = block_scan1(n_take, wtot);
 #pragma unroll
   for (int j = 0; j < KPT; ++j)
     if (taken(j)) sel_out[pos++] = i0 + j;
